@@ -1,0 +1,134 @@
+/*
+ * sliceprop_b200 — C ABI of the B200-native equiprop hot path.
+ *
+ * This is the drop-in boundary for the reference's propagation hot path
+ * (sliceprop 0.1.0, /root/reference/pkg/src/sliceprop).  Every entry point
+ * takes plain pointers and sizes; no torch or numpy types cross it.  The
+ * reference has no C ABI of its own (it is pure Python/numpy), so each
+ * function below cites the Python interface it replaces and the paper's
+ * Parament_* C API it is modelled on.
+ *
+ * Conventions
+ *   - complex matrices: row-major, interleaved (re, im) — numpy
+ *     complex128 / complex64 memory layout (reference linalg.py:1-13);
+ *   - amplitude tables: (pts, n_ctrl) float64 row-major, also in fp32 mode
+ *     (reference hamiltonian.py:114-129);
+ *   - time order: U = U[n-1] ... U[0], later slice on the left
+ *     (reference propagator.py:68-80);
+ *   - return value: 0 on success, else an SP_E_* code that maps 1:1 onto
+ *     the reference ErrorCode strings (errors.py:27-36) plus SP_E_INTERNAL
+ *     for CUDA failures (the reference CLI's exit code 4, cli.py:191-193);
+ *     sp_last_error() returns the message.
+ *   - a context is not thread-safe and not reentrant (PAPER.md:270,
+ *     SPEC.md:416); independent contexts may coexist.
+ */
+#ifndef SLICEPROP_B200_H
+#define SLICEPROP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes: errors.py:27-36 (+ internal) */
+enum {
+  SP_OK = 0,
+  SP_E_SHAPE = 1,            /* "shape"            */
+  SP_E_HERMITICITY = 2,      /* "hermiticity"      */
+  SP_E_AMPLITUDE_BOUND = 3,  /* "amplitude-bound"  */
+  SP_E_SAMPLING_PARITY = 4,  /* "sampling-parity"  */
+  SP_E_STEP_TOO_LARGE = 5,   /* "step-too-large"   */
+  SP_E_STATE_MACHINE = 6,    /* "state-machine"    */
+  SP_E_ALIASING = 7,         /* "aliasing"         */
+  SP_E_DOMAIN = 8,           /* "domain"           */
+  SP_E_CONFIG = 9,           /* "config"           */
+  SP_E_INTERNAL = 10         /* CUDA / NCCL / no device */
+};
+
+/* slicing modes: propagator.py:175-201, hamiltonian.py:8-14, magnus.py:1-16 */
+enum { SP_MODE_MIDPOINT = 0, SP_MODE_SIMPSON = 1, SP_MODE_MAGNUS = 2 };
+
+/* reductions: propagator.py:279-308 ("pairwise" | "sequential") */
+enum { SP_REDUCE_PAIRWISE = 0, SP_REDUCE_SEQUENTIAL = 1 };
+
+#define SP_MAX_ORDER 25
+
+/* Chebyshev plan — replaces ChebyshevPlan / make_plan (chebyshev.py:155-218). */
+typedef struct sp_plan {
+  double alpha, beta;
+  int m_max;
+  double coeffs[2 * (SP_MAX_ORDER + 1)]; /* a_k = (-i)^k J_k(span/2), interleaved */
+  double phase[2];                       /* e^{-i(alpha+beta)/2} */
+  double predicted_error;
+  double capability;                     /* filled on SP_E_STEP_TOO_LARGE */
+  double norm_bound;                     /* filled on SP_E_STEP_TOO_LARGE */
+} sp_plan;
+
+typedef struct sp_ctx sp_ctx;
+
+/* ---- host plan (CPU only; chebyshev.py:61-218) ------------------------ */
+const char* sp_version(void);
+/* J_k(x), 0<=k<=64, 0<=x<=64 (bessel_j, chebyshev.py:61-104) */
+int sp_bessel_j(int k, double x, double* out);
+/* 4 (e^{1-s^2} s)^{m+1}, s = span/(4m+4) (chebyshev_error, chebyshev.py:107-110) */
+double sp_chebyshev_error(int m, double span);
+/* smallest odd m in 3..25 (select_m_max, chebyshev.py:113-134);
+ * on SP_E_STEP_TOO_LARGE *capability holds the order-25 capability */
+int sp_select_m_max(double norm_bound, int precision_bits, int* m_out, double* capability);
+/* norm_capability, chebyshev.py:137-152 */
+int sp_norm_capability(int m, int precision_bits, double* out);
+/* make_plan, chebyshev.py:185-218; m_override = 0 selects automatically */
+int sp_make_plan(double alpha, double beta, int precision_bits, int m_override, sp_plan* out);
+
+/* ---- context lifecycle (create / set_hamiltonian / close,
+ *      propagator.py:132-216 and 334-355; Parament_create/_free) -------- */
+/* no device work happens here: the GPU is touched lazily by the first
+ * propagation, so contexts can be created and validated without a GPU */
+int sp_create(sp_ctx** out, int precision_bits, int device_ordinal);
+int sp_free(sp_ctx* ctx);
+const char* sp_last_error(const sp_ctx* ctx);   /* ctx may be NULL */
+/* load the expansion terms [H0, effective controls...] (T x d x d complex128,
+ * host).  For magnus the caller passes the effective system of
+ * magnus.py:45-85 (controls, i[H0,Hk], i[Hk,Hk']).  Replaces
+ * IntegratorContext.set_hamiltonian (propagator.py:175-201). */
+int sp_set_hamiltonian(sp_ctx* ctx, int dim, int n_ctrl, int n_terms, int mode,
+                       const double* terms);
+
+/* ---- propagation (equiprop, propagator.py:238-308; Parament_equiprop) - */
+/* host buffers: amps (pts x n_ctrl float64), u_out (d x d, complex128 for
+ * fp64 contexts, complex64 for fp32).  plan comes from sp_make_plan on the
+ * global bound (propagator.py:258-263).  Synchronous. */
+int sp_equiprop(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
+                const sp_plan* plan, int reduction, void* u_out);
+/* same, device-resident: d_amps and d_u_out are device pointers, stream a
+ * cudaStream_t (NULL = the context stream).  Asynchronous. */
+int sp_equiprop_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
+                       double dt, const sp_plan* plan, int reduction, void* d_u_out,
+                       void* stream);
+/* cumulative propagators U(t_k <- 0), k = 0..slices-1 (equiprop_all,
+ * propagator.py:310-331).  u_all_out holds slices x d x d (host). */
+int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
+                    const sp_plan* plan, void* u_all_out);
+/* ordered product mats[count-1] ... mats[0] of device-resident complex128
+ * d x d matrices (the multi-GPU gather step; pairwise =
+ * reduce_pairwise propagator.py:68-102, sequential = left fold) */
+int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction,
+                      void* d_out, void* stream);
+/* slice count for a table of pts samples in the loaded mode
+ * (propagator.py:245-252); SP_E_SAMPLING_PARITY for even/short 3-point tables */
+int sp_slice_count(const sp_ctx* ctx, int64_t pts, int64_t* out);
+
+/* ---- measurement hooks ------------------------------------------------ */
+/* when enabled, the next propagations record CUDA events around the main
+ * lane kernel; sp_last_timing returns its duration (ms), the number of
+ * kernels launched by the last call and the executed FP64 flops */
+int sp_set_profiling(sp_ctx* ctx, int enabled);
+int sp_last_timing(const sp_ctx* ctx, double* main_kernel_ms, int* launches,
+                   double* executed_flops, char* kernel_name, int name_len);
+int sp_device_count(int* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLICEPROP_B200_H */

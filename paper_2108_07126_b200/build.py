@@ -1,0 +1,69 @@
+"""Build the sm_100a C-ABI library in-tree (no JIT cache, travels with gpurun).
+
+    python -m paper_2108_07126_b200.build        # or __graft_entry__.build()
+
+Produces ``paper_2108_07126_b200/libsliceprop_b200.so`` from
+``csrc/engine.cu`` (kernels + C ABI) and ``csrc/plan.cpp`` (host plan), with
+``-gencode arch=compute_100a,code=sm_100a -lineinfo`` and a static cudart so
+the library loads on machines without a GPU (for the CPU test tier).
+"""
+
+from __future__ import annotations
+
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libsliceprop_b200.so")
+SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "plan.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "internal.h")] + [
+    os.path.join(ROOT, "include", "sliceprop_b200.h")]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+    "-Xptxas", "-v",
+]
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(OUT):
+        return False
+    t = os.path.getmtime(OUT)
+    return all(os.path.getmtime(p) <= t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return OUT
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           *SOURCES, "-o", OUT + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log = res.stdout + res.stderr
+    with open(os.path.join(HERE, "build.log"), "w") as fh:
+        fh.write(" ".join(cmd) + "\n" + log)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{log[-4000:]}")
+    if any(int(n) > 0 for n in re.findall(r"(\d+) bytes spill stores", log)):
+        print("warning: register spills in the sm_100a build (see build.log)", file=sys.stderr)
+    os.replace(OUT + ".tmp", OUT)
+    if verbose:
+        print(log)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,771 @@
+// C ABI + device orchestration of the equiprop hot path (sm_100a).
+//
+// Replaces, behind include/sliceprop_b200.h, the reference's
+// IntegratorContext._slice_propagators + reduce_pairwise + equiprop +
+// equiprop_all (sliceprop/propagator.py:132-331) with one streaming kernel
+// pass per call (kernels.cuh) plus a short ordered-product tail.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.cuh"
+
+using namespace sp;
+
+namespace {
+
+const char* kVersion = "sliceprop_b200 0.1.0 (sm_100a)";
+thread_local char g_err[512] = "";
+
+enum Family { FAM_NONE = 0, FAM_S2, FAM_S4, FAM_T16, FAM_T32, FAM_T64, FAM_T128, FAM_T256 };
+
+// tensor-core configurations (see TCCfg): D, WC, MT, NT, WPL, LPC, GPL, X-in-smem
+using Cfg16 = TCCfg<16, 16, 1, 2, 1, 4, 1, true>;
+using Cfg32 = TCCfg<32, 32, 1, 2, 4, 1, 1, true>;
+using Cfg64 = TCCfg<64, 64, 1, 4, 8, 1, 1, true>;
+using Cfg128 = TCCfg<128, 32, 1, 4, 8, 1, 4, false>;
+using Cfg256 = TCCfg<256, 16, 2, 2, 8, 1, 16, false>;
+
+int family_for(int d, int* D) {
+  if (d <= 2) { *D = 2; return FAM_S2; }
+  if (d <= 4) { *D = 4; return FAM_S4; }
+  if (d <= 16) { *D = 16; return FAM_T16; }
+  if (d <= 32) { *D = 32; return FAM_T32; }
+  if (d <= 64) { *D = 64; return FAM_T64; }
+  if (d <= 128) { *D = 128; return FAM_T128; }
+  if (d <= 256) { *D = 256; return FAM_T256; }
+  *D = 0;
+  return FAM_NONE;
+}
+
+const char* family_kernel_name(int fam) {
+  switch (fam) {
+    case FAM_S2: return "lane_small_kernel<2,1>";
+    case FAM_S4: return "lane_small_kernel<4,4>";
+    case FAM_T16: return "lane_tc_kernel<D16>";
+    case FAM_T32: return "lane_tc_kernel<D32>";
+    case FAM_T64: return "lane_tc_kernel<D64>";
+    case FAM_T128: return "lane_tc_kernel<D128,group4>";
+    case FAM_T256: return "lane_tc_kernel<D256,group16>";
+  }
+  return "none";
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+}  // namespace
+
+struct sp_ctx {
+  int bits = 64;
+  int device = 0;
+  char err[512] = "";
+  // host-side system
+  bool loaded = false;
+  int dim = 0, n_ctrl = 0, n_terms = 0, mode = 0;
+  std::vector<double> terms_host;  // T x d x d complex128 interleaved
+  // device-side
+  bool dev_ready = false;
+  bool terms_uploaded = false;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  int fam = FAM_NONE, D = 0;
+  DevBuf terms, amps, lanes, ctab, tree0, tree1, xglob, gctr, result, out, cumP, cumE, cumO,
+      fold_scratch;
+  // profiling
+  bool prof = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool ev_pending = false;
+  float last_ms = 0.f;
+  int launches = 0;
+  double flops = 0.0;
+  const char* kname = "none";
+};
+
+namespace {
+
+int fail(sp_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) snprintf(ctx->err, sizeof(ctx->err), "%s", buf);
+  snprintf(g_err, sizeof(g_err), "%s", buf);
+  return code;
+}
+
+#define CUDA_TRY(ctx, call)                                                              \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(ctx, SP_E_INTERNAL, "CUDA error %s (%s) at %s:%d", cudaGetErrorName(e_), \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                           \
+  } while (0)
+
+int ensure(sp_ctx* ctx, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return SP_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  CUDA_TRY(ctx, cudaMalloc(&b.p, bytes));
+  b.cap = bytes;
+  return SP_OK;
+}
+
+int device_init(sp_ctx* ctx) {
+  if (ctx->dev_ready) return SP_OK;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(ctx, SP_E_INTERNAL,
+                "no CUDA device available (%s): the sliceprop_b200 propagation path is "
+                "GPU-only and has no CPU fallback",
+                e == cudaSuccess ? "device count 0" : cudaGetErrorString(e));
+  if (ctx->device < 0 || ctx->device >= n)
+    return fail(ctx, SP_E_CONFIG, "device ordinal %d out of range (have %d)", ctx->device, n);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  cudaDeviceProp prop;
+  CUDA_TRY(ctx, cudaGetDeviceProperties(&prop, ctx->device));
+  if (prop.major < 10)
+    return fail(ctx, SP_E_INTERNAL, "device %s (sm_%d%d) is not a Blackwell sm_100 part",
+                prop.name, prop.major, prop.minor);
+  ctx->sms = prop.multiProcessorCount;
+  CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CUDA_TRY(ctx, cudaEventCreate(&ctx->ev0));
+  CUDA_TRY(ctx, cudaEventCreate(&ctx->ev1));
+  ctx->dev_ready = true;
+  return SP_OK;
+}
+
+template <class C>
+int tc_prepare(sp_ctx* ctx) {
+  CUDA_TRY(ctx, cudaFuncSetAttribute(lane_tc_kernel<C>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)C::SMEM));
+  return SP_OK;
+}
+
+// permute + pad the host terms into the family's device layout
+int upload_terms(sp_ctx* ctx) {
+  const int d = ctx->dim, D = ctx->D, T = ctx->n_terms;
+  std::vector<double> h;
+  if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
+    h.assign((size_t)T * D * D * 2, 0.0);
+    for (int t = 0; t < T; ++t)
+      for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+          const double* src = &ctx->terms_host[(((size_t)t * d + r) * d + c) * 2];
+          double* dst = &h[(((size_t)t * D + r) * D + c) * 2];
+          dst[0] = src[0];
+          dst[1] = src[1];
+        }
+  } else {
+    const size_t xd = (size_t)2 * D * D;
+    h.assign((size_t)T * xd, 0.0);
+    for (int t = 0; t < T; ++t)
+      for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+          const double* src = &ctx->terms_host[(((size_t)t * d + r) * d + c) * 2];
+          h[t * xd + xfrag_index(D, r, c, 0)] = src[0];
+          h[t * xd + xfrag_index(D, r, c, 1)] = src[1];
+        }
+  }
+  int rc = ensure(ctx, ctx->terms, h.size() * sizeof(double));
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaMemcpy(ctx->terms.p, h.data(), h.size() * sizeof(double),
+                           cudaMemcpyHostToDevice));
+  switch (ctx->fam) {
+    case FAM_T16: rc = tc_prepare<Cfg16>(ctx); break;
+    case FAM_T32: rc = tc_prepare<Cfg32>(ctx); break;
+    case FAM_T64: rc = tc_prepare<Cfg64>(ctx); break;
+    case FAM_T128: rc = tc_prepare<Cfg128>(ctx); break;
+    case FAM_T256: rc = tc_prepare<Cfg256>(ctx); break;
+    default: break;
+  }
+  if (rc) return rc;
+  ctx->terms_uploaded = true;
+  return SP_OK;
+}
+
+int64_t slice_count_for(int mode, int64_t pts, int* code) {
+  *code = SP_OK;
+  if (mode == SP_MODE_MIDPOINT) return pts;
+  if (pts < 3 || pts % 2 == 0) {
+    *code = SP_E_SAMPLING_PARITY;
+    return -1;
+  }
+  return (pts - 1) / 2;
+}
+
+int grid_for(int64_t total, int threads) {
+  int64_t b = (total + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 64));
+}
+
+template <class C>
+int tc_lanes(sp_ctx* ctx, int64_t n) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_tc_kernel<C>, C::THREADS, C::SMEM);
+  if (occ < 1) occ = 1;
+  int64_t ctas = (int64_t)ctx->sms * occ;
+  int64_t units = (C::GPL > 1) ? ctas / C::GPL : ctas * C::LPC;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(units, n));
+}
+
+template <class C>
+int tc_launch(sp_ctx* ctx, const SliceJob& job, int lanes, double2* lane_out,
+              double2* prefix_out, cudaStream_t st) {
+  const int groups = (lanes + C::LPC - 1) / C::LPC;
+  const int grid = groups * C::GPL;
+  double* xg = nullptr;
+  unsigned* ctr = nullptr;
+  if (C::GPL > 1) {
+    int rc = ensure(ctx, ctx->xglob, (size_t)groups * 2 * C::XDBL * sizeof(double));
+    if (rc) return rc;
+    rc = ensure(ctx, ctx->gctr, (size_t)groups * sizeof(unsigned));
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->gctr.p, 0, (size_t)groups * sizeof(unsigned), st));
+    ++ctx->launches;
+    xg = (double*)ctx->xglob.p;
+    ctr = (unsigned*)ctx->gctr.p;
+    const double* terms = (const double*)ctx->terms.p;
+    void* args[] = {(void*)&job, (void*)&terms, (void*)&lanes, (void*)&xg,
+                    (void*)&ctr,  (void*)&lane_out, (void*)&prefix_out};
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)lane_tc_kernel<C>, dim3(grid),
+                                              dim3(C::THREADS), args, C::SMEM, st));
+  } else {
+    lane_tc_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(
+        job, (const double*)ctx->terms.p, lanes, xg, ctr, lane_out, prefix_out);
+  }
+  CUDA_TRY(ctx, cudaGetLastError());
+  ++ctx->launches;
+  return SP_OK;
+}
+
+template <int D>
+__global__ void chunk_reduce_kernel(const double2* __restrict__ in, int cnt,
+                                    double2* __restrict__ out) {
+  constexpr int CH = (D == 2) ? 256 : 64;
+  __shared__ double2 buf[2][CH * D * D];
+  const int base = blockIdx.x * CH;
+  const int here = min(CH, cnt - base);
+  for (int e = threadIdx.x; e < here * D * D; e += blockDim.x)
+    buf[0][e] = in[(size_t)base * D * D + e];
+  __syncthreads();
+  int c = here, src = 0;
+  while (c > 1) {
+    const int pairs = c >> 1;
+    for (int e = threadIdx.x; e < pairs * D * D; e += blockDim.x) {
+      const int p = e / (D * D), rc = e % (D * D), r = rc / D, cc = rc % D;
+      buf[src ^ 1][p * D * D + rc] =
+          cdot(&buf[src][(2 * p + 1) * D * D + r * D], &buf[src][(2 * p) * D * D], D, cc, D);
+    }
+    if (c & 1)
+      for (int e = threadIdx.x; e < D * D; e += blockDim.x)
+        buf[src ^ 1][pairs * D * D + e] = buf[src][(c - 1) * D * D + e];
+    __syncthreads();
+    c = pairs + (c & 1);
+    src ^= 1;
+  }
+  for (int e = threadIdx.x; e < D * D; e += blockDim.x)
+    out[(size_t)blockIdx.x * D * D + e] = buf[src][e];
+}
+
+// pairwise tree over cnt matrices (in place ping-pong); returns the buffer
+// holding the single result
+int reduce_pairwise_dev(sp_ctx* ctx, const double2* in, int cnt, int D, cudaStream_t st,
+                        const double2** result) {
+  const size_t dd = (size_t)D * D;
+  if (cnt == 1) {
+    *result = in;
+    return SP_OK;
+  }
+  int rc = ensure(ctx, ctx->tree0, ((cnt + 1) / 2) * dd * sizeof(double2));
+  if (rc) return rc;
+  rc = ensure(ctx, ctx->tree1, ((cnt + 3) / 4 + 1) * dd * sizeof(double2));
+  if (rc) return rc;
+  const double2* src = in;
+  DevBuf* bufs[2] = {&ctx->tree0, &ctx->tree1};
+  int which = 0;
+  while (cnt > 1) {
+    const int nxt = cnt / 2 + (cnt & 1);
+    double2* dst = (double2*)bufs[which]->p;
+    if (D <= 4 && cnt > 2) {
+      const int ch = (D == 2) ? 256 : 64;
+      const int blocks = (cnt + ch - 1) / ch;
+      if (D == 2)
+        chunk_reduce_kernel<2><<<blocks, 256, 0, st>>>(src, cnt, dst);
+      else
+        chunk_reduce_kernel<4><<<blocks, 256, 0, st>>>(src, cnt, dst);
+      CUDA_TRY(ctx, cudaGetLastError());
+      ++ctx->launches;
+      cnt = blocks;
+    } else {
+      pair_level_kernel<<<grid_for((int64_t)nxt * dd, 256), 256, 0, st>>>(src, cnt, D, dst);
+      CUDA_TRY(ctx, cudaGetLastError());
+      ++ctx->launches;
+      cnt = nxt;
+    }
+    src = dst;
+    which ^= 1;
+  }
+  *result = src;
+  return SP_OK;
+}
+
+// Run the lane pass.  Returns the lane products (lane_count of them) on the
+// device, or (small families, pairwise) the per-CTA products.
+int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix_out,
+              cudaStream_t st, const double2** prods, int* count) {
+  const int64_t n = job.n_slices;
+  const int D = ctx->D;
+  const size_t dd = (size_t)D * D;
+  int lanes = 1;
+  if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
+    const int tpl = (ctx->fam == FAM_S2) ? 1 : 4;
+    int64_t cap = (int64_t)ctx->sms * 2048 / tpl;
+    int64_t want = cta_reduce ? std::max<int64_t>((int64_t)ctx->sms * 256 / tpl, (n + 7) / 8)
+                              : 1024;
+    lanes = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(cap, want), n));
+    const int blocks = (int)(((int64_t)lanes * tpl + 255) / 256);
+    int rc = ensure(ctx, ctx->lanes, (size_t)(cta_reduce ? blocks : lanes) * dd * sizeof(double2));
+    if (rc) return rc;
+    double2* lane_out = (double2*)ctx->lanes.p;
+    double2* cta_out = cta_reduce ? lane_out : nullptr;
+    if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+    if (ctx->fam == FAM_S2)
+      lane_small_kernel<2, 1><<<blocks, 256, 0, st>>>(job, (const double2*)ctx->terms.p, lanes,
+                                                      lane_out, cta_out, prefix_out);
+    else
+      lane_small_kernel<4, 4><<<blocks, 256, 0, st>>>(job, (const double2*)ctx->terms.p, lanes,
+                                                      lane_out, cta_out, prefix_out);
+    CUDA_TRY(ctx, cudaGetLastError());
+    if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+    ++ctx->launches;
+    *prods = lane_out;
+    *count = cta_reduce ? blocks : lanes;
+    return SP_OK;
+  }
+  switch (ctx->fam) {
+    case FAM_T16: lanes = tc_lanes<Cfg16>(ctx, n); break;
+    case FAM_T32: lanes = tc_lanes<Cfg32>(ctx, n); break;
+    case FAM_T64: lanes = tc_lanes<Cfg64>(ctx, n); break;
+    case FAM_T128: lanes = tc_lanes<Cfg128>(ctx, n); break;
+    case FAM_T256: lanes = tc_lanes<Cfg256>(ctx, n); break;
+  }
+  int rc = ensure(ctx, ctx->lanes, (size_t)lanes * dd * sizeof(double2));
+  if (rc) return rc;
+  double2* lane_out = (double2*)ctx->lanes.p;
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+  switch (ctx->fam) {
+    case FAM_T16: rc = tc_launch<Cfg16>(ctx, job, lanes, lane_out, prefix_out, st); break;
+    case FAM_T32: rc = tc_launch<Cfg32>(ctx, job, lanes, lane_out, prefix_out, st); break;
+    case FAM_T64: rc = tc_launch<Cfg64>(ctx, job, lanes, lane_out, prefix_out, st); break;
+    case FAM_T128: rc = tc_launch<Cfg128>(ctx, job, lanes, lane_out, prefix_out, st); break;
+    case FAM_T256: rc = tc_launch<Cfg256>(ctx, job, lanes, lane_out, prefix_out, st); break;
+  }
+  if (rc) return rc;
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+  *prods = lane_out;
+  *count = lanes;
+  return SP_OK;
+}
+
+int check_loaded(sp_ctx* ctx) {
+  if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
+  if (!ctx->loaded)
+    return fail(ctx, SP_E_STATE_MACHINE, "no Hamiltonian loaded; call set_hamiltonian first");
+  return SP_OK;
+}
+
+int build_job(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double dt,
+              const sp_plan* plan, SliceJob* job) {
+  if (n_ctrl != ctx->n_ctrl)
+    return fail(ctx, SP_E_SHAPE, "amplitude table has %d controls, system has %d", n_ctrl,
+                ctx->n_ctrl);
+  if (!(dt > 0.0)) return fail(ctx, SP_E_CONFIG, "time step must be > 0, got %g", dt);
+  if (!plan) return fail(ctx, SP_E_CONFIG, "missing plan");
+  if (plan->m_max < 3 || plan->m_max > SP_MAX_ORDER || plan->m_max % 2 == 0)
+    return fail(ctx, SP_E_CONFIG, "plan order %d not on the odd grid 3..25", plan->m_max);
+  if (plan->alpha != -plan->beta)
+    return fail(ctx, SP_E_CONFIG, "equiprop plans are symmetric (alpha = -beta)");
+  int code;
+  const int64_t n = slice_count_for(ctx->mode, pts, &code);
+  if (code)
+    return fail(ctx, code, "three-point quadrature needs an odd number of samples >= 3, got %lld",
+                (long long)pts);
+  std::memset(job, 0, sizeof(*job));
+  job->amps = d_amps;
+  job->pts = pts;
+  job->n_ctrl = n_ctrl;
+  job->n_terms = ctx->n_terms;
+  job->mode = ctx->mode;
+  job->dt = dt;
+  const double scale = (ctx->mode == SP_MODE_MIDPOINT) ? dt : 2.0 * dt;
+  const double span = plan->beta - plan->alpha;
+  job->xs = (span == 0.0) ? 0.0 : 2.0 * scale * (2.0 / span);
+  job->m = plan->m_max;
+  std::memcpy(job->coef, plan->coeffs, sizeof(job->coef));
+  job->phase[0] = plan->phase[0];
+  job->phase[1] = plan->phase[1];
+  job->n_slices = n;
+  return SP_OK;
+}
+
+int prepare_device(sp_ctx* ctx) {
+  int rc = device_init(ctx);
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  if (!ctx->terms_uploaded) {
+    rc = upload_terms(ctx);
+    if (rc) return rc;
+  }
+  return SP_OK;
+}
+
+double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
+  const double D = ctx->D;
+  return (double)n * (8.0 * D * D * D * m + 4.0 * D * D * ctx->n_terms);
+}
+
+// total propagator on the device -> d x d in d_out (output dtype)
+int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double dt,
+                 const sp_plan* plan, int reduction, void* d_out, cudaStream_t st) {
+  ctx->launches = 0;
+  ctx->flops = 0.0;
+  ctx->ev_pending = false;
+  SliceJob job;
+  int rc = build_job(ctx, d_amps, pts, n_ctrl, dt, plan, &job);
+  if (rc) return rc;
+  const int D = ctx->D, d = ctx->dim;
+  const size_t dd = (size_t)D * D;
+  rc = ensure(ctx, ctx->result, dd * sizeof(double2));
+  if (rc) return rc;
+  const double2* total = nullptr;
+  if (job.n_slices == 0) {
+    // empty product (propagator.py:297-299)
+    std::vector<double2> eye(dd, make_double2(0.0, 0.0));
+    for (int i = 0; i < D; ++i) eye[(size_t)i * D + i].x = 1.0;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->result.p, eye.data(), dd * sizeof(double2),
+                                  cudaMemcpyHostToDevice, st));
+    total = (const double2*)ctx->result.p;
+  } else {
+    const bool small = ctx->fam == FAM_S2 || ctx->fam == FAM_S4;
+    const bool cta_reduce = small && reduction == SP_REDUCE_PAIRWISE;
+    const double2* prods = nullptr;
+    int cnt = 0;
+    rc = run_lanes(ctx, job, cta_reduce, nullptr, st, &prods, &cnt);
+    if (rc) return rc;
+    ctx->ev_pending = ctx->prof;
+    ctx->kname = family_kernel_name(ctx->fam);
+    ctx->flops = executed_flops(ctx, job.n_slices, job.m);
+    if (reduction == SP_REDUCE_PAIRWISE) {
+      rc = reduce_pairwise_dev(ctx, prods, cnt, D, st, &total);
+      if (rc) return rc;
+    } else {
+      rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
+      if (rc) return rc;
+      fold_kernel<<<1, 1024, 0, st>>>(prods, cnt, D, (double2*)ctx->fold_scratch.p, nullptr,
+                                       (double2*)ctx->result.p);
+      CUDA_TRY(ctx, cudaGetLastError());
+      ++ctx->launches;
+      total = (const double2*)ctx->result.p;
+    }
+  }
+  extract_kernel<<<grid_for((int64_t)d * d, 256), 256, 0, st>>>(total, 1, D, d,
+                                                                ctx->bits == 32, d_out);
+  CUDA_TRY(ctx, cudaGetLastError());
+  ++ctx->launches;
+  return SP_OK;
+}
+
+int product_dev(sp_ctx* ctx, int count, const double2* d_mats, int reduction, void* d_out,
+                cudaStream_t st) {
+  const int d = ctx->dim, D = ctx->D;
+  const size_t dd = (size_t)D * D;
+  int rc = ensure(ctx, ctx->cumP, std::max(1, count) * dd * sizeof(double2));
+  if (rc) return rc;
+  rc = ensure(ctx, ctx->result, dd * sizeof(double2));
+  if (rc) return rc;
+  double2* padded = (double2*)ctx->cumP.p;
+  if (count == 0) {
+    std::vector<double2> eye(dd, make_double2(0.0, 0.0));
+    for (int i = 0; i < D; ++i) eye[(size_t)i * D + i].x = 1.0;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->result.p, eye.data(), dd * sizeof(double2),
+                                  cudaMemcpyHostToDevice, st));
+    extract_kernel<<<grid_for((int64_t)d * d, 256), 256, 0, st>>>(
+        (const double2*)ctx->result.p, 1, D, d, ctx->bits == 32, d_out);
+    CUDA_TRY(ctx, cudaGetLastError());
+    return SP_OK;
+  }
+  embed_kernel<<<grid_for((int64_t)count * dd, 256), 256, 0, st>>>(d_mats, count, d, D, padded);
+  CUDA_TRY(ctx, cudaGetLastError());
+  const double2* total = nullptr;
+  if (reduction == SP_REDUCE_PAIRWISE) {
+    rc = reduce_pairwise_dev(ctx, padded, count, D, st, &total);
+    if (rc) return rc;
+  } else {
+    rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
+    if (rc) return rc;
+    fold_kernel<<<1, 1024, 0, st>>>(padded, count, D, (double2*)ctx->fold_scratch.p, nullptr,
+                                     (double2*)ctx->result.p);
+    CUDA_TRY(ctx, cudaGetLastError());
+    total = (const double2*)ctx->result.p;
+  }
+  extract_kernel<<<grid_for((int64_t)d * d, 256), 256, 0, st>>>(total, 1, D, d,
+                                                                ctx->bits == 32, d_out);
+  CUDA_TRY(ctx, cudaGetLastError());
+  return SP_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* sp_version(void) { return kVersion; }
+
+int sp_bessel_j(int k, double x, double* out) {
+  if (!out) return fail(nullptr, SP_E_CONFIG, "null output");
+  return bessel_j(k, x, out, g_err, sizeof(g_err));
+}
+
+double sp_chebyshev_error(int m, double span) { return chebyshev_error(m, span); }
+
+int sp_select_m_max(double norm_bound, int precision_bits, int* m_out, double* capability) {
+  if (precision_bits != 32 && precision_bits != 64)
+    return fail(nullptr, SP_E_CONFIG, "precision must be 32 or 64 bits");
+  return select_m_max(norm_bound, precision_bits, m_out, capability, g_err, sizeof(g_err));
+}
+
+int sp_norm_capability(int m, int precision_bits, double* out) {
+  if (precision_bits != 32 && precision_bits != 64)
+    return fail(nullptr, SP_E_CONFIG, "precision must be 32 or 64 bits");
+  return norm_capability(m, precision_bits, out, g_err, sizeof(g_err));
+}
+
+int sp_make_plan(double alpha, double beta, int precision_bits, int m_override, sp_plan* out) {
+  if (!out) return fail(nullptr, SP_E_CONFIG, "null plan");
+  if (precision_bits != 32 && precision_bits != 64)
+    return fail(nullptr, SP_E_CONFIG, "precision must be 32 or 64 bits");
+  return make_plan(alpha, beta, precision_bits, m_override, out, g_err, sizeof(g_err));
+}
+
+int sp_create(sp_ctx** out, int precision_bits, int device_ordinal) {
+  if (!out) return fail(nullptr, SP_E_CONFIG, "null output pointer");
+  if (precision_bits != 32 && precision_bits != 64)
+    return fail(nullptr, SP_E_CONFIG, "unknown precision %d; expected 32 or 64", precision_bits);
+  sp_ctx* ctx = new sp_ctx();
+  ctx->bits = precision_bits;
+  ctx->device = device_ordinal;
+  *out = ctx;
+  return SP_OK;
+}
+
+int sp_free(sp_ctx* ctx) {
+  if (!ctx) return SP_OK;
+  if (ctx->dev_ready) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DevBuf* bufs[] = {&ctx->terms, &ctx->amps,  &ctx->lanes, &ctx->ctab, &ctx->tree0,
+                      &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
+                      &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch};
+    for (DevBuf* b : bufs)
+      if (b->p) cudaFree(b->p);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
+  return SP_OK;
+}
+
+const char* sp_last_error(const sp_ctx* ctx) { return ctx ? ctx->err : g_err; }
+
+int sp_set_hamiltonian(sp_ctx* ctx, int dim, int n_ctrl, int n_terms, int mode,
+                       const double* terms) {
+  if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
+  if (dim < 1) return fail(ctx, SP_E_SHAPE, "dim must be >= 1, got %d", dim);
+  if (mode < SP_MODE_MIDPOINT || mode > SP_MODE_MAGNUS)
+    return fail(ctx, SP_E_CONFIG, "unknown mode %d", mode);
+  const int expect = (mode == SP_MODE_MAGNUS) ? 1 + 2 * n_ctrl + n_ctrl * (n_ctrl - 1) / 2
+                                              : 1 + n_ctrl;
+  if (n_ctrl < 0 || n_terms != expect)
+    return fail(ctx, SP_E_SHAPE, "%d expansion terms do not match %d controls in mode %d",
+                n_terms, n_ctrl, mode);
+  if (n_terms > 256) return fail(ctx, SP_E_CONFIG, "at most 256 expansion terms supported");
+  int D = 0;
+  const int fam = family_for(dim, &D);
+  if (fam == FAM_NONE)
+    return fail(ctx, SP_E_CONFIG, "dimension %d not supported (max 256)", dim);
+  if (!terms) return fail(ctx, SP_E_SHAPE, "null terms");
+  ctx->dim = dim;
+  ctx->n_ctrl = n_ctrl;
+  ctx->n_terms = n_terms;
+  ctx->mode = mode;
+  ctx->terms_host.assign(terms, terms + (size_t)n_terms * dim * dim * 2);
+  ctx->fam = fam;
+  ctx->D = D;
+  ctx->terms_uploaded = false;
+  ctx->loaded = true;
+  return SP_OK;
+}
+
+int sp_slice_count(const sp_ctx* ctx, int64_t pts, int64_t* out) {
+  if (!ctx || !ctx->loaded) return fail(nullptr, SP_E_STATE_MACHINE, "no Hamiltonian loaded");
+  int code;
+  *out = slice_count_for(ctx->mode, pts, &code);
+  if (code) return fail(nullptr, code, "three-point quadrature needs an odd number of samples >= 3");
+  return SP_OK;
+}
+
+int sp_equiprop_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double dt,
+                       const sp_plan* plan, int reduction, void* d_u_out, void* stream) {
+  int rc = check_loaded(ctx);
+  if (rc) return rc;
+  if (reduction != SP_REDUCE_PAIRWISE && reduction != SP_REDUCE_SEQUENTIAL)
+    return fail(ctx, SP_E_CONFIG, "unknown reduction %d", reduction);
+  rc = prepare_device(ctx);
+  if (rc) return rc;
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  return equiprop_dev(ctx, d_amps, pts, n_ctrl, dt, plan, reduction, d_u_out, st);
+}
+
+int sp_equiprop(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
+                const sp_plan* plan, int reduction, void* u_out) {
+  int rc = check_loaded(ctx);
+  if (rc) return rc;
+  if (reduction != SP_REDUCE_PAIRWISE && reduction != SP_REDUCE_SEQUENTIAL)
+    return fail(ctx, SP_E_CONFIG, "unknown reduction %d", reduction);
+  if (pts < 0) return fail(ctx, SP_E_SHAPE, "negative sample count");
+  rc = prepare_device(ctx);
+  if (rc) return rc;
+  cudaStream_t st = ctx->stream;
+  const size_t abytes = (size_t)pts * n_ctrl * sizeof(double);
+  rc = ensure(ctx, ctx->amps, abytes);
+  if (rc) return rc;
+  if (abytes)
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->amps.p, amps, abytes, cudaMemcpyHostToDevice, st));
+  const size_t obytes = (size_t)ctx->dim * ctx->dim * (ctx->bits == 32 ? 8 : 16);
+  rc = ensure(ctx, ctx->out, obytes);
+  if (rc) return rc;
+  rc = equiprop_dev(ctx, (const double*)ctx->amps.p, pts, n_ctrl, dt, plan, reduction,
+                    ctx->out.p, st);
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaMemcpyAsync(u_out, ctx->out.p, obytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
+                    const sp_plan* plan, void* u_all_out) {
+  int rc = check_loaded(ctx);
+  if (rc) return rc;
+  if (pts < 0) return fail(ctx, SP_E_SHAPE, "negative sample count");
+  rc = prepare_device(ctx);
+  if (rc) return rc;
+  cudaStream_t st = ctx->stream;
+  ctx->launches = 0;
+  ctx->ev_pending = false;
+  const size_t abytes = (size_t)pts * n_ctrl * sizeof(double);
+  rc = ensure(ctx, ctx->amps, abytes);
+  if (rc) return rc;
+  if (abytes)
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->amps.p, amps, abytes, cudaMemcpyHostToDevice, st));
+  SliceJob job;
+  rc = build_job(ctx, (const double*)ctx->amps.p, pts, n_ctrl, dt, plan, &job);
+  if (rc) return rc;
+  const int64_t n = job.n_slices;
+  if (n == 0) return SP_OK;
+  const int D = ctx->D, d = ctx->dim;
+  const size_t dd = (size_t)D * D;
+  rc = ensure(ctx, ctx->cumP, (size_t)n * dd * sizeof(double2));
+  if (rc) return rc;
+  const double2* prods = nullptr;
+  int cnt = 0;
+  rc = run_lanes(ctx, job, false, (double2*)ctx->cumP.p, st, &prods, &cnt);
+  if (rc) return rc;
+  ctx->ev_pending = ctx->prof;
+  ctx->kname = family_kernel_name(ctx->fam);
+  ctx->flops = executed_flops(ctx, n, job.m);
+  rc = ensure(ctx, ctx->cumE, (size_t)cnt * dd * sizeof(double2));
+  if (rc) return rc;
+  rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
+  if (rc) return rc;
+  rc = ensure(ctx, ctx->result, dd * sizeof(double2));
+  if (rc) return rc;
+  fold_kernel<<<1, 1024, 0, st>>>(prods, cnt, D, (double2*)ctx->fold_scratch.p,
+                                   (double2*)ctx->cumE.p, (double2*)ctx->result.p);
+  CUDA_TRY(ctx, cudaGetLastError());
+  rc = ensure(ctx, ctx->cumO, (size_t)n * dd * sizeof(double2));
+  if (rc) return rc;
+  apply_prefix_kernel<<<grid_for((int64_t)n * dd, 256), 256, 0, st>>>(
+      (const double2*)ctx->cumP.p, (const double2*)ctx->cumE.p, n, cnt, D,
+      (double2*)ctx->cumO.p);
+  CUDA_TRY(ctx, cudaGetLastError());
+  const size_t obytes = (size_t)n * d * d * (ctx->bits == 32 ? 8 : 16);
+  rc = ensure(ctx, ctx->out, obytes);
+  if (rc) return rc;
+  extract_kernel<<<grid_for((int64_t)n * d * d, 256), 256, 0, st>>>(
+      (const double2*)ctx->cumO.p, n, D, d, ctx->bits == 32, ctx->out.p);
+  CUDA_TRY(ctx, cudaGetLastError());
+  ctx->launches += 3;
+  CUDA_TRY(ctx, cudaMemcpyAsync(u_all_out, ctx->out.p, obytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction, void* d_out,
+                      void* stream) {
+  int rc = check_loaded(ctx);
+  if (rc) return rc;
+  if (count < 0) return fail(ctx, SP_E_SHAPE, "negative count");
+  rc = prepare_device(ctx);
+  if (rc) return rc;
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  return product_dev(ctx, count, (const double2*)d_mats, reduction, d_out, st);
+}
+
+int sp_set_profiling(sp_ctx* ctx, int enabled) {
+  if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
+  ctx->prof = enabled != 0;
+  return SP_OK;
+}
+
+int sp_last_timing(const sp_ctx* cctx, double* main_kernel_ms, int* launches,
+                   double* executed, char* kernel_name, int name_len) {
+  sp_ctx* ctx = const_cast<sp_ctx*>(cctx);
+  if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
+  if (ctx->ev_pending) {
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ctx->last_ms, ctx->ev0, ctx->ev1));
+    ctx->ev_pending = false;
+  }
+  if (main_kernel_ms) *main_kernel_ms = ctx->last_ms;
+  if (launches) *launches = ctx->launches;
+  if (executed) *executed = ctx->flops;
+  if (kernel_name && name_len > 0) snprintf(kernel_name, name_len, "%s", ctx->kname);
+  return SP_OK;
+}
+
+int sp_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  *out = (e == cudaSuccess) ? n : 0;
+  return SP_OK;
+}
+
+}  // extern "C"

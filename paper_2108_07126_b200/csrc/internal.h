@@ -1,0 +1,33 @@
+// Internal declarations shared by the host plan, the C ABI and the kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "sliceprop_b200.h"
+
+namespace sp {
+
+int bessel_j(int k, double x, double* out, char* err, size_t errlen);
+double chebyshev_error(int m, double span);
+int norm_capability(int m, int bits, double* out, char* err, size_t errlen);
+int select_m_max(double norm_bound, int bits, int* m_out, double* capability, char* err,
+                 size_t errlen);
+int make_plan(double alpha, double beta, int bits, int m_override, sp_plan* out, char* err,
+              size_t errlen);
+
+// Everything one propagation needs on the device (all pointers device).
+struct SliceJob {
+  const double* amps;     // (pts, n_ctrl) float64
+  int64_t pts;
+  int n_ctrl;
+  int n_terms;            // T = 1 + effective controls
+  int mode;               // SP_MODE_*
+  double dt;
+  double xs;              // 2 * scale / beta  (0 when beta == 0): "2X" factor
+  int m;                  // series order
+  double coef[2 * (SP_MAX_ORDER + 1)];
+  double phase[2];
+  int64_t n_slices;
+};
+
+}  // namespace sp

@@ -1,0 +1,665 @@
+// sm_100a kernels of the equiprop hot path.
+//
+// What the reference does in three materialised passes — expand every slice
+// exponent (linalg.py:246-288), Chebyshev/Clenshaw-exponentiate the batch
+// (chebyshev.py:259-306), fold the batch pairwise (propagator.py:68-102) —
+// runs here as ONE streaming pass per "lane" (a contiguous run of slices):
+//
+//   for each slice s of the lane:
+//     X_s = (2 scale / beta) (H0 + sum_t w_t(s) T_t)        assembled on chip
+//     V   = p(X_s) V   by the reference's Clenshaw recurrence applied to
+//           the running product V instead of I:
+//           b_m = a_m V, b_{j} = a_j V + 2X b_{j+1} - (j==0 ? 2 : 1) b_{j+2}
+//
+// so p(X_s) (the slice propagator U_s) is never formed and nothing of size
+// n*d^2 touches HBM.  The same m products per slice as the reference's
+// m - 1 Clenshaw GEMMs + 1 reduction GEMM.  The lane products are then
+// multiplied in time order (tree or left fold).
+//
+// Families
+//   lane_small_kernel<D,TPL>  D in {2,4}: TPL threads per lane, each owning
+//                             D/TPL columns of V; X in registers; DFMA.
+//   lane_tc_kernel<Cfg>       D in {16..256}: FP64 tensor cores (DMMA,
+//                             mma.sync m16n8k4 -> SASS DMMA.8x8x4).  A CTA
+//                             (or a group of GPL CTAs) owns a lane; each CTA
+//                             owns a WC-wide column block of V, because
+//                             column j of p(X) V depends only on column j of
+//                             V and on X — the Clenshaw recurrence needs no
+//                             inter-CTA traffic except sharing X.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace sp {
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_16x8x4(double& c0, double& c1, double& c2, double& c3,
+                                            double a0, double a1, double b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Weight of expansion term t >= 1 for slice s (term 0 = drift, weight 1).
+//   midpoint  hamiltonian.py:199-201        w = c_{s,t-1}
+//   simpson   hamiltonian.py:202-205        w = (c1 + 4 c2 + c3) / 6
+//   magnus    magnus.py:88-106, 134-139     controls: (c1+4c2+c3)/6,
+//             i[H0,Hk]: (dt/6)(c3-c1),  i[Hk,Hk']: (dt/6)(c1_k c3_k' - c3_k c1_k')
+//   (the reference divides the magnus columns by the 2dt scale; same values)
+__device__ __forceinline__ double slice_weight(const SliceJob& j, int64_t s, int t) {
+  const int N = j.n_ctrl;
+  if (j.mode == SP_MODE_MIDPOINT) return j.amps[s * N + (t - 1)];
+  const double* r1 = j.amps + (2 * s) * N;
+  const double* r2 = r1 + N;
+  const double* r3 = r2 + N;
+  int e = t - 1;
+  if (e < N) return (r1[e] + 4.0 * r2[e] + r3[e]) / 6.0;
+  e -= N;
+  if (e < N) return (j.dt / 6.0) * (r3[e] - r1[e]);
+  e -= N;
+  int k = 0;
+  while (e >= N - 1 - k) {
+    e -= N - 1 - k;
+    ++k;
+  }
+  const int kp = k + 1 + e;
+  return (j.dt / 6.0) * (r1[k] * r3[kp] - r3[k] * r1[kp]);
+}
+
+// The one complex dot product every ordered-product kernel uses (pair
+// levels, left fold, prefix application): identical summation order
+// everywhere keeps equiprop_all's last entry bitwise equal to the
+// sequential reduction (reference property propagator.py:304-306, 310-316).
+// (no __restrict__: the left fold reads matrices it wrote earlier in the
+// same launch, so the non-coherent load path must not be used)
+__device__ __forceinline__ double2 cdot(const double2* a_row, const double2* b, int ldb, int c,
+                                        int D) {
+  double re = 0.0, im = 0.0;
+  for (int k = 0; k < D; ++k) {
+    const double2 a = a_row[k];
+    const double2 x = b[(size_t)k * ldb + c];
+    re = fma(a.x, x.x, re);
+    re = fma(-a.y, x.y, re);
+    im = fma(a.x, x.y, im);
+    im = fma(a.y, x.x, im);
+  }
+  return make_double2(re, im);
+}
+
+__device__ __forceinline__ void lane_range(int64_t n, int lanes, int lane, int64_t& s0,
+                                           int64_t& s1) {
+  s0 = (int64_t)lane * n / lanes;
+  s1 = ((int64_t)lane + 1) * n / lanes;
+}
+
+// ---------------------------------------------------------------------------
+// Family S: D in {2, 4}.  TPL threads per lane, CPT = D / TPL columns each.
+// ---------------------------------------------------------------------------
+template <int D, int TPL>
+__global__ void __launch_bounds__(256) lane_small_kernel(SliceJob job,
+                                                         const double2* __restrict__ terms,
+                                                         int lanes, double2* __restrict__ lane_out,
+                                                         double2* __restrict__ cta_out,
+                                                         double2* __restrict__ prefix_out) {
+  constexpr int CPT = D / TPL;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = gtid / TPL;
+  const int c0 = (gtid % TPL) * CPT;
+  double2 V[D][CPT];
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) V[r][cc] = make_double2(r == c0 + cc ? 1.0 : 0.0, 0.0);
+
+  int64_t s0 = 0, s1 = 0;
+  if (lane < lanes) lane_range(job.n_slices, lanes, lane, s0, s1);
+  const int T = job.n_terms;
+  const int m = job.m;
+  const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
+
+  for (int64_t s = s0; s < s1; ++s) {
+    // ---- assemble 2X in registers
+    double2 X[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) X[r][c] = __ldg(&terms[r * D + c]);
+    for (int t = 1; t < T; ++t) {
+      const double w = slice_weight(job, s, t);
+      const double2* tt = terms + (size_t)t * D * D;
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const double2 h = __ldg(&tt[r * D + c]);
+          X[r][c].x = fma(w, h.x, X[r][c].x);
+          X[r][c].y = fma(w, h.y, X[r][c].y);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        X[r][c].x *= job.xs;
+        X[r][c].y *= job.xs;
+      }
+    // ---- Clenshaw applied to V (chebyshev.py:298-303 with I -> V)
+    double2 cur[D][CPT], old[D][CPT];
+    {
+      const double ar = job.coef[2 * m], ai = job.coef[2 * m + 1];
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+          cur[r][cc] = make_double2(ar * V[r][cc].x - ai * V[r][cc].y,
+                                    ar * V[r][cc].y + ai * V[r][cc].x);
+          old[r][cc] = make_double2(0.0, 0.0);
+        }
+    }
+    for (int jj = m - 1; jj >= 0; --jj) {
+      const double ar = job.coef[2 * jj], ai = job.coef[2 * jj + 1];
+      const double beta = (jj == 0) ? 2.0 : 1.0;
+      double2 nw[D][CPT];
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+          double re = fma(ar, V[r][cc].x, fma(-ai, V[r][cc].y, -beta * old[r][cc].x));
+          double im = fma(ar, V[r][cc].y, fma(ai, V[r][cc].x, -beta * old[r][cc].y));
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            re = fma(X[r][k].x, cur[k][cc].x, re);
+            re = fma(-X[r][k].y, cur[k][cc].y, re);
+            im = fma(X[r][k].x, cur[k][cc].y, im);
+            im = fma(X[r][k].y, cur[k][cc].x, im);
+          }
+          nw[r][cc] = make_double2(re, im);
+        }
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+          old[r][cc] = cur[r][cc];
+          cur[r][cc] = nw[r][cc];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int cc = 0; cc < CPT; ++cc) {
+        if (phase_one) {
+          V[r][cc] = cur[r][cc];
+        } else {
+          V[r][cc] = make_double2(job.phase[0] * cur[r][cc].x - job.phase[1] * cur[r][cc].y,
+                                  job.phase[0] * cur[r][cc].y + job.phase[1] * cur[r][cc].x);
+        }
+      }
+    if (prefix_out) {
+      double2* o = prefix_out + (size_t)s * D * D;
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) o[r * D + c0 + cc] = V[r][cc];
+    }
+  }
+
+  if (cta_out == nullptr) {
+    if (lane < lanes) {
+      double2* o = lane_out + (size_t)lane * D * D;
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) o[r * D + c0 + cc] = V[r][cc];
+    }
+    return;
+  }
+  // ---- in-CTA ordered pairwise tree over the CTA's consecutive lanes
+  constexpr int LPB = 256 / TPL;  // lanes per block (blockDim = 256)
+  __shared__ double2 buf[2][LPB * D * D];
+  const int lb = threadIdx.x / TPL;
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) buf[0][lb * D * D + r * D + c0 + cc] = V[r][cc];
+  __syncthreads();
+  int cnt = LPB, src = 0;
+  while (cnt > 1) {
+    const int pairs = cnt >> 1;
+    for (int e = threadIdx.x; e < pairs * D * D; e += blockDim.x) {
+      const int p = e / (D * D), rc = e % (D * D), r = rc / D, c = rc % D;
+      const double2* later = &buf[src][(2 * p + 1) * D * D];
+      const double2* earlier = &buf[src][(2 * p) * D * D];
+      buf[src ^ 1][p * D * D + rc] = cdot(later + r * D, earlier, D, c, D);
+    }
+    if (cnt & 1)
+      for (int e = threadIdx.x; e < D * D; e += blockDim.x)
+        buf[src ^ 1][pairs * D * D + e] = buf[src][(cnt - 1) * D * D + e];
+    __syncthreads();
+    cnt = pairs + (cnt & 1);
+    src ^= 1;
+  }
+  for (int e = threadIdx.x; e < D * D; e += blockDim.x)
+    cta_out[(size_t)blockIdx.x * D * D + e] = buf[src][e];
+}
+
+// ---------------------------------------------------------------------------
+// Family TC: FP64 tensor cores.
+// ---------------------------------------------------------------------------
+// X fragment layout ("A-native"): for strip S (rows 16S..16S+15), k-block kb
+// (cols 4kb..4kb+3), plane p (0 re, 1 im): 64 doubles; lane l holds
+// {X[16S + g][4kb + t], X[16S + 8 + g][4kb + t]} at offset 2l, g = l>>2, t = l&3.
+// B fragment layout (iterates, smem): for k-block kb, n-tile nt, plane p: 32
+// doubles; lane l holds B[4kb + t][8nt + g].
+template <int D_, int WC_, int MT_, int NT_, int WPL_, int LPC_, int GPL_, bool XS_>
+struct TCCfg {
+  static constexpr int D = D_, WC = WC_, MT = MT_, NT = NT_, WPL = WPL_, LPC = LPC_,
+                       GPL = GPL_;
+  static constexpr bool XS = XS_;
+  static constexpr int S = D / 16;
+  static constexpr int KB = D / 4;
+  static constexpr int NTC = WC / 8;
+  static constexpr int XDBL = 2 * D * D;
+  static constexpr int BDBL = 2 * D * WC;
+  static constexpr int WMAX = 256;  // max expansion terms
+  static constexpr int THREADS = 32 * WPL * LPC;
+  static constexpr int LANE_DBL = 2 * BDBL + (XS ? XDBL : 0) + WMAX;
+  static constexpr size_t SMEM = (size_t)LANE_DBL * LPC * sizeof(double);
+  static_assert(D == WC * GPL, "column blocks must tile D");
+  static_assert((S / MT) * (NTC / NT) == WPL, "warp tiling must cover the block");
+  static_assert(GPL == 1 || LPC == 1, "groups own one lane per CTA");
+};
+
+__host__ __device__ constexpr int xfrag_index(int D, int r, int c, int plane) {
+  // element (r, c) of a D x D matrix in the A-native layout
+  return (((r >> 4) * (D >> 2) + (c >> 2)) * 2 + plane) * 64 + (((r & 7) << 2) | (c & 3)) * 2 +
+         ((r >> 3) & 1);
+}
+
+template <class C>
+__device__ __forceinline__ int bfrag_index(int r, int n, int plane) {
+  return (((r >> 2) * C::NTC + (n >> 3)) * 2 + plane) * 32 + ((n & 7) << 2) + (r & 3);
+}
+
+template <class C>
+__device__ __forceinline__ void lane_sync() {
+  if constexpr (C::WPL == 1) {
+    __syncwarp();
+  } else if constexpr (C::LPC == 1) {
+    __syncthreads();
+  } else {
+    const int lic = (threadIdx.x >> 5) / C::WPL;
+    asm volatile("bar.sync %0, %1;" ::"r"(lic + 1), "r"(C::WPL * 32) : "memory");
+  }
+}
+
+__device__ __forceinline__ void group_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (ld_acquire_gpu(ctr) < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
+    lane_tc_kernel(SliceJob job, const double* __restrict__ terms, int lanes,
+                   double* __restrict__ xglob, unsigned* __restrict__ gctr,
+                   double2* __restrict__ lane_out, double2* __restrict__ prefix_out) {
+  constexpr int D = C::D, WC = C::WC, MT = C::MT, NT = C::NT, KB = C::KB;
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const int lic = warp / C::WPL;
+  const int wil = warp % C::WPL;
+  const int tid_l = threadIdx.x - lic * C::WPL * 32;  // thread index within the lane
+  constexpr int LT = C::WPL * 32;                      // threads per lane
+  const int group = blockIdx.x / C::GPL;
+  const int cb = blockIdx.x % C::GPL;
+  const int lane = group * C::LPC + lic;
+  const bool active = lane < lanes;
+
+  double* base = smem + (size_t)lic * C::LANE_DBL;
+  double* Bbuf[2] = {base, base + C::BDBL};
+  double* Xs = base + 2 * C::BDBL;
+  double* W = Xs + (C::XS ? C::XDBL : 0);
+
+  const int g = ln >> 2, t4 = ln & 3;
+  const int ms0 = (wil % (C::S / MT)) * MT;
+  const int nt0 = (wil / (C::S / MT)) * NT;
+  const int col0 = cb * WC;
+
+  double Vr[MT][NT][4], Vi[MT][NT][4];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
+        const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
+        Vr[i][jn][e] = (r == col0 + n) ? 1.0 : 0.0;
+        Vi[i][jn][e] = 0.0;
+      }
+
+  int64_t s0 = 0, s1 = 0;
+  if (active) lane_range(job.n_slices, lanes, lane, s0, s1);
+  const int T = job.n_terms, m = job.m;
+  const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
+  int p = 0;  // Bbuf[p] = current iterate
+  unsigned iter = 0;
+
+  for (int64_t s = s0; s < s1; ++s, ++iter) {
+    // ---- 1. expansion weights (scaled by 2*scale/beta)
+    for (int tt = tid_l; tt < T; tt += LT)
+      W[tt] = (tt == 0) ? job.xs : job.xs * slice_weight(job, s, tt);
+    lane_sync<C>();
+    // ---- 2. assemble 2X in the A-native layout
+    const double* Xsrc;
+    {
+      double* Xdst;
+      int lo, hi, stride, first;
+      if constexpr (C::XS) {
+        Xdst = Xs;
+        lo = 0;
+        hi = C::XDBL;
+        first = tid_l;
+        stride = LT;
+      } else {
+        Xdst = xglob + ((size_t)group * 2 + (iter & 1)) * C::XDBL;
+        lo = cb * (C::XDBL / C::GPL);
+        hi = lo + C::XDBL / C::GPL;
+        first = threadIdx.x;
+        stride = C::THREADS;
+      }
+      for (int i = lo + 2 * first; i < hi; i += 2 * stride) {
+        double2 h = __ldg(reinterpret_cast<const double2*>(terms + i));
+        double xr = W[0] * h.x, xi = W[0] * h.y;
+        for (int tt = 1; tt < T; ++tt) {
+          h = __ldg(reinterpret_cast<const double2*>(terms + (size_t)tt * C::XDBL + i));
+          xr = fma(W[tt], h.x, xr);
+          xi = fma(W[tt], h.y, xi);
+        }
+        *reinterpret_cast<double2*>(Xdst + i) = make_double2(xr, xi);
+      }
+      Xsrc = C::XS ? Xs : xglob + ((size_t)group * 2 + (iter & 1)) * C::XDBL;
+    }
+    // ---- 3. b_m = a_m V into the current buffer
+    {
+      const double ar = job.coef[2 * m], ai = job.coef[2 * m + 1];
+      double* B = Bbuf[p];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
+            const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
+            const double vr = Vr[i][jn][e], vi = Vi[i][jn][e];
+            B[bfrag_index<C>(r, n, 0)] = ar * vr - ai * vi;
+            B[bfrag_index<C>(r, n, 1)] = ar * vi + ai * vr;
+          }
+    }
+    if constexpr (C::GPL > 1)
+      group_barrier(gctr + group, (iter + 1) * C::GPL);
+    else
+      lane_sync<C>();
+
+    // ---- 4. m Clenshaw steps: new = 2X cur - beta old + a_j V
+    for (int jj = m - 1; jj >= 0; --jj) {
+      const double ar = job.coef[2 * jj], ai = job.coef[2 * jj + 1];
+      const double* Bc = Bbuf[p];
+      double* Bo = Bbuf[p ^ 1];
+      double accR[MT][NT][4], accI[MT][NT][4];
+      const bool first = (jj == m - 1);
+      const double beta = (jj == 0) ? 2.0 : 1.0;
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
+            const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
+            double orr = 0.0, oi = 0.0;
+            if (!first) {
+              orr = Bo[bfrag_index<C>(r, n, 0)];
+              oi = Bo[bfrag_index<C>(r, n, 1)];
+            }
+            const double vr = Vr[i][jn][e], vi = Vi[i][jn][e];
+            accR[i][jn][e] = fma(ar, vr, fma(-ai, vi, -beta * orr));
+            accI[i][jn][e] = fma(ar, vi, fma(ai, vr, -beta * oi));
+          }
+      // MMA over k with a one-step register prefetch of the A fragments
+      double2 aR[MT], aI[MT], nR[MT], nI[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double* xa = Xsrc + ((size_t)((ms0 + i) * KB + 0) * 2) * 64 + 2 * ln;
+        if constexpr (C::XS) {
+          aR[i] = *reinterpret_cast<const double2*>(xa);
+          aI[i] = *reinterpret_cast<const double2*>(xa + 64);
+        } else {
+          aR[i] = __ldcg(reinterpret_cast<const double2*>(xa));
+          aI[i] = __ldcg(reinterpret_cast<const double2*>(xa + 64));
+        }
+      }
+#pragma unroll 2
+      for (int kb = 0; kb < KB; ++kb) {
+        if (kb + 1 < KB) {
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const double* xa = Xsrc + ((size_t)((ms0 + i) * KB + kb + 1) * 2) * 64 + 2 * ln;
+            if constexpr (C::XS) {
+              nR[i] = *reinterpret_cast<const double2*>(xa);
+              nI[i] = *reinterpret_cast<const double2*>(xa + 64);
+            } else {
+              nR[i] = __ldcg(reinterpret_cast<const double2*>(xa));
+              nI[i] = __ldcg(reinterpret_cast<const double2*>(xa + 64));
+            }
+          }
+        }
+        double bR[NT], bI[NT], bN[NT];
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn) {
+          const double* bp = Bc + ((kb * C::NTC + nt0 + jn) * 2) * 32 + ln;
+          bR[jn] = bp[0];
+          bI[jn] = bp[32];
+          bN[jn] = -bI[jn];
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int jn = 0; jn < NT; ++jn) {
+            double* cr = accR[i][jn];
+            double* ci = accI[i][jn];
+            dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aR[i].x, aR[i].y, bR[jn]);
+            dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aR[i].x, aR[i].y, bI[jn]);
+            dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aI[i].x, aI[i].y, bN[jn]);
+            dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aI[i].x, aI[i].y, bR[jn]);
+          }
+        if (kb + 1 < KB) {
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            aR[i] = nR[i];
+            aI[i] = nI[i];
+          }
+        }
+      }
+      if (jj > 0) {
+        // new iterate becomes "cur" for the next step (own positions only)
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
+              const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
+              Bo[bfrag_index<C>(r, n, 0)] = accR[i][jn][e];
+              Bo[bfrag_index<C>(r, n, 1)] = accI[i][jn][e];
+            }
+        p ^= 1;
+        lane_sync<C>();
+      } else {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (phase_one) {
+                Vr[i][jn][e] = accR[i][jn][e];
+                Vi[i][jn][e] = accI[i][jn][e];
+              } else {
+                Vr[i][jn][e] = job.phase[0] * accR[i][jn][e] - job.phase[1] * accI[i][jn][e];
+                Vi[i][jn][e] = job.phase[0] * accI[i][jn][e] + job.phase[1] * accR[i][jn][e];
+              }
+            }
+        // next slice writes b_m into Bbuf[p^1] (only own positions were read
+        // there); flip so that the current buffer of the next slice is it
+        p ^= 1;
+      }
+    }
+    if (prefix_out) {
+      double2* o = prefix_out + (size_t)s * D * D;
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
+            const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
+            o[(size_t)r * D + col0 + n] = make_double2(Vr[i][jn][e], Vi[i][jn][e]);
+          }
+    }
+    // X (smem) and W are rewritten by the next slice
+    if constexpr (C::GPL == 1) lane_sync<C>();
+  }
+  if (active) {
+    double2* o = lane_out + (size_t)lane * D * D;
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
+          const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
+          o[(size_t)r * D + col0 + n] = make_double2(Vr[i][jn][e], Vi[i][jn][e]);
+        }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ordered products of lane / block products
+// ---------------------------------------------------------------------------
+// one level of the reference's level-order fold (propagator.py:91-101):
+// out[i] = in[2i+1] in[2i] (later on the left), odd last copied forward
+__global__ void pair_level_kernel(const double2* __restrict__ in, int cnt, int D,
+                                  double2* __restrict__ out) {
+  const int pairs = cnt >> 1;
+  const int64_t total = (int64_t)(pairs + (cnt & 1)) * D * D;
+  const int64_t dd = (int64_t)D * D;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pi = e / dd;
+    const int rc = (int)(e % dd), r = rc / D, c = rc % D;
+    if (pi < pairs)
+      out[e] = cdot(in + (2 * pi + 1) * dd + (int64_t)r * D, in + 2 * pi * dd, D, c, D);
+    else
+      out[e] = in[(cnt - 1) * dd + rc];
+  }
+}
+
+// single-CTA left fold: E[0] = I, E[l] = M[l-1] E[l-1] (exclusive prefixes,
+// optional) and total = M[cnt-1] ... M[0] written to out.
+__global__ void fold_kernel(const double2* __restrict__ mats, int cnt, int D,
+                            double2* __restrict__ scratch, double2* __restrict__ prefixes,
+                            double2* __restrict__ out) {
+  const int dd = D * D;
+  double2* acc[2] = {scratch, scratch + dd};
+  for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+    const double2 id = make_double2((e / D) == (e % D) ? 1.0 : 0.0, 0.0);
+    acc[0][e] = id;
+    if (prefixes) prefixes[e] = id;
+  }
+  __syncthreads();
+  int cur = 0;
+  for (int l = 0; l < cnt; ++l) {
+    const double2* Ml = mats + (size_t)l * dd;
+    double2* dst = (l == cnt - 1) ? out : acc[cur ^ 1];
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+      const int r = e / D, c = e % D;
+      dst[e] = cdot(Ml + (size_t)r * D, acc[cur], D, c, D);
+    }
+    __syncthreads();
+    if (l == cnt - 1) break;
+    cur ^= 1;
+    if (prefixes)
+      for (int e = threadIdx.x; e < dd; e += blockDim.x)
+        prefixes[(size_t)(l + 1) * dd + e] = acc[cur][e];
+  }
+}
+
+// cumulative products: out[s] = P[s] E[lane(s)] with P[s] the in-lane prefix
+__global__ void apply_prefix_kernel(const double2* __restrict__ P, const double2* __restrict__ E,
+                                    int64_t n, int lanes, int D, double2* __restrict__ out) {
+  const int64_t dd = (int64_t)D * D;
+  const int64_t total = n * dd;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = e / dd;
+    const int rc = (int)(e % dd), r = rc / D, c = rc % D;
+    // lane of slice s under lane_range(): largest l with l*n/lanes <= s
+    int64_t l = ((s + 1) * lanes - 1) / n;
+    while (l > 0 && l * n / lanes > s) --l;
+    while (l + 1 < lanes && (l + 1) * n / lanes <= s) ++l;
+    out[e] = cdot(P + s * dd + (int64_t)r * D, E + l * dd, D, c, D);
+  }
+}
+
+// pad a (cnt, d, d) complex128 batch to (cnt, D, D) by embedding in the
+// top-left corner with an identity tail, and the reverse extraction
+__global__ void embed_kernel(const double2* __restrict__ in, int cnt, int d, int D,
+                             double2* __restrict__ out) {
+  const int64_t total = (int64_t)cnt * D * D;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / ((int64_t)D * D);
+    const int rc = (int)(e % ((int64_t)D * D)), r = rc / D, c = rc % D;
+    out[e] = (r < d && c < d) ? in[k * d * d + r * d + c]
+                              : make_double2(r == c ? 1.0 : 0.0, 0.0);
+  }
+}
+
+__global__ void extract_kernel(const double2* __restrict__ in, int64_t cnt, int D, int d,
+                               int to_fp32, void* __restrict__ out) {
+  const int64_t total = cnt * d * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / ((int64_t)d * d);
+    const int rc = (int)(e % ((int64_t)d * d)), r = rc / d, c = rc % d;
+    const double2 v = in[k * D * D + (int64_t)r * D + c];
+    if (to_fp32)
+      reinterpret_cast<float2*>(out)[e] = make_float2((float)v.x, (float)v.y);
+    else
+      reinterpret_cast<double2*>(out)[e] = v;
+  }
+}
+
+}  // namespace sp

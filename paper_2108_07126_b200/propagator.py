@@ -1,0 +1,376 @@
+"""Equidistant propagation on the B200: the ``create`` / ``IntegratorContext``
+drop-in for the reference ``sliceprop/propagator.py``.
+
+The host keeps the reference's contract — lifecycle created -> loaded ->
+closed (``propagator.py:121-216``), mode resolution (``:175-201``), the
+order of validation (``:238-308``), the global spectral bound and the
+Chebyshev plan (``:258-263``) — and hands the propagation itself to the
+sm_100a library through one C-ABI call (``sp_equiprop`` /
+``sp_equiprop_all``).  There is no CPU path: on a machine without a B200 the
+call raises ``InternalError``.
+
+Result ordering: U = U[n-1] ... U[0] (later slice on the left).  The device
+multiplies slices inside contiguous lanes and then combines the lane
+products in time order, pairwise (tree) or sequentially (left fold) — the
+same products as the reference in a different association, so results agree
+to rounding (tests/test_parity_gpu.py states the tolerances).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._native import MODE, REDUCTION, check, lib
+from .chebyshev import ORDER_GRID, ChebyshevPlan, make_plan
+from .errors import (ConfigError, HermiticityError, SamplingParityError, ShapeError,
+                     StateMachineError)
+from .hamiltonian import (ControlAmplitudes, ControlSystem, Quadrature, check_pair,
+                          simpson_triplets, spectral_bound)
+from .linalg import Precision
+from .magnus import EffectiveSystem, build_effective_system, magnus_bound
+
+__all__ = [
+    "IntegratorContext",
+    "PropagatorResult",
+    "CumulativeResult",
+    "create",
+    "apply",
+]
+
+_CREATED, _LOADED, _CLOSED = "created", "loaded", "closed"
+
+BACKEND_NAME = "b200"
+_BACKEND_TOKENS = ("b200", "cuda", "gpu", "sm_100a")
+
+
+@dataclass(frozen=True)
+class PropagatorResult:
+    """Total propagator plus bookkeeping (``propagator.py:31-41``)."""
+
+    u: np.ndarray
+    slice_count: int
+    plan: dict | None
+
+    @property
+    def dim(self) -> int:
+        return self.u.shape[0]
+
+
+@dataclass(frozen=True)
+class CumulativeResult:
+    """Running products U(t_k <- 0) at every slice boundary
+    (``propagator.py:44-65``).  ``u_all[-1]`` equals the sequential-reduction
+    total of the same call bit for bit."""
+
+    u_all: np.ndarray
+    slice_count: int
+    plan: dict | None
+
+    @property
+    def dim(self) -> int:
+        return self.u_all.shape[1]
+
+    @property
+    def final(self) -> np.ndarray:
+        if self.slice_count == 0:
+            return np.eye(self.dim, dtype=self.u_all.dtype)
+        return self.u_all[-1]
+
+
+def apply(u, state) -> np.ndarray:
+    """Propagate a state vector (U psi) or a density matrix (U rho U^+)
+    (``propagator.py:105-118``)."""
+    m = u.u if isinstance(u, PropagatorResult) else np.asarray(u)
+    if m.ndim != 2 or m.shape[0] != m.shape[1]:
+        raise ShapeError(f"propagator must be a square matrix, got shape {m.shape}")
+    d = m.shape[0]
+    state = np.asarray(state)
+    if state.shape == (d,):
+        return m @ state
+    if state.shape == (d, d):
+        return m @ state @ m.conj().T
+    raise ShapeError(
+        f"state shape {state.shape} matches neither a vector ({d},) "
+        f"nor a density matrix ({d}, {d})")
+
+
+class IntegratorContext:
+    """Stateful propagation session bound to one B200 (``propagator.py:132-331``).
+
+    Use :func:`create`.  Owns one native context (device scratch, stream);
+    independent contexts may coexist.  Not thread-safe, not reentrant.
+    """
+
+    def __init__(self, precision: Precision, m_max: int | None, checked: bool, device: int):
+        self.precision = precision
+        self.m_max = m_max
+        self.checked = checked
+        self.device = device
+        self.backend = BACKEND_NAME
+        self._state = _CREATED
+        self._system: ControlSystem | None = None
+        self._effective: EffectiveSystem | None = None
+        self._magnus = False
+        self._quadrature = Quadrature.MIDPOINT
+        handle = ctypes.c_void_p()
+        check(lib.sp_create(ctypes.byref(handle), precision.bits, int(device)))
+        self._handle = handle
+
+    # -- lifecycle ---------------------------------------------------------
+    @property
+    def state(self) -> str:
+        return self._state
+
+    @property
+    def magnus(self) -> bool:
+        return self._magnus
+
+    @property
+    def quadrature(self) -> Quadrature:
+        return self._quadrature
+
+    @property
+    def mode(self) -> str:
+        if self._magnus:
+            return "magnus"
+        return self._quadrature.value
+
+    def _require_open(self) -> None:
+        if self._state == _CLOSED:
+            raise StateMachineError("context is closed")
+
+    def _require_loaded(self) -> None:
+        self._require_open()
+        if self._state != _LOADED:
+            raise StateMachineError("no Hamiltonian loaded; call set_hamiltonian first")
+
+    def set_hamiltonian(self, system: ControlSystem, magnus: bool = False,
+                        quadrature=None) -> None:
+        """Load (or replace) the system; resolves the slicing mode
+        (``propagator.py:175-201``)."""
+        self._require_open()
+        if not isinstance(system, ControlSystem):
+            raise ShapeError(f"expected a ControlSystem, got {type(system).__name__}")
+        magnus = bool(magnus)
+        if quadrature is None:
+            quadrature = Quadrature.SIMPSON if magnus else Quadrature.MIDPOINT
+        quadrature = Quadrature.parse(quadrature)
+        if magnus and quadrature is Quadrature.MIDPOINT:
+            raise ConfigError("the fourth-order mode requires the three-point "
+                              "quadrature; midpoint sampling cannot feed it")
+        effective = build_effective_system(system) if magnus else None
+        terms = effective.terms() if magnus else system.terms()
+        stacked = np.ascontiguousarray(np.stack(terms), dtype=np.complex128)
+        mode = "magnus" if magnus else quadrature.value
+        check(lib.sp_set_hamiltonian(self._handle, system.dim, system.n_controls,
+                                     len(terms), MODE[mode],
+                                     stacked.ctypes.data_as(ctypes.c_void_p)), self._handle)
+        self._system = system
+        self._effective = effective
+        self._magnus = magnus
+        self._quadrature = quadrature
+        self._state = _LOADED
+
+    def close(self) -> None:
+        """Release device storage; further calls raise.  Idempotent."""
+        if getattr(self, "_handle", None) is not None and self._handle.value:
+            lib.sp_free(self._handle)
+            self._handle = ctypes.c_void_p()
+        self._system = None
+        self._effective = None
+        self._state = _CLOSED
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self) -> "IntegratorContext":
+        return self
+
+    def __exit__(self, exc_type, exc, tb) -> None:
+        self.close()
+
+    # -- host-side preparation (validation order of propagator.py:238-263) --
+    def slice_count(self, pts: int) -> int:
+        if self._quadrature is Quadrature.SIMPSON:
+            if pts < 3 or pts % 2 == 0:
+                raise SamplingParityError(
+                    f"three-point quadrature needs an odd number of samples >= 3, got {pts}")
+            return (pts - 1) // 2
+        return pts
+
+    def bound(self, dt: float) -> float:
+        """Global spectral bound beta for sample step dt (alpha = -beta)."""
+        if self._magnus:
+            return magnus_bound(self._effective, dt)
+        step = dt if self._quadrature is Quadrature.MIDPOINT else 2.0 * dt
+        return spectral_bound(self._system, step)
+
+    def plan_for(self, dt: float) -> ChebyshevPlan:
+        beta = self.bound(dt)
+        return make_plan(-beta, beta, self.precision, m_max=self.m_max)
+
+    def _prepare(self, amps: ControlAmplitudes):
+        self._require_loaded()
+        if not isinstance(amps, ControlAmplitudes):
+            raise ShapeError(f"expected ControlAmplitudes, got {type(amps).__name__}")
+        count = self.slice_count(amps.pts)
+        check_pair(self._system, amps)
+        plan = self.plan_for(amps.dt)
+        if self.checked:
+            self._check_hermitian(amps)
+        return count, plan
+
+    def _check_hermitian(self, amps: ControlAmplitudes) -> None:
+        """checked=True: Hermiticity of every slice exponent in the working
+        precision, tolerance 100 u max(1, max|G| d) (``chebyshev.py:249-256``).
+        Host-side validation only; the propagation still runs on the GPU."""
+        cdt = self.precision.complex_dtype
+        terms = [np.asarray(t).astype(cdt) for t in
+                 (self._effective.terms() if self._magnus else self._system.terms())]
+        v = amps.values
+        if self._magnus:
+            from .magnus import magnus_coefficients
+            scale = 2.0 * amps.dt
+            table = magnus_coefficients(amps) / scale
+        elif self._quadrature is Quadrature.SIMPSON:
+            c1, c2, c3 = simpson_triplets(v)
+            scale = 2.0 * amps.dt
+            table = (c1 + 4.0 * c2 + c3) / 6.0
+        else:
+            scale = amps.dt
+            table = v
+        d = self._system.dim
+        flat = np.stack([t.reshape(d * d) for t in terms])
+        asym_t = np.stack([(t - t.conj().T).reshape(d * d) for t in terms])
+        asym = gmax = 0.0
+        step = max(1, (1 << 20) // max(1, d * d))
+        for lo in range(0, table.shape[0], step):
+            w = np.column_stack([np.ones(min(step, table.shape[0] - lo)),
+                                 table[lo:lo + step]]).astype(cdt)
+            g = scale * (w @ flat)
+            a = scale * (w @ asym_t)
+            gmax = max(gmax, float(np.abs(g).max()))
+            asym = max(asym, float(np.abs(a).max()))
+        tol = 100.0 * self.precision.roundoff * max(1.0, gmax * d)
+        if asym > tol:
+            raise HermiticityError(
+                f"exponent batch asymmetry {asym:.3g} exceeds tolerance {tol:.3g}")
+
+    # -- propagation --------------------------------------------------------
+    def _out_dtype(self):
+        return self.precision.complex_dtype
+
+    def equiprop(self, amps: ControlAmplitudes, reduction: str = "pairwise") -> PropagatorResult:
+        """Total propagator over the sampled window (``propagator.py:279-308``)."""
+        if reduction not in REDUCTION:
+            raise ConfigError(f"unknown reduction {reduction!r}; expected pairwise or sequential")
+        self._require_loaded()
+        if not isinstance(amps, ControlAmplitudes):
+            raise ShapeError(f"expected ControlAmplitudes, got {type(amps).__name__}")
+        d = self._system.dim
+        if amps.pts == 0:
+            return PropagatorResult(u=np.eye(d, dtype=self._out_dtype()), slice_count=0,
+                                    plan=None)
+        count, plan = self._prepare(amps)
+        out = np.empty((d, d), dtype=self._out_dtype())
+        native = plan.to_native()
+        check(lib.sp_equiprop(self._handle, amps.values.ctypes.data_as(ctypes.c_void_p),
+                              amps.pts, amps.n_controls, amps.dt, ctypes.byref(native),
+                              REDUCTION[reduction], out.ctypes.data_as(ctypes.c_void_p)),
+              self._handle)
+        return PropagatorResult(u=out, slice_count=count, plan=plan.summary())
+
+    def equiprop_all(self, amps: ControlAmplitudes) -> CumulativeResult:
+        """Cumulative propagators at every slice boundary (``propagator.py:310-331``)."""
+        self._require_loaded()
+        if not isinstance(amps, ControlAmplitudes):
+            raise ShapeError(f"expected ControlAmplitudes, got {type(amps).__name__}")
+        d = self._system.dim
+        if amps.pts == 0:
+            return CumulativeResult(u_all=np.zeros((0, d, d), dtype=self._out_dtype()),
+                                    slice_count=0, plan=None)
+        count, plan = self._prepare(amps)
+        out = np.empty((count, d, d), dtype=self._out_dtype())
+        native = plan.to_native()
+        check(lib.sp_equiprop_all(self._handle, amps.values.ctypes.data_as(ctypes.c_void_p),
+                                  amps.pts, amps.n_controls, amps.dt, ctypes.byref(native),
+                                  out.ctypes.data_as(ctypes.c_void_p)), self._handle)
+        return CumulativeResult(u_all=out, slice_count=count, plan=plan.summary())
+
+    # -- device-resident entry (bench / multi-GPU sharding) -------------------
+    def equiprop_device_ptr(self, amps_ptr: int, pts: int, n_ctrl: int, dt: float,
+                            out_ptr: int, stream: int = 0, reduction: str = "pairwise",
+                            plan: ChebyshevPlan | None = None) -> dict:
+        """Asynchronous propagation of a device-resident (pts, n_ctrl) float64
+        table into a device d x d output (working dtype).  The caller owns
+        amplitude validation (see ``sharding.equiprop_tensor``)."""
+        self._require_loaded()
+        if reduction not in REDUCTION:
+            raise ConfigError(f"unknown reduction {reduction!r}; expected pairwise or sequential")
+        if n_ctrl != self._system.n_controls:
+            raise ShapeError(f"amplitude table has {n_ctrl} controls, "
+                             f"system has {self._system.n_controls}")
+        count = self.slice_count(pts) if pts else 0
+        plan = plan or self.plan_for(dt)
+        native = plan.to_native()
+        check(lib.sp_equiprop_device(self._handle, ctypes.c_void_p(amps_ptr), int(pts),
+                                     int(n_ctrl), float(dt), ctypes.byref(native),
+                                     REDUCTION[reduction], ctypes.c_void_p(out_ptr),
+                                     ctypes.c_void_p(stream)), self._handle)
+        return {"slice_count": count, "plan": plan.summary()}
+
+    def product_device_ptr(self, count: int, mats_ptr: int, out_ptr: int, stream: int = 0,
+                           reduction: str = "pairwise") -> None:
+        """Ordered product mats[count-1] ... mats[0] of device complex128 d x d
+        matrices (multi-GPU gather step)."""
+        self._require_loaded()
+        check(lib.sp_product_device(self._handle, int(count), ctypes.c_void_p(mats_ptr),
+                                    REDUCTION[reduction], ctypes.c_void_p(out_ptr),
+                                    ctypes.c_void_p(stream)), self._handle)
+
+    def set_profiling(self, enabled: bool = True) -> None:
+        check(lib.sp_set_profiling(self._handle, int(bool(enabled))), self._handle)
+
+    def last_timing(self) -> dict:
+        ms = ctypes.c_double()
+        launches = ctypes.c_int()
+        flops = ctypes.c_double()
+        name = ctypes.create_string_buffer(128)
+        check(lib.sp_last_timing(self._handle, ctypes.byref(ms), ctypes.byref(launches),
+                                 ctypes.byref(flops), name, 128), self._handle)
+        return {"main_kernel_ms": ms.value, "launches": launches.value,
+                "executed_flops": flops.value, "kernel": name.value.decode()}
+
+
+def _default_device() -> int:
+    for key in ("SLICEPROP_DEVICE", "LOCAL_RANK"):
+        if os.environ.get(key, "").isdigit():
+            return int(os.environ[key])
+    return 0
+
+
+def create(precision="fp64", m_max: int | None = None, checked: bool = False,
+           backend=None, device: int | None = None) -> IntegratorContext:
+    """New propagation context on one B200 (``propagator.py:334-355``).
+
+    precision "fp32" | "fp64"; m_max pins the series order (odd 3..25);
+    checked enables the Hermiticity sanity pass.  backend accepts None or a
+    GPU token ("b200", "cuda", "gpu", "sm_100a") — the reference's "cpu"
+    backend is not offered: this package has no CPU path.
+    """
+    precision = Precision.parse(precision)
+    if m_max is not None and m_max not in ORDER_GRID:
+        raise ConfigError(f"m_max override {m_max} not an odd integer in "
+                          f"{ORDER_GRID[0]}..{ORDER_GRID[-1]}")
+    if backend is not None:
+        if not isinstance(backend, str) or backend.lower() not in _BACKEND_TOKENS:
+            raise ConfigError(f"unknown backend {backend!r}; expected one of {_BACKEND_TOKENS}")
+    return IntegratorContext(precision, m_max, bool(checked),
+                             _default_device() if device is None else int(device))

@@ -1,0 +1,95 @@
+"""GPU parity: the sm_100a path (through the public API, i.e. the C ABI)
+against the reference outputs committed in tests/golden/ and against the CPU
+oracle on the same seeded inputs.
+
+Tolerance: rel-Frobenius(U_gpu, U_ref) <= max(floor,
+4 eps_self), floor = 1e-12 (complex128) / 1e-5 (complex64), eps_self = the
+reference's own pairwise-vs-sequential difference on the same input.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from cases import CASES, CONVERGE_PTS, build_inputs, input_digest
+from helpers import parity_tolerance, rel_fro
+
+import paper_2108_07126_b200 as sp
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _run(case, reduction="pairwise"):
+    h0, hs, values, dt = build_inputs(case)
+    mode = case["mode"]
+    ctx = sp.create(precision=case["precision"], m_max=case.get("m_max"))
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                        quadrature=None if mode == "magnus" else mode)
+    amps = sp.ControlAmplitudes(values, dt)
+    res = ctx.equiprop(amps, reduction=reduction)
+    return ctx, amps, res, (h0, hs, values, dt)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_equiprop_matches_reference(case, golden):
+    key = case["name"]
+    ctx, amps, res, inputs = _run(case)
+    assert bytes(golden[f"{key}__digest"]) == input_digest(*inputs)
+    u_ref = golden[f"{key}__u"]
+    tol, eps_self = parity_tolerance(u_ref, golden[f"{key}__u_seq"], case["precision"])
+    err = rel_fro(res.u, u_ref)
+    assert res.u.dtype == u_ref.dtype
+    assert res.slice_count == int(golden[f"{key}__slice_count"])
+    if f"{key}__m_max" in golden.files:
+        assert res.plan["m_max"] == int(golden[f"{key}__m_max"])
+        assert res.plan["beta"] == pytest.approx(float(golden[f"{key}__beta"]), rel=1e-15)
+    assert err <= tol, f"{key}: err {err:.3e} > tol {tol:.3e} (eps_self {eps_self:.3e})"
+    # sequential reduction obeys the same gate
+    u_seq = ctx.equiprop(amps, reduction="sequential").u
+    assert rel_fro(u_seq, u_ref) <= tol
+    if case.get("cumulative"):
+        cum = ctx.equiprop_all(amps)
+        ref_all = golden[f"{key}__u_all"]
+        assert cum.u_all.shape == ref_all.shape
+        for k in range(ref_all.shape[0]):
+            assert rel_fro(cum.u_all[k], ref_all[k]) <= tol, k
+        # reference property propagator.py:304-306: last entry == sequential
+        assert np.array_equal(cum.final, u_seq)
+    ctx.close()
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "random"][:12],
+                         ids=lambda c: c["name"])
+def test_deterministic(case):
+    ctx, amps, res, _ = _run(case)
+    again = ctx.equiprop(amps).u
+    assert np.array_equal(res.u, again)
+    ctx.close()
+
+
+def test_convergence_orders_reproduced():
+    """C2: the dt sweep of the driven qubit on the GPU reproduces the
+    reference's errors where truncation dominates and its fitted orders
+    (bands of reference test_acceptance.py:133-145)."""
+    with open(os.path.join(HERE, "golden", "converge.json")) as fh:
+        gold = json.load(fh)
+    problem = sp.DrivenQubit(1.0, 0.1, 1.0, 6.0)
+    bands = {"midpoint": (1.9, 2.2), "simpson": (1.9, 2.2), "magnus": (3.7, 4.3)}
+    for label, magnus, quad in [("midpoint", False, "midpoint"),
+                                ("simpson", False, "simpson"),
+                                ("magnus", True, None)]:
+        rows = sp.convergence_sweep(problem, CONVERGE_PTS, magnus=magnus, quadrature=quad)
+        pts = [p for p, _ in rows]
+        errs = np.array([e for _, e in rows])
+        ref = np.array(gold[label]["errors"])
+        assert pts == gold[label]["pts"]
+        # truncation-dominated points agree to 1e-4 relative (+ roundoff floor)
+        assert np.all(np.abs(errs - ref) <= 1e-4 * ref + 5e-11), (label, errs, ref)
+        order, _ = sp.fit_convergence_order(pts, errs)
+        lo, hi = bands[label]
+        assert lo <= order <= hi, (label, order)
+        assert abs(order - gold[label]["order"]) < 0.05, (label, order, gold[label]["order"])

@@ -1,0 +1,35 @@
+"""Quick GPU probe: time the lane kernel per family (CUDA events inside the library)."""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden"))
+import numpy as np
+import paper_2108_07126_b200 as sp
+from cases import random_inputs, qubit_inputs
+
+PEAK = 37.0e12
+def run(label, h0, hs, v, dt, mode="midpoint", reps=3):
+    ctx = sp.create(); ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                                           quadrature=None if mode == "magnus" else mode)
+    ctx.set_profiling(True)
+    amps = sp.ControlAmplitudes(v, dt)
+    r = ctx.equiprop(amps)
+    best = 1e9; wall = 1e9
+    for _ in range(reps):
+        t0 = time.perf_counter(); ctx.equiprop(amps); wall = min(wall, time.perf_counter() - t0)
+        t = ctx.last_timing(); best = min(best, t["main_kernel_ms"])
+    n = r.slice_count; m = r.plan["m_max"]; d = h0.shape[0]
+    canon = n * (8 * d**3 * (m + 1) + 4 * d * d * (len(hs) + 1))
+    print(f"{label}: n={n} m={m} kernel {best:.3f} ms ({t['kernel']}), wall {wall*1e3:.2f} ms, "
+          f"slices/s {n/(best/1e3):.3e}, canon TF {canon/(best/1e3)/1e12:.2f} ({canon/(best/1e3)/PEAK*100:.1f}%), "
+          f"exec TF {t['executed_flops']/(best/1e3)/1e12:.2f}, launches {t['launches']}", flush=True)
+    ctx.close()
+
+run("d2 qubit 1e5", *qubit_inputs(100000, "midpoint"))
+run("d2 qubit 1e6", *qubit_inputs(1000000, "midpoint"))
+run("d2 rand 1e6", *random_inputs(2, 2, 1000000, 1))
+run("d4 rand 1e6", *random_inputs(4, 2, 1000000, 1))
+run("d16 rand 1e5", *random_inputs(16, 2, 100000, 1))
+run("d32 rand 1e5", *random_inputs(32, 2, 100000, 1))
+run("d64 rand 2e4", *random_inputs(64, 2, 20000, 1))
+run("d128 rand 4e3", *random_inputs(128, 4, 4000, 1))
+run("d256 rand 500", *random_inputs(256, 4, 500, 1))
