@@ -236,19 +236,22 @@ int tc_launch(sp_ctx* ctx, const SliceJob& job, int lanes, double2* lane_out,
     rc = ensure(ctx, ctx->gctr, (size_t)groups * sizeof(unsigned));
     if (rc) return rc;
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->gctr.p, 0, (size_t)groups * sizeof(unsigned), st));
-    ++ctx->launches;
     xg = (double*)ctx->xglob.p;
     ctr = (unsigned*)ctx->gctr.p;
     const double* terms = (const double*)ctx->terms.p;
     void* args[] = {(void*)&job, (void*)&terms, (void*)&lanes, (void*)&xg,
                     (void*)&ctr,  (void*)&lane_out, (void*)&prefix_out};
+    // co-residency of a lane's GPL CTAs is required by the group barrier
+    if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
     CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)lane_tc_kernel<C>, dim3(grid),
                                               dim3(C::THREADS), args, C::SMEM, st));
   } else {
+    if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
     lane_tc_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(
         job, (const double*)ctx->terms.p, lanes, xg, ctr, lane_out, prefix_out);
   }
   CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
   ++ctx->launches;
   return SP_OK;
 }
@@ -367,7 +370,6 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   int rc = ensure(ctx, ctx->lanes, (size_t)lanes * dd * sizeof(double2));
   if (rc) return rc;
   double2* lane_out = (double2*)ctx->lanes.p;
-  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
   switch (ctx->fam) {
     case FAM_T16: rc = tc_launch<Cfg16>(ctx, job, lanes, lane_out, prefix_out, st); break;
     case FAM_T32: rc = tc_launch<Cfg32>(ctx, job, lanes, lane_out, prefix_out, st); break;
@@ -376,7 +378,6 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     case FAM_T256: rc = tc_launch<Cfg256>(ctx, job, lanes, lane_out, prefix_out, st); break;
   }
   if (rc) return rc;
-  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
   *prods = lane_out;
   *count = lanes;
   return SP_OK;
@@ -455,10 +456,11 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
   const double2* total = nullptr;
   if (job.n_slices == 0) {
     // empty product (propagator.py:297-299)
-    std::vector<double2> eye(dd, make_double2(0.0, 0.0));
-    for (int i = 0; i < D; ++i) eye[(size_t)i * D + i].x = 1.0;
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->result.p, eye.data(), dd * sizeof(double2),
-                                  cudaMemcpyHostToDevice, st));
+    // identity (embed of a 0 x 0 block)
+    embed_kernel<<<grid_for((int64_t)dd, 256), 256, 0, st>>>(nullptr, 1, 0, D,
+                                                              (double2*)ctx->result.p);
+    CUDA_TRY(ctx, cudaGetLastError());
+    ++ctx->launches;
     total = (const double2*)ctx->result.p;
   } else {
     const bool small = ctx->fam == FAM_S2 || ctx->fam == FAM_S4;
@@ -500,17 +502,20 @@ int product_dev(sp_ctx* ctx, int count, const double2* d_mats, int reduction, vo
   if (rc) return rc;
   double2* padded = (double2*)ctx->cumP.p;
   if (count == 0) {
-    std::vector<double2> eye(dd, make_double2(0.0, 0.0));
-    for (int i = 0; i < D; ++i) eye[(size_t)i * D + i].x = 1.0;
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->result.p, eye.data(), dd * sizeof(double2),
-                                  cudaMemcpyHostToDevice, st));
+    // identity (embed of a 0 x 0 block)
+    embed_kernel<<<grid_for((int64_t)dd, 256), 256, 0, st>>>(nullptr, 1, 0, D,
+                                                              (double2*)ctx->result.p);
+    CUDA_TRY(ctx, cudaGetLastError());
+    ++ctx->launches;
     extract_kernel<<<grid_for((int64_t)d * d, 256), 256, 0, st>>>(
         (const double2*)ctx->result.p, 1, D, d, ctx->bits == 32, d_out);
     CUDA_TRY(ctx, cudaGetLastError());
+    ++ctx->launches;
     return SP_OK;
   }
   embed_kernel<<<grid_for((int64_t)count * dd, 256), 256, 0, st>>>(d_mats, count, d, D, padded);
   CUDA_TRY(ctx, cudaGetLastError());
+  ++ctx->launches;
   const double2* total = nullptr;
   if (reduction == SP_REDUCE_PAIRWISE) {
     rc = reduce_pairwise_dev(ctx, padded, count, D, st, &total);
@@ -521,11 +526,13 @@ int product_dev(sp_ctx* ctx, int count, const double2* d_mats, int reduction, vo
     fold_kernel<<<1, 1024, 0, st>>>(padded, count, D, (double2*)ctx->fold_scratch.p, nullptr,
                                      (double2*)ctx->result.p);
     CUDA_TRY(ctx, cudaGetLastError());
+    ++ctx->launches;
     total = (const double2*)ctx->result.p;
   }
   extract_kernel<<<grid_for((int64_t)d * d, 256), 256, 0, st>>>(total, 1, D, d,
                                                                 ctx->bits == 32, d_out);
   CUDA_TRY(ctx, cudaGetLastError());
+  ++ctx->launches;
   return SP_OK;
 }
 
