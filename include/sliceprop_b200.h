@@ -102,7 +102,8 @@ int sp_set_hamiltonian(sp_ctx* ctx, int dim, int n_ctrl, int n_terms, int mode,
 int sp_equiprop(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
                 const sp_plan* plan, int reduction, void* u_out);
 /* same, device-resident: d_amps and d_u_out are device pointers, stream a
- * cudaStream_t (NULL = the context stream).  Asynchronous. */
+ * cudaStream_t (NULL = the CUDA default stream); stream-ordered with the
+ * caller's own work, asynchronous.  The caller owns amplitude validation. */
 int sp_equiprop_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
                        double dt, const sp_plan* plan, int reduction, void* d_u_out,
                        void* stream);

@@ -647,7 +647,7 @@ int sp_equiprop_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctr
     return fail(ctx, SP_E_CONFIG, "unknown reduction %d", reduction);
   rc = prepare_device(ctx);
   if (rc) return rc;
-  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = the CUDA default stream
   return equiprop_dev(ctx, d_amps, pts, n_ctrl, dt, plan, reduction, d_u_out, st);
 }
 
@@ -742,7 +742,7 @@ int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction,
   if (count < 0) return fail(ctx, SP_E_SHAPE, "negative count");
   rc = prepare_device(ctx);
   if (rc) return rc;
-  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  cudaStream_t st = (cudaStream_t)stream;  // NULL = the CUDA default stream
   return product_dev(ctx, count, (const double2*)d_mats, reduction, d_out, st);
 }
 

@@ -480,6 +480,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           bI[jn] = bp[32];
           bN[jn] = -bI[jn];
         }
+        // two passes so that MMAs into the same accumulator are 2*MT*NT
+        // instructions apart (hides the DMMA latency without more warps)
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -488,6 +490,13 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             double* ci = accI[i][jn];
             dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aR[i].x, aR[i].y, bR[jn]);
             dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aR[i].x, aR[i].y, bI[jn]);
+          }
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int jn = 0; jn < NT; ++jn) {
+            double* cr = accR[i][jn];
+            double* ci = accI[i][jn];
             dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aI[i].x, aI[i].y, bN[jn]);
             dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aI[i].x, aI[i].y, bR[jn]);
           }
