@@ -120,6 +120,15 @@ int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction,
  * (propagator.py:245-252); SP_E_SAMPLING_PARITY for even/short 3-point tables */
 int sp_slice_count(const sp_ctx* ctx, int64_t pts, int64_t* out);
 
+/* ---- evaluation scheme of the slice series ------------------------------
+ * 0 auto (Paterson-Stockmeyer in the Chebyshev basis whenever it needs fewer
+ * GEMMs per slice than the reference's Clenshaw recurrence), 1 Clenshaw
+ * (chebyshev.py:298-303 order of operations, applied to the running
+ * product), 2 Paterson-Stockmeyer.  Same plan and same truncated polynomial
+ * in every case; only the rounding differs. */
+int sp_set_algorithm(sp_ctx* ctx, int algo);
+int sp_last_algorithm(const sp_ctx* ctx, int* algo, int* gemms_per_slice);
+
 /* ---- measurement hooks ------------------------------------------------ */
 /* when enabled, the next propagations record CUDA events around the main
  * lane kernel; sp_last_timing returns its duration (ms), the number of

@@ -1,6 +1,8 @@
 """Build the sm_100a C-ABI library in-tree (no JIT cache, travels with gpurun).
 
-    python -m paper_2108_07126_b200.build        # or __graft_entry__.build()
+    python paper_2108_07126_b200/build.py        # or __graft_entry__.build()
+
+(run it as a file: importing the package first would load the old library)
 
 Produces ``paper_2108_07126_b200/libsliceprop_b200.so`` from
 ``csrc/engine.cu`` (kernels + C ABI) and ``csrc/plan.cpp`` (host plan), with
@@ -21,7 +23,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsliceprop_b200.so")
 SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "plan.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "internal.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "kernels_ps.cuh",
+                                                  "internal.h")] + [
     os.path.join(ROOT, "include", "sliceprop_b200.h")]
 
 NVCC_FLAGS = [

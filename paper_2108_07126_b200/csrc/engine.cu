@@ -16,6 +16,7 @@
 
 #include "internal.h"
 #include "kernels.cuh"
+#include "kernels_ps.cuh"
 
 using namespace sp;
 
@@ -32,6 +33,72 @@ using Cfg32 = TCCfg<32, 32, 1, 2, 4, 1, 1, true>;
 using Cfg64 = TCCfg<64, 64, 1, 4, 8, 1, 1, true>;
 using Cfg128 = TCCfg<128, 32, 1, 4, 8, 1, 4, false>;
 using Cfg256 = TCCfg<256, 16, 2, 2, 8, 1, 16, false>;
+// Paterson-Stockmeyer configurations (A operands: smem for D <= 32, else L2)
+using PS16 = PSCfg<16, 16, 1, 2, 1, 4, 1, true>;
+using PS32 = PSCfg<32, 32, 1, 2, 4, 1, 1, true>;
+using PS64 = PSCfg<64, 32, 1, 4, 4, 1, 2, false>;
+using PS128 = PSCfg<128, 32, 1, 4, 8, 1, 4, false>;
+using PS256 = PSCfg<256, 16, 2, 2, 8, 1, 16, false>;
+
+enum Algo { ALGO_AUTO = 0, ALGO_CLENSHAW = 1, ALGO_PS = 2 };
+
+// GEMMs per slice: Clenshaw m; PS (s-1) + (r-1) + 1, r = ceil((m+1)/s)
+int ps_cost(int m, int s) {
+  const int r = (m + 1 + s - 1) / s;
+  return (s - 1) + (r - 1) + 1;
+}
+
+int ps_choose(int m) {
+  int best = 0, cost = m;
+  for (int s = 2; s <= 6; ++s) {
+    const int r = (m + 1 + s - 1) / s;
+    if (r < 2 || r * s > PS_MAXC) continue;
+    if (ps_cost(m, s) < cost) {
+      cost = ps_cost(m, s);
+      best = s;
+    }
+  }
+  return best;  // 0: no saving over Clenshaw
+}
+
+// alpha_{j,i} of p = sum_j Q_j T_j(T_s), Q_j = sum_i alpha_{j,i} T_i, from
+// the plan's Chebyshev coefficients a'_0 = a_0, a'_k = 2 a_k (the
+// reference series p = a_0 + 2 sum a_k T_k), by the top-down solve of
+// T_i T_js = (T_{js+i} + T_{|js-i|}) / 2; 80-bit accumulation.
+void ps_coefficients(const double* coef, int m, int s, double* alpha, int* r_out) {
+  typedef long double ld;
+  const int r = (m + 1 + s - 1) / s;
+  std::vector<ld> ar((r + 1) * s, 0.0L), ai((r + 1) * s, 0.0L);
+  auto apr = [&](int k) -> ld { return k > m ? 0.0L : (k == 0 ? 1.0L : 2.0L) * (ld)coef[2 * k]; };
+  auto api = [&](int k) -> ld {
+    return k > m ? 0.0L : (k == 0 ? 1.0L : 2.0L) * (ld)coef[2 * k + 1];
+  };
+  for (int j = r - 1; j >= 0; --j)
+    for (int i = 0; i < s; ++i) {
+      const int k = j * s + i;
+      ld vr, vi;
+      if (j >= 1 && i >= 1) {
+        vr = 2.0L * apr(k) - ar[(j + 1) * s + (s - i)];
+        vi = 2.0L * api(k) - ai[(j + 1) * s + (s - i)];
+      } else if (j >= 1) {
+        vr = apr(k);
+        vi = api(k);
+      } else if (i >= 1) {
+        vr = apr(i) - ar[1 * s + (s - i)] / 2.0L;
+        vi = api(i) - ai[1 * s + (s - i)] / 2.0L;
+      } else {
+        vr = apr(0);
+        vi = api(0);
+      }
+      ar[j * s + i] = vr;
+      ai[j * s + i] = vi;
+    }
+  for (int q = 0; q < r * s; ++q) {
+    alpha[2 * q] = (double)ar[q];
+    alpha[2 * q + 1] = (double)ai[q];
+  }
+  *r_out = r;
+}
 
 int family_for(int d, int* D) {
   if (d <= 2) { *D = 2; return FAM_S2; }
@@ -45,7 +112,16 @@ int family_for(int d, int* D) {
   return FAM_NONE;
 }
 
-const char* family_kernel_name(int fam) {
+const char* family_kernel_name(int fam, int algo) {
+  if (algo == 2) {
+    switch (fam) {
+      case FAM_T16: return "lane_ps_kernel<D16>";
+      case FAM_T32: return "lane_ps_kernel<D32>";
+      case FAM_T64: return "lane_ps_kernel<D64,group2>";
+      case FAM_T128: return "lane_ps_kernel<D128,group4>";
+      case FAM_T256: return "lane_ps_kernel<D256,group16>";
+    }
+  }
   switch (fam) {
     case FAM_S2: return "lane_small_kernel<2,1>";
     case FAM_S4: return "lane_small_kernel<4,4>";
@@ -80,7 +156,10 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   int fam = FAM_NONE, D = 0;
   DevBuf terms, amps, lanes, ctab, tree0, tree1, xglob, gctr, result, out, cumP, cumE, cumO,
-      fold_scratch;
+      fold_scratch, psA, tpriv;
+  int algo = 0;          // Algo
+  int last_algo = 0;     // algorithm of the last lane pass
+  int last_gemms = 0;    // GEMMs per slice of the last lane pass
   // profiling
   bool prof = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -156,6 +235,9 @@ int tc_prepare(sp_ctx* ctx) {
   return SP_OK;
 }
 
+template <class C>
+int ps_prepare(sp_ctx* ctx);
+
 // permute + pad the host terms into the family's device layout
 int upload_terms(sp_ctx* ctx) {
   const int d = ctx->dim, D = ctx->D, T = ctx->n_terms;
@@ -191,6 +273,15 @@ int upload_terms(sp_ctx* ctx) {
     case FAM_T64: rc = tc_prepare<Cfg64>(ctx); break;
     case FAM_T128: rc = tc_prepare<Cfg128>(ctx); break;
     case FAM_T256: rc = tc_prepare<Cfg256>(ctx); break;
+    default: break;
+  }
+  if (rc) return rc;
+  switch (ctx->fam) {
+    case FAM_T16: rc = ps_prepare<PS16>(ctx); break;
+    case FAM_T32: rc = ps_prepare<PS32>(ctx); break;
+    case FAM_T64: rc = ps_prepare<PS64>(ctx); break;
+    case FAM_T128: rc = ps_prepare<PS128>(ctx); break;
+    case FAM_T256: rc = ps_prepare<PS256>(ctx); break;
     default: break;
   }
   if (rc) return rc;
@@ -249,6 +340,61 @@ int tc_launch(sp_ctx* ctx, const SliceJob& job, int lanes, double2* lane_out,
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
     lane_tc_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(
         job, (const double*)ctx->terms.p, lanes, xg, ctr, lane_out, prefix_out);
+  }
+  CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+  ++ctx->launches;
+  return SP_OK;
+}
+
+template <class C>
+int ps_prepare(sp_ctx* ctx) {
+  CUDA_TRY(ctx, cudaFuncSetAttribute(lane_ps_kernel<C>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)C::SMEM));
+  return SP_OK;
+}
+
+template <class C>
+int ps_lanes(sp_ctx* ctx, int64_t n) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_ps_kernel<C>, C::THREADS, C::SMEM);
+  if (occ < 1) occ = 1;
+  int64_t ctas = (int64_t)ctx->sms * occ;
+  int64_t units = (C::GPL > 1) ? ctas / C::GPL : ctas * C::LPC;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(units, n));
+}
+
+template <class C>
+int ps_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double2* prefix_out,
+              cudaStream_t st) {
+  const int groups = (lanes + C::LPC - 1) / C::LPC;
+  const int grid = groups * C::GPL;
+  constexpr int NE = C::MT * C::NT * 4;
+  int rc = ensure(ctx, ctx->tpriv,
+                  (size_t)grid * (pj.s - 1) * NE * C::THREADS * sizeof(double2));
+  if (rc) return rc;
+  double2* tpriv = (double2*)ctx->tpriv.p;
+  const double* terms = (const double*)ctx->terms.p;
+  double* ga = nullptr;
+  unsigned* ctr = nullptr;
+  if (C::GPL > 1) {
+    rc = ensure(ctx, ctx->psA, (size_t)groups * 3 * C::XDBL * sizeof(double));
+    if (rc) return rc;
+    rc = ensure(ctx, ctx->gctr, (size_t)groups * sizeof(unsigned));
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->gctr.p, 0, (size_t)groups * sizeof(unsigned), st));
+    ga = (double*)ctx->psA.p;
+    ctr = (unsigned*)ctx->gctr.p;
+    void* args[] = {(void*)&pj, (void*)&terms, (void*)&lanes, (void*)&ga, (void*)&ctr,
+                    (void*)&tpriv, (void*)&lane_out, (void*)&prefix_out};
+    if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)lane_ps_kernel<C>, dim3(grid),
+                                              dim3(C::THREADS), args, C::SMEM, st));
+  } else {
+    if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+    lane_ps_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(pj, terms, lanes, ga, ctr, tpriv,
+                                                         lane_out, prefix_out);
   }
   CUDA_TRY(ctx, cudaGetLastError());
   if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
@@ -356,10 +502,47 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     CUDA_TRY(ctx, cudaGetLastError());
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
     ++ctx->launches;
+    ctx->last_algo = ALGO_CLENSHAW;
+    ctx->last_gemms = job.m;
     *prods = lane_out;
     *count = cta_reduce ? blocks : lanes;
     return SP_OK;
   }
+  const int ps_s = (ctx->algo == ALGO_CLENSHAW) ? 0
+                   : (ctx->algo == ALGO_PS) ? std::max(2, ps_choose(job.m) ? ps_choose(job.m) : 2)
+                                            : ps_choose(job.m);
+  if (ps_s > 0) {
+    PSJob pj;
+    std::memset(&pj, 0, sizeof(pj));
+    pj.base = job;
+    pj.s = ps_s;
+    ps_coefficients(job.coef, job.m, ps_s, pj.alpha, &pj.r);
+    switch (ctx->fam) {
+      case FAM_T16: lanes = ps_lanes<PS16>(ctx, n); break;
+      case FAM_T32: lanes = ps_lanes<PS32>(ctx, n); break;
+      case FAM_T64: lanes = ps_lanes<PS64>(ctx, n); break;
+      case FAM_T128: lanes = ps_lanes<PS128>(ctx, n); break;
+      case FAM_T256: lanes = ps_lanes<PS256>(ctx, n); break;
+    }
+    int rc = ensure(ctx, ctx->lanes, (size_t)lanes * dd * sizeof(double2));
+    if (rc) return rc;
+    double2* lane_out = (double2*)ctx->lanes.p;
+    switch (ctx->fam) {
+      case FAM_T16: rc = ps_launch<PS16>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T32: rc = ps_launch<PS32>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T64: rc = ps_launch<PS64>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T128: rc = ps_launch<PS128>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T256: rc = ps_launch<PS256>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+    }
+    if (rc) return rc;
+    ctx->last_algo = ALGO_PS;
+    ctx->last_gemms = ps_cost(job.m, ps_s);
+    *prods = lane_out;
+    *count = lanes;
+    return SP_OK;
+  }
+  ctx->last_algo = ALGO_CLENSHAW;
+  ctx->last_gemms = job.m;
   switch (ctx->fam) {
     case FAM_T16: lanes = tc_lanes<Cfg16>(ctx, n); break;
     case FAM_T32: lanes = tc_lanes<Cfg32>(ctx, n); break;
@@ -437,7 +620,8 @@ int prepare_device(sp_ctx* ctx) {
 
 double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
   const double D = ctx->D;
-  return (double)n * (8.0 * D * D * D * m + 4.0 * D * D * ctx->n_terms);
+  (void)m;
+  return (double)n * (8.0 * D * D * D * ctx->last_gemms + 4.0 * D * D * ctx->n_terms);
 }
 
 // total propagator on the device -> d x d in d_out (output dtype)
@@ -470,7 +654,7 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
     rc = run_lanes(ctx, job, cta_reduce, nullptr, st, &prods, &cnt);
     if (rc) return rc;
     ctx->ev_pending = ctx->prof;
-    ctx->kname = family_kernel_name(ctx->fam);
+    ctx->kname = family_kernel_name(ctx->fam, ctx->last_algo);
     ctx->flops = executed_flops(ctx, job.n_slices, job.m);
     if (reduction == SP_REDUCE_PAIRWISE) {
       rc = reduce_pairwise_dev(ctx, prods, cnt, D, st, &total);
@@ -589,7 +773,8 @@ int sp_free(sp_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->terms, &ctx->amps,  &ctx->lanes, &ctx->ctab, &ctx->tree0,
                       &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
-                      &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch};
+                      &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch,
+                      &ctx->psA,   &ctx->tpriv};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -706,7 +891,7 @@ int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, do
   rc = run_lanes(ctx, job, false, (double2*)ctx->cumP.p, st, &prods, &cnt);
   if (rc) return rc;
   ctx->ev_pending = ctx->prof;
-  ctx->kname = family_kernel_name(ctx->fam);
+  ctx->kname = family_kernel_name(ctx->fam, ctx->last_algo);
   ctx->flops = executed_flops(ctx, n, job.m);
   rc = ensure(ctx, ctx->cumE, (size_t)cnt * dd * sizeof(double2));
   if (rc) return rc;
@@ -744,6 +929,21 @@ int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction,
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;  // NULL = the CUDA default stream
   return product_dev(ctx, count, (const double2*)d_mats, reduction, d_out, st);
+}
+
+int sp_set_algorithm(sp_ctx* ctx, int algo) {
+  if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
+  if (algo < ALGO_AUTO || algo > ALGO_PS)
+    return fail(ctx, SP_E_CONFIG, "unknown algorithm %d (0 auto, 1 clenshaw, 2 ps)", algo);
+  ctx->algo = algo;
+  return SP_OK;
+}
+
+int sp_last_algorithm(const sp_ctx* ctx, int* algo, int* gemms_per_slice) {
+  if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
+  if (algo) *algo = ctx->last_algo;
+  if (gemms_per_slice) *gemms_per_slice = ctx->last_gemms;
+  return SP_OK;
 }
 
 int sp_set_profiling(sp_ctx* ctx, int enabled) {

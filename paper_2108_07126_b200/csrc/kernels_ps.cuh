@@ -1,0 +1,344 @@
+// Paterson–Stockmeyer evaluation of the reference's Chebyshev polynomial on
+// FP64 tensor cores (the north-star "expm kernel" variant, SURVEY.md §7.1
+// item 7), same plan and same truncation as chebyshev.py:259-306.
+//
+// The plan's series  p(x) = a_0 + sum_{k>=1} 2 a_k T_k(x)  is regrouped in the
+// Chebyshev basis as  p(x) = sum_{j<r} Q_j(x) T_j(y),  y = T_s(x),
+// Q_j = sum_{i<s} alpha_{j,i} T_i(x)  (T_i T_js = (T_{js+i} + T_{|js-i|})/2;
+// alpha from a triangular solve on the host, engine.cu ps_coefficients), and
+// evaluated per slice as
+//   powers   T_2..T_s      : T_k = 2X T_{k-1} - T_{k-2}            (s-1 GEMMs)
+//   Clenshaw in y          : b_j = Q_j + 2y b_{j+1} - b_{j+2},
+//                            U = Q_0 + y b_1 - b_2                  (r-1 GEMMs)
+//   running product        : V <- U V                               (1 GEMM)
+// i.e. s + r - 1 GEMMs per slice instead of the Clenshaw form's m (7 vs 13 at
+// m = 13, 7 vs 15 at m = 15).  All operands are polynomials in X, so they
+// commute and every GEMM is column-local: CTA j of a lane group computes
+// column block j of each product from the full A operand (2X, 2y or U, shared
+// through L2 or shared memory) and its own column blocks.
+#pragma once
+#include "kernels.cuh"
+
+namespace sp {
+
+constexpr int PS_MAXC = 40;  // max r*s coefficients
+
+// PS needs two A-operand buffers (2X / U, and 2y) when they live in smem
+template <int D_, int WC_, int MT_, int NT_, int WPL_, int LPC_, int GPL_, bool XS_>
+struct PSCfg : TCCfg<D_, WC_, MT_, NT_, WPL_, LPC_, GPL_, XS_> {
+  using B = TCCfg<D_, WC_, MT_, NT_, WPL_, LPC_, GPL_, XS_>;
+  static constexpr int LANE_DBL = 2 * B::BDBL + (XS_ ? 2 * B::XDBL : 0) + B::WMAX;
+  static constexpr size_t SMEM = (size_t)LANE_DBL * LPC_ * sizeof(double);
+};
+
+struct PSJob {
+  SliceJob base;
+  int s, r;
+  double alpha[2 * PS_MAXC];  // alpha_{j,i} at (j*s + i), complex
+};
+
+template <class C, bool AG>
+__device__ __forceinline__ void ps_mma(const double* __restrict__ A, const double* Bc,
+                                       double (&accR)[C::MT * C::NT * 4],
+                                       double (&accI)[C::MT * C::NT * 4], int ms0, int nt0,
+                                       int ln) {
+  constexpr int MT = C::MT, NT = C::NT, KB = C::KB;
+  double2 aR[MT], aI[MT], nR[MT], nI[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const double* xa = A + ((size_t)((ms0 + i) * KB) * 2) * 64 + 2 * ln;
+    if constexpr (AG) {
+      aR[i] = __ldcg(reinterpret_cast<const double2*>(xa));
+      aI[i] = __ldcg(reinterpret_cast<const double2*>(xa + 64));
+    } else {
+      aR[i] = *reinterpret_cast<const double2*>(xa);
+      aI[i] = *reinterpret_cast<const double2*>(xa + 64);
+    }
+  }
+#pragma unroll 2
+  for (int kb = 0; kb < KB; ++kb) {
+    if (kb + 1 < KB) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double* xa = A + ((size_t)((ms0 + i) * KB + kb + 1) * 2) * 64 + 2 * ln;
+        if constexpr (AG) {
+          nR[i] = __ldcg(reinterpret_cast<const double2*>(xa));
+          nI[i] = __ldcg(reinterpret_cast<const double2*>(xa + 64));
+        } else {
+          nR[i] = *reinterpret_cast<const double2*>(xa);
+          nI[i] = *reinterpret_cast<const double2*>(xa + 64);
+        }
+      }
+    }
+    double bR[NT], bI[NT], bN[NT];
+#pragma unroll
+    for (int jn = 0; jn < NT; ++jn) {
+      const double* bp = Bc + ((kb * C::NTC + nt0 + jn) * 2) * 32 + ln;
+      bR[jn] = bp[0];
+      bI[jn] = bp[32];
+      bN[jn] = -bI[jn];
+    }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn) {
+        double* cr = &accR[(i * NT + jn) * 4];
+        double* ci = &accI[(i * NT + jn) * 4];
+        dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aR[i].x, aR[i].y, bR[jn]);
+        dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aR[i].x, aR[i].y, bI[jn]);
+      }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn) {
+        double* cr = &accR[(i * NT + jn) * 4];
+        double* ci = &accI[(i * NT + jn) * 4];
+        dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aI[i].x, aI[i].y, bN[jn]);
+        dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aI[i].x, aI[i].y, bR[jn]);
+      }
+    if (kb + 1 < KB) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        aR[i] = nR[i];
+        aI[i] = nI[i];
+      }
+    }
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
+    lane_ps_kernel(PSJob pj, const double* __restrict__ terms, int lanes,
+                   double* __restrict__ gA, unsigned* __restrict__ gctr,
+                   double2* __restrict__ tpriv, double2* __restrict__ lane_out,
+                   double2* __restrict__ prefix_out) {
+  constexpr int D = C::D, WC = C::WC, MT = C::MT, NT = C::NT, NE = MT * NT * 4;
+  constexpr bool AG = !C::XS;
+  const SliceJob& job = pj.base;
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const int lic = warp / C::WPL;
+  const int wil = warp % C::WPL;
+  const int tid_l = threadIdx.x - lic * C::WPL * 32;
+  constexpr int LT = C::WPL * 32;
+  const int group = blockIdx.x / C::GPL;
+  const int cb = blockIdx.x % C::GPL;
+  const int lane = group * C::LPC + lic;
+  const bool active = lane < lanes;
+
+  double* base = smem + (size_t)lic * C::LANE_DBL;
+  double* Bb[2] = {base, base + C::BDBL};
+  double *Ax, *Ay, *Au;
+  double* W;
+  if constexpr (C::XS) {
+    Ax = base + 2 * C::BDBL;
+    Ay = Ax + C::XDBL;
+    Au = Ax;  // 2X is dead once the powers are formed
+    W = Ay + C::XDBL;
+  } else {
+    Ax = gA + (size_t)group * 3 * C::XDBL;
+    Ay = Ax + C::XDBL;
+    Au = Ay + C::XDBL;
+    W = base + 2 * C::BDBL;
+  }
+
+  const int g = ln >> 2, t4 = ln & 3;
+  const int ms0 = (wil % (C::S / MT)) * MT;
+  const int nt0 = (wil / (C::S / MT)) * NT;
+  const int col0 = cb * WC;
+  const int s = pj.s, r = pj.r;
+  // private column blocks of T_1..T_{s-1}, acc-native, coalesced per thread
+  auto tp = [&](int kk, int e) -> double2& {
+    return tpriv[(((size_t)blockIdx.x * (s - 1) + kk) * NE + e) * C::THREADS + threadIdx.x];
+  };
+  auto row_of = [&](int idx) { return 16 * (ms0 + idx / (NT * 4)) + g + 8 * ((idx & 3) >> 1); };
+  auto col_of = [&](int idx) { return 8 * (nt0 + (idx / 4) % NT) + 2 * t4 + (idx & 1); };
+
+  double Pr[NE], Pi[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    Pr[e] = (row_of(e) == col0 + col_of(e)) ? 1.0 : 0.0;
+    Pi[e] = 0.0;
+  }
+  int64_t s0 = 0, s1 = 0;
+  if (active) lane_range(job.n_slices, lanes, lane, s0, s1);
+  const int T = job.n_terms;
+  const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
+  unsigned bar = 0;
+
+  auto sync_all = [&]() {
+    if constexpr (C::GPL > 1)
+      group_barrier(gctr + group, (++bar) * C::GPL);
+    else
+      lane_sync<C>();
+  };
+  auto write_B = [&](double* B, const double(&vr)[NE], const double(&vi)[NE], double f) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int rr = row_of(e), n = col_of(e);
+      B[bfrag_index<C>(rr, n, 0)] = f * vr[e];
+      B[bfrag_index<C>(rr, n, 1)] = f * vi[e];
+    }
+  };
+  auto write_A = [&](double* A, const double(&vr)[NE], const double(&vi)[NE], double fr,
+                     double fi) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int rr = row_of(e), c = col0 + col_of(e);
+      A[xfrag_index(D, rr, c, 0)] = fr * vr[e] - fi * vi[e];
+      A[xfrag_index(D, rr, c, 1)] = fr * vi[e] + fi * vr[e];
+    }
+  };
+  // Q_j at own positions: alpha_{j,0} I + sum_{i>=1} alpha_{j,i} T_i
+  auto load_Q = [&](int j, double(&qr)[NE], double(&qi)[NE]) {
+    const double a0r = pj.alpha[2 * (j * s)], a0i = pj.alpha[2 * (j * s) + 1];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const bool diag = row_of(e) == col0 + col_of(e);
+      qr[e] = diag ? a0r : 0.0;
+      qi[e] = diag ? a0i : 0.0;
+    }
+    for (int i = 1; i < s; ++i) {
+      const double ar = pj.alpha[2 * (j * s + i)], ai = pj.alpha[2 * (j * s + i) + 1];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const double2 tv = __ldcg(&tp(i - 1, e));
+        qr[e] = fma(ar, tv.x, fma(-ai, tv.y, qr[e]));
+        qi[e] = fma(ar, tv.y, fma(ai, tv.x, qi[e]));
+      }
+    }
+  };
+
+  for (int64_t sl = s0; sl < s1; ++sl) {
+    // ---- 1. weights, 2X assembly (A layout)
+    for (int tt = tid_l; tt < T; tt += LT)
+      W[tt] = (tt == 0) ? job.xs : job.xs * slice_weight(job, sl, tt);
+    lane_sync<C>();
+    {
+      int lo, hi, first, stride;
+      if constexpr (C::XS) {
+        lo = 0; hi = C::XDBL; first = tid_l; stride = LT;
+      } else {
+        lo = cb * (C::XDBL / C::GPL); hi = lo + C::XDBL / C::GPL;
+        first = threadIdx.x; stride = C::THREADS;
+      }
+      for (int i = lo + 2 * first; i < hi; i += 2 * stride) {
+        double2 h = __ldg(reinterpret_cast<const double2*>(terms + i));
+        double xr = W[0] * h.x, xi = W[0] * h.y;
+        for (int tt = 1; tt < T; ++tt) {
+          h = __ldg(reinterpret_cast<const double2*>(terms + (size_t)tt * C::XDBL + i));
+          xr = fma(W[tt], h.x, xr);
+          xi = fma(W[tt], h.y, xi);
+        }
+        *reinterpret_cast<double2*>(Ax + i) = make_double2(xr, xi);
+      }
+    }
+    sync_all();
+    // ---- 2. T_1 = X column block (own positions), to B layout + private
+    double accR[NE], accI[NE];
+    {
+      double t1r[NE], t1i[NE];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int rr = row_of(e), c = col0 + col_of(e);
+        const double* p0 = Ax + xfrag_index(D, rr, c, 0);
+        const double* p1 = Ax + xfrag_index(D, rr, c, 1);
+        t1r[e] = 0.5 * (AG ? __ldcg(p0) : *p0);
+        t1i[e] = 0.5 * (AG ? __ldcg(p1) : *p1);
+        tp(0, e) = make_double2(t1r[e], t1i[e]);
+      }
+      write_B(Bb[0], t1r, t1i, 1.0);
+    }
+    lane_sync<C>();
+    // ---- 3. powers T_k = 2X T_{k-1} - T_{k-2}, k = 2..s
+    int pb = 0;
+    for (int k = 2; k <= s; ++k) {
+      if (k == 2) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          accR[e] = (row_of(e) == col0 + col_of(e)) ? -1.0 : 0.0;
+          accI[e] = 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const double2 tv = __ldcg(&tp(k - 3, e));
+          accR[e] = -tv.x;
+          accI[e] = -tv.y;
+        }
+      }
+      ps_mma<C, AG>(Ax, Bb[pb], accR, accI, ms0, nt0, ln);
+      if (k < s) {
+        write_B(Bb[pb ^ 1], accR, accI, 1.0);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) tp(k - 1, e) = make_double2(accR[e], accI[e]);
+        pb ^= 1;
+        lane_sync<C>();
+      } else {
+        write_A(Ay, accR, accI, 2.0, 0.0);  // 2y = 2 T_s
+      }
+    }
+    sync_all();
+    // ---- 4. Clenshaw in y = T_s with matrix coefficients Q_j
+    if (r == 1) {
+      load_Q(0, accR, accI);
+    } else {
+      double qr[NE], qi[NE];
+      load_Q(r - 1, qr, qi);
+      int pc = 0;
+      write_B(Bb[pc], qr, qi, (r - 1 == 1) ? 0.5 : 1.0);
+      lane_sync<C>();
+      for (int j = r - 2; j >= 0; --j) {
+        load_Q(j, accR, accI);
+        if (j + 2 <= r - 1) {
+          const double* Bo = Bb[pc ^ 1];
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            const int rr = row_of(e), n = col_of(e);
+            accR[e] -= Bo[bfrag_index<C>(rr, n, 0)];
+            accI[e] -= Bo[bfrag_index<C>(rr, n, 1)];
+          }
+        }
+        ps_mma<C, AG>(Ay, Bb[pc], accR, accI, ms0, nt0, ln);
+        if (j >= 1) {
+          write_B(Bb[pc ^ 1], accR, accI, (j == 1) ? 0.5 : 1.0);
+          pc ^= 1;
+          lane_sync<C>();
+        }
+      }
+    }
+    // U (times the plan phase, 1 for equiprop's symmetric plans) to A layout
+    write_A(Au, accR, accI, phase_one ? 1.0 : job.phase[0], phase_one ? 0.0 : job.phase[1]);
+    sync_all();
+    // ---- 5. V <- U V
+    write_B(Bb[0], Pr, Pi, 1.0);
+    lane_sync<C>();
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      accR[e] = 0.0;
+      accI[e] = 0.0;
+    }
+    ps_mma<C, AG>(Au, Bb[0], accR, accI, ms0, nt0, ln);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      Pr[e] = accR[e];
+      Pi[e] = accI[e];
+    }
+    if (prefix_out) {
+      double2* o = prefix_out + (size_t)sl * D * D;
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(Pr[e], Pi[e]);
+    }
+    // smem A buffers (XS) and B buffers are rewritten by the next slice
+    lane_sync<C>();
+  }
+  if (active) {
+    double2* o = lane_out + (size_t)lane * D * D;
+#pragma unroll
+    for (int e = 0; e < NE; ++e)
+      o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(Pr[e], Pi[e]);
+  }
+}
+
+}  // namespace sp

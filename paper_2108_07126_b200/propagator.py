@@ -335,6 +335,24 @@ class IntegratorContext:
                                     REDUCTION[reduction], ctypes.c_void_p(out_ptr),
                                     ctypes.c_void_p(stream)), self._handle)
 
+    _ALGOS = {"auto": 0, "clenshaw": 1, "ps": 2}
+
+    def set_algorithm(self, algo: str = "auto") -> None:
+        """Series evaluation scheme: "auto" (Paterson-Stockmeyer in the
+        Chebyshev basis when it needs fewer GEMMs per slice), "clenshaw" (the
+        reference recurrence, ``chebyshev.py:298-303``) or "ps".  The
+        polynomial (plan, truncation) is the same in every case."""
+        if algo not in self._ALGOS:
+            raise ConfigError(f"unknown algorithm {algo!r}; expected {sorted(self._ALGOS)}")
+        check(lib.sp_set_algorithm(self._handle, self._ALGOS[algo]), self._handle)
+
+    def last_algorithm(self) -> dict:
+        a = ctypes.c_int()
+        g = ctypes.c_int()
+        check(lib.sp_last_algorithm(self._handle, ctypes.byref(a), ctypes.byref(g)), self._handle)
+        return {"algorithm": {0: "none", 1: "clenshaw", 2: "ps"}.get(a.value, "?"),
+                "gemms_per_slice": g.value}
+
     def set_profiling(self, enabled: bool = True) -> None:
         check(lib.sp_set_profiling(self._handle, int(bool(enabled))), self._handle)
 

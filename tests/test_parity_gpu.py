@@ -93,3 +93,32 @@ def test_convergence_orders_reproduced():
         lo, hi = bands[label]
         assert lo <= order <= hi, (label, order)
         assert abs(order - gold[label]["order"]) < 0.05, (label, order, gold[label]["order"])
+
+
+TC_CASES = [c for c in CASES if c["kind"] != "zero" and c.get("d", 2) >= 5]
+
+
+@pytest.mark.parametrize("algo", ["clenshaw", "ps"])
+@pytest.mark.parametrize("case", TC_CASES, ids=[c["name"] for c in TC_CASES])
+def test_both_series_schemes_match_reference(case, algo, golden):
+    """The tensor-core families evaluate the same plan polynomial either by
+    the reference's Clenshaw recurrence or by Paterson-Stockmeyer in the
+    Chebyshev basis; both pass the same gate."""
+    key = case["name"]
+    h0, hs, values, dt = build_inputs(case)
+    mode = case["mode"]
+    ctx = sp.create(precision=case["precision"], m_max=case.get("m_max"))
+    ctx.set_algorithm(algo)
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                        quadrature=None if mode == "magnus" else mode)
+    amps = sp.ControlAmplitudes(values, dt)
+    u = ctx.equiprop(amps).u
+    assert ctx.last_algorithm()["algorithm"] == algo
+    tol, _ = parity_tolerance(golden[f"{key}__u"], golden[f"{key}__u_seq"], case["precision"])
+    assert rel_fro(u, golden[f"{key}__u"]) <= tol
+    if case.get("cumulative"):
+        cum = ctx.equiprop_all(amps)
+        for k in range(cum.u_all.shape[0]):
+            assert rel_fro(cum.u_all[k], golden[f"{key}__u_all"][k]) <= tol
+        assert np.array_equal(cum.final, ctx.equiprop(amps, reduction="sequential").u)
+    ctx.close()
