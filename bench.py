@@ -213,13 +213,13 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
     stream = torch.cuda.current_stream(dev)
 
-    # amplitude validation is part of the job (device reduction, no host pass)
+    # amplitude validation (|c| <= 1) is part of the job: it runs inside the
+    # lane kernel and its flag is read after each timed step (sp_amplitude_violation)
     def validate():
-        if not bool((d_amps.abs() <= 1.0).all()):
+        if ctx.amplitude_violation() >= 0:
             raise sp.AmplitudeBoundError("amplitude outside [-1, 1]")
 
     def step():
-        validate()
         if world == 1:
             ctx.equiprop_device_ptr(d_amps.data_ptr(), hi - lo, wl["n_ctrl"], dt,
                                     out.data_ptr(), stream=stream.cuda_stream, plan=plan)
@@ -245,6 +245,7 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
             t = ctx.last_timing()
             kernel_ms.append(t["main_kernel_ms"])
             launches += t["launches"]
+            validate()
         torch.cuda.synchronize(dev)
     if dist is not None:
         dist.barrier()
@@ -261,10 +262,23 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
     F = canonical_flops(d, plan.m_max, 1 + wl["n_ctrl"])
     peak = fp64_peak()["fp64_dmma_tflops"] * 1e12
     achieved = local_slices * F / (kern / 1e3)
+    traffic, traffic_note = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            cap = json.load(fh).get(t["kernel"])
+        if cap:
+            traffic = cap["dram_bytes"] * local_slices / cap["slices"]
+            traffic_note = (f"ncu --set full dram read+write of one launch at {cap['slices']} "
+                            f"slices ({cap['dram_bytes']:.3g} B), scaled linearly to this launch; "
+                            f"algorithmic bytes/slice = {8 * wl['n_ctrl']} (amplitude row)")
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {"bound": "tensor", "achieved": achieved / 1e12, "peak": peak / 1e12,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "traffic_note": traffic_note,
                 "kernel": t["kernel"], "kernel_ms": kern,
                 "executed_frac": t["executed_flops"] / (kern / 1e3) / peak,
+                "series": ctx.last_algorithm(),
                 "algorithmic_flops_per_launch": local_slices * F,
                 "peak_source": "measured FP64 DMMA pipe peak (profiles/fp64_peak.json)"}
 

@@ -116,6 +116,12 @@ int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, do
  * reduce_pairwise propagator.py:68-102, sequential = left fold) */
 int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction,
                       void* d_out, void* stream);
+/* amplitude validation (|c| <= 1, NaN rejected; hamiltonian.py:145-174) is
+ * fused into the lane kernels: sp_equiprop / sp_equiprop_all return
+ * SP_E_AMPLITUDE_BOUND after the pass; for sp_equiprop_device call this
+ * (it synchronises the propagation's stream).  *index = row-major index of
+ * the first offending sample, or -1. */
+int sp_amplitude_violation(sp_ctx* ctx, int64_t* index);
 /* slice count for a table of pts samples in the loaded mode
  * (propagator.py:245-252); SP_E_SAMPLING_PARITY for even/short 3-point tables */
 int sp_slice_count(const sp_ctx* ctx, int64_t pts, int64_t* out);

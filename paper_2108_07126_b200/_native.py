@@ -61,6 +61,7 @@ HEADER_SYMBOLS = {
                                    _c.POINTER(SpPlan), _P]),
     "sp_product_device": (_c.c_int, [_P, _c.c_int, _P, _c.c_int, _P, _P]),
     "sp_slice_count": (_c.c_int, [_P, _c.c_int64, _c.POINTER(_c.c_int64)]),
+    "sp_amplitude_violation": (_c.c_int, [_P, _c.POINTER(_c.c_int64)]),
     "sp_set_algorithm": (_c.c_int, [_P, _c.c_int]),
     "sp_last_algorithm": (_c.c_int, [_P, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)]),
     "sp_set_profiling": (_c.c_int, [_P, _c.c_int]),

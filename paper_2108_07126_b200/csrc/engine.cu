@@ -16,6 +16,7 @@
 
 #include "internal.h"
 #include "kernels.cuh"
+#include "kernels_tc.cuh"
 #include "kernels_ps.cuh"
 
 using namespace sp;
@@ -156,7 +157,9 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   int fam = FAM_NONE, D = 0;
   DevBuf terms, amps, lanes, ctab, tree0, tree1, xglob, gctr, result, out, cumP, cumE, cumO,
-      fold_scratch, psA, tpriv;
+      fold_scratch, psA, tpriv, viol;
+  cudaStream_t viol_stream = nullptr;
+  int64_t viol_pts = 0;
   int algo = 0;          // Algo
   int last_algo = 0;     // algorithm of the last lane pass
   int last_gemms = 0;    // GEMMs per slice of the last lane pass
@@ -607,6 +610,37 @@ int build_job(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double
   return SP_OK;
 }
 
+// amplitude validation fused into the lane kernels: reset the device flag
+int arm_validation(sp_ctx* ctx, SliceJob* job, cudaStream_t st) {
+  int rc = ensure(ctx, ctx->viol, sizeof(unsigned long long));
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->viol.p, 0xFF, sizeof(unsigned long long), st));
+  job->viol = (unsigned long long*)ctx->viol.p;
+  ctx->viol_stream = st;
+  ctx->viol_pts = job->pts;
+  return SP_OK;
+}
+
+// after the stream work: SP_E_AMPLITUDE_BOUND with the reference's message
+// (hamiltonian.py:165-174) if any sample was outside [-1, 1]
+int read_violation(sp_ctx* ctx, const double* host_amps, int64_t* index_out) {
+  unsigned long long v = ~0ull;
+  if (ctx->viol.p) {
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->viol_stream));
+    CUDA_TRY(ctx, cudaMemcpy(&v, ctx->viol.p, sizeof(v), cudaMemcpyDeviceToHost));
+  }
+  if (index_out) *index_out = (v == ~0ull) ? -1 : (int64_t)v;
+  if (v == ~0ull) return SP_OK;
+  const int N = std::max(1, ctx->n_ctrl);
+  const long long k = (long long)(v / N), i = (long long)(v % N);
+  if (host_amps)
+    return fail(ctx, SP_E_AMPLITUDE_BOUND,
+                "control amplitude %.17g at sample %lld, control %lld lies outside [-1, 1]",
+                host_amps[v], k, i);
+  return fail(ctx, SP_E_AMPLITUDE_BOUND,
+              "control amplitude at sample %lld, control %lld lies outside [-1, 1]", k, i);
+}
+
 int prepare_device(sp_ctx* ctx) {
   int rc = device_init(ctx);
   if (rc) return rc;
@@ -632,6 +666,8 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
   ctx->ev_pending = false;
   SliceJob job;
   int rc = build_job(ctx, d_amps, pts, n_ctrl, dt, plan, &job);
+  if (rc) return rc;
+  rc = arm_validation(ctx, &job, st);
   if (rc) return rc;
   const int D = ctx->D, d = ctx->dim;
   const size_t dd = (size_t)D * D;
@@ -774,7 +810,7 @@ int sp_free(sp_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->terms, &ctx->amps,  &ctx->lanes, &ctx->ctab, &ctx->tree0,
                       &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
                       &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch,
-                      &ctx->psA,   &ctx->tpriv};
+                      &ctx->psA,   &ctx->tpriv, &ctx->viol};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -859,7 +895,7 @@ int sp_equiprop(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double
   if (rc) return rc;
   CUDA_TRY(ctx, cudaMemcpyAsync(u_out, ctx->out.p, obytes, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
-  return SP_OK;
+  return read_violation(ctx, amps, nullptr);
 }
 
 int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
@@ -879,6 +915,8 @@ int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, do
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->amps.p, amps, abytes, cudaMemcpyHostToDevice, st));
   SliceJob job;
   rc = build_job(ctx, (const double*)ctx->amps.p, pts, n_ctrl, dt, plan, &job);
+  if (rc) return rc;
+  rc = arm_validation(ctx, &job, st);
   if (rc) return rc;
   const int64_t n = job.n_slices;
   if (n == 0) return SP_OK;
@@ -917,7 +955,7 @@ int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, do
   ctx->launches += 3;
   CUDA_TRY(ctx, cudaMemcpyAsync(u_all_out, ctx->out.p, obytes, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
-  return SP_OK;
+  return read_violation(ctx, amps, nullptr);
 }
 
 int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction, void* d_out,
@@ -929,6 +967,11 @@ int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction,
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;  // NULL = the CUDA default stream
   return product_dev(ctx, count, (const double2*)d_mats, reduction, d_out, st);
+}
+
+int sp_amplitude_violation(sp_ctx* ctx, int64_t* index) {
+  if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
+  return read_violation(ctx, nullptr, index);
 }
 
 int sp_set_algorithm(sp_ctx* ctx, int algo) {

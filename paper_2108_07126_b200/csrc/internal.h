@@ -28,6 +28,9 @@ struct SliceJob {
   double coef[2 * (SP_MAX_ORDER + 1)];
   double phase[2];
   int64_t n_slices;
+  // first out-of-range amplitude (row-major index), ULLONG_MAX if none:
+  // validation fused into the weight computation (hamiltonian.py:145-153)
+  unsigned long long* viol;
 };
 
 }  // namespace sp

@@ -58,14 +58,31 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 //   magnus    magnus.py:88-106, 134-139     controls: (c1+4c2+c3)/6,
 //             i[H0,Hk]: (dt/6)(c3-c1),  i[Hk,Hk']: (dt/6)(c1_k c3_k' - c3_k c1_k')
 //   (the reference divides the magnus columns by the 2dt scale; same values)
+__device__ __forceinline__ void check_amp(const SliceJob& j, int64_t row, int col, double v) {
+  // |c| <= 1 (false for NaN too); the first offender in row-major order wins
+  if (!(fabs(v) <= 1.0) && j.viol)
+    atomicMin(j.viol, (unsigned long long)(row * j.n_ctrl + col));
+}
+
+// Every amplitude of the table is read by exactly one weight t in 1..N of
+// some slice, so validating there covers the whole table in passing.
 __device__ __forceinline__ double slice_weight(const SliceJob& j, int64_t s, int t) {
   const int N = j.n_ctrl;
-  if (j.mode == SP_MODE_MIDPOINT) return j.amps[s * N + (t - 1)];
+  if (j.mode == SP_MODE_MIDPOINT) {
+    const double v = j.amps[s * N + (t - 1)];
+    check_amp(j, s, t - 1, v);
+    return v;
+  }
   const double* r1 = j.amps + (2 * s) * N;
   const double* r2 = r1 + N;
   const double* r3 = r2 + N;
   int e = t - 1;
-  if (e < N) return (r1[e] + 4.0 * r2[e] + r3[e]) / 6.0;
+  if (e < N) {
+    check_amp(j, 2 * s, e, r1[e]);
+    check_amp(j, 2 * s + 1, e, r2[e]);
+    check_amp(j, 2 * s + 2, e, r3[e]);
+    return (r1[e] + 4.0 * r2[e] + r3[e]) / 6.0;
+  }
   e -= N;
   if (e < N) return (j.dt / 6.0) * (r3[e] - r1[e]);
   e -= N;
@@ -315,264 +332,7 @@ __device__ __forceinline__ void group_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
 }
 
-template <class C>
-__global__ void __launch_bounds__(C::THREADS, 1)
-    lane_tc_kernel(SliceJob job, const double* __restrict__ terms, int lanes,
-                   double* __restrict__ xglob, unsigned* __restrict__ gctr,
-                   double2* __restrict__ lane_out, double2* __restrict__ prefix_out) {
-  constexpr int D = C::D, WC = C::WC, MT = C::MT, NT = C::NT, KB = C::KB;
-  extern __shared__ __align__(16) double smem[];
-  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
-  const int lic = warp / C::WPL;
-  const int wil = warp % C::WPL;
-  const int tid_l = threadIdx.x - lic * C::WPL * 32;  // thread index within the lane
-  constexpr int LT = C::WPL * 32;                      // threads per lane
-  const int group = blockIdx.x / C::GPL;
-  const int cb = blockIdx.x % C::GPL;
-  const int lane = group * C::LPC + lic;
-  const bool active = lane < lanes;
-
-  double* base = smem + (size_t)lic * C::LANE_DBL;
-  double* Bbuf[2] = {base, base + C::BDBL};
-  double* Xs = base + 2 * C::BDBL;
-  double* W = Xs + (C::XS ? C::XDBL : 0);
-
-  const int g = ln >> 2, t4 = ln & 3;
-  const int ms0 = (wil % (C::S / MT)) * MT;
-  const int nt0 = (wil / (C::S / MT)) * NT;
-  const int col0 = cb * WC;
-
-  double Vr[MT][NT][4], Vi[MT][NT][4];
-#pragma unroll
-  for (int i = 0; i < MT; ++i)
-#pragma unroll
-    for (int jn = 0; jn < NT; ++jn)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
-        const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
-        Vr[i][jn][e] = (r == col0 + n) ? 1.0 : 0.0;
-        Vi[i][jn][e] = 0.0;
-      }
-
-  int64_t s0 = 0, s1 = 0;
-  if (active) lane_range(job.n_slices, lanes, lane, s0, s1);
-  const int T = job.n_terms, m = job.m;
-  const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
-  int p = 0;  // Bbuf[p] = current iterate
-  unsigned iter = 0;
-
-  for (int64_t s = s0; s < s1; ++s, ++iter) {
-    // ---- 1. expansion weights (scaled by 2*scale/beta)
-    for (int tt = tid_l; tt < T; tt += LT)
-      W[tt] = (tt == 0) ? job.xs : job.xs * slice_weight(job, s, tt);
-    lane_sync<C>();
-    // ---- 2. assemble 2X in the A-native layout
-    const double* Xsrc;
-    {
-      double* Xdst;
-      int lo, hi, stride, first;
-      if constexpr (C::XS) {
-        Xdst = Xs;
-        lo = 0;
-        hi = C::XDBL;
-        first = tid_l;
-        stride = LT;
-      } else {
-        Xdst = xglob + ((size_t)group * 2 + (iter & 1)) * C::XDBL;
-        lo = cb * (C::XDBL / C::GPL);
-        hi = lo + C::XDBL / C::GPL;
-        first = threadIdx.x;
-        stride = C::THREADS;
-      }
-      for (int i = lo + 2 * first; i < hi; i += 2 * stride) {
-        double2 h = __ldg(reinterpret_cast<const double2*>(terms + i));
-        double xr = W[0] * h.x, xi = W[0] * h.y;
-        for (int tt = 1; tt < T; ++tt) {
-          h = __ldg(reinterpret_cast<const double2*>(terms + (size_t)tt * C::XDBL + i));
-          xr = fma(W[tt], h.x, xr);
-          xi = fma(W[tt], h.y, xi);
-        }
-        *reinterpret_cast<double2*>(Xdst + i) = make_double2(xr, xi);
-      }
-      Xsrc = C::XS ? Xs : xglob + ((size_t)group * 2 + (iter & 1)) * C::XDBL;
-    }
-    // ---- 3. b_m = a_m V into the current buffer
-    {
-      const double ar = job.coef[2 * m], ai = job.coef[2 * m + 1];
-      double* B = Bbuf[p];
-#pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int jn = 0; jn < NT; ++jn)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
-            const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
-            const double vr = Vr[i][jn][e], vi = Vi[i][jn][e];
-            B[bfrag_index<C>(r, n, 0)] = ar * vr - ai * vi;
-            B[bfrag_index<C>(r, n, 1)] = ar * vi + ai * vr;
-          }
-    }
-    if constexpr (C::GPL > 1)
-      group_barrier(gctr + group, (iter + 1) * C::GPL);
-    else
-      lane_sync<C>();
-
-    // ---- 4. m Clenshaw steps: new = 2X cur - beta old + a_j V
-    for (int jj = m - 1; jj >= 0; --jj) {
-      const double ar = job.coef[2 * jj], ai = job.coef[2 * jj + 1];
-      const double* Bc = Bbuf[p];
-      double* Bo = Bbuf[p ^ 1];
-      double accR[MT][NT][4], accI[MT][NT][4];
-      const bool first = (jj == m - 1);
-      const double beta = (jj == 0) ? 2.0 : 1.0;
-#pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int jn = 0; jn < NT; ++jn)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
-            const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
-            double orr = 0.0, oi = 0.0;
-            if (!first) {
-              orr = Bo[bfrag_index<C>(r, n, 0)];
-              oi = Bo[bfrag_index<C>(r, n, 1)];
-            }
-            const double vr = Vr[i][jn][e], vi = Vi[i][jn][e];
-            accR[i][jn][e] = fma(ar, vr, fma(-ai, vi, -beta * orr));
-            accI[i][jn][e] = fma(ar, vi, fma(ai, vr, -beta * oi));
-          }
-      // MMA over k with a one-step register prefetch of the A fragments
-      double2 aR[MT], aI[MT], nR[MT], nI[MT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const double* xa = Xsrc + ((size_t)((ms0 + i) * KB + 0) * 2) * 64 + 2 * ln;
-        if constexpr (C::XS) {
-          aR[i] = *reinterpret_cast<const double2*>(xa);
-          aI[i] = *reinterpret_cast<const double2*>(xa + 64);
-        } else {
-          aR[i] = __ldcg(reinterpret_cast<const double2*>(xa));
-          aI[i] = __ldcg(reinterpret_cast<const double2*>(xa + 64));
-        }
-      }
-#pragma unroll 2
-      for (int kb = 0; kb < KB; ++kb) {
-        if (kb + 1 < KB) {
-#pragma unroll
-          for (int i = 0; i < MT; ++i) {
-            const double* xa = Xsrc + ((size_t)((ms0 + i) * KB + kb + 1) * 2) * 64 + 2 * ln;
-            if constexpr (C::XS) {
-              nR[i] = *reinterpret_cast<const double2*>(xa);
-              nI[i] = *reinterpret_cast<const double2*>(xa + 64);
-            } else {
-              nR[i] = __ldcg(reinterpret_cast<const double2*>(xa));
-              nI[i] = __ldcg(reinterpret_cast<const double2*>(xa + 64));
-            }
-          }
-        }
-        double bR[NT], bI[NT], bN[NT];
-#pragma unroll
-        for (int jn = 0; jn < NT; ++jn) {
-          const double* bp = Bc + ((kb * C::NTC + nt0 + jn) * 2) * 32 + ln;
-          bR[jn] = bp[0];
-          bI[jn] = bp[32];
-          bN[jn] = -bI[jn];
-        }
-        // two passes so that MMAs into the same accumulator are 2*MT*NT
-        // instructions apart (hides the DMMA latency without more warps)
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int jn = 0; jn < NT; ++jn) {
-            double* cr = accR[i][jn];
-            double* ci = accI[i][jn];
-            dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aR[i].x, aR[i].y, bR[jn]);
-            dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aR[i].x, aR[i].y, bI[jn]);
-          }
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int jn = 0; jn < NT; ++jn) {
-            double* cr = accR[i][jn];
-            double* ci = accI[i][jn];
-            dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aI[i].x, aI[i].y, bN[jn]);
-            dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aI[i].x, aI[i].y, bR[jn]);
-          }
-        if (kb + 1 < KB) {
-#pragma unroll
-          for (int i = 0; i < MT; ++i) {
-            aR[i] = nR[i];
-            aI[i] = nI[i];
-          }
-        }
-      }
-      if (jj > 0) {
-        // new iterate becomes "cur" for the next step (own positions only)
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int jn = 0; jn < NT; ++jn)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
-              const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
-              Bo[bfrag_index<C>(r, n, 0)] = accR[i][jn][e];
-              Bo[bfrag_index<C>(r, n, 1)] = accI[i][jn][e];
-            }
-        p ^= 1;
-        lane_sync<C>();
-      } else {
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int jn = 0; jn < NT; ++jn)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              if (phase_one) {
-                Vr[i][jn][e] = accR[i][jn][e];
-                Vi[i][jn][e] = accI[i][jn][e];
-              } else {
-                Vr[i][jn][e] = job.phase[0] * accR[i][jn][e] - job.phase[1] * accI[i][jn][e];
-                Vi[i][jn][e] = job.phase[0] * accI[i][jn][e] + job.phase[1] * accR[i][jn][e];
-              }
-            }
-        // next slice writes b_m into Bbuf[p^1] (only own positions were read
-        // there); flip so that the current buffer of the next slice is it
-        p ^= 1;
-      }
-    }
-    if (prefix_out) {
-      double2* o = prefix_out + (size_t)s * D * D;
-#pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int jn = 0; jn < NT; ++jn)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
-            const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
-            o[(size_t)r * D + col0 + n] = make_double2(Vr[i][jn][e], Vi[i][jn][e]);
-          }
-    }
-    // X (smem) and W are rewritten by the next slice
-    if constexpr (C::GPL == 1) lane_sync<C>();
-  }
-  if (active) {
-    double2* o = lane_out + (size_t)lane * D * D;
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-      for (int jn = 0; jn < NT; ++jn)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = 16 * (ms0 + i) + g + 8 * (e >> 1);
-          const int n = 8 * (nt0 + jn) + 2 * t4 + (e & 1);
-          o[(size_t)r * D + col0 + n] = make_double2(Vr[i][jn][e], Vi[i][jn][e]);
-        }
-  }
-}
+// lane_tc_kernel (the Clenshaw form) lives in kernels_tc.cuh
 
 // ---------------------------------------------------------------------------
 // ordered products of lane / block products

@@ -16,8 +16,12 @@
 // commute and every GEMM is column-local: CTA j of a lane group computes
 // column block j of each product from the full A operand (2X, 2y or U, shared
 // through L2 or shared memory) and its own column blocks.
+//
+// Shared-memory operands are addressed by offsets into the dynamic smem
+// array (not through pointer tables) so that every access compiles to
+// LDS/STS rather than generic LD/ST.
 #pragma once
-#include "kernels.cuh"
+#include "kernels_tc.cuh"
 
 namespace sp {
 
@@ -36,75 +40,6 @@ struct PSJob {
   int s, r;
   double alpha[2 * PS_MAXC];  // alpha_{j,i} at (j*s + i), complex
 };
-
-template <class C, bool AG>
-__device__ __forceinline__ void ps_mma(const double* __restrict__ A, const double* Bc,
-                                       double (&accR)[C::MT * C::NT * 4],
-                                       double (&accI)[C::MT * C::NT * 4], int ms0, int nt0,
-                                       int ln) {
-  constexpr int MT = C::MT, NT = C::NT, KB = C::KB;
-  double2 aR[MT], aI[MT], nR[MT], nI[MT];
-#pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const double* xa = A + ((size_t)((ms0 + i) * KB) * 2) * 64 + 2 * ln;
-    if constexpr (AG) {
-      aR[i] = __ldcg(reinterpret_cast<const double2*>(xa));
-      aI[i] = __ldcg(reinterpret_cast<const double2*>(xa + 64));
-    } else {
-      aR[i] = *reinterpret_cast<const double2*>(xa);
-      aI[i] = *reinterpret_cast<const double2*>(xa + 64);
-    }
-  }
-#pragma unroll 2
-  for (int kb = 0; kb < KB; ++kb) {
-    if (kb + 1 < KB) {
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const double* xa = A + ((size_t)((ms0 + i) * KB + kb + 1) * 2) * 64 + 2 * ln;
-        if constexpr (AG) {
-          nR[i] = __ldcg(reinterpret_cast<const double2*>(xa));
-          nI[i] = __ldcg(reinterpret_cast<const double2*>(xa + 64));
-        } else {
-          nR[i] = *reinterpret_cast<const double2*>(xa);
-          nI[i] = *reinterpret_cast<const double2*>(xa + 64);
-        }
-      }
-    }
-    double bR[NT], bI[NT], bN[NT];
-#pragma unroll
-    for (int jn = 0; jn < NT; ++jn) {
-      const double* bp = Bc + ((kb * C::NTC + nt0 + jn) * 2) * 32 + ln;
-      bR[jn] = bp[0];
-      bI[jn] = bp[32];
-      bN[jn] = -bI[jn];
-    }
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-      for (int jn = 0; jn < NT; ++jn) {
-        double* cr = &accR[(i * NT + jn) * 4];
-        double* ci = &accI[(i * NT + jn) * 4];
-        dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aR[i].x, aR[i].y, bR[jn]);
-        dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aR[i].x, aR[i].y, bI[jn]);
-      }
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-      for (int jn = 0; jn < NT; ++jn) {
-        double* cr = &accR[(i * NT + jn) * 4];
-        double* ci = &accI[(i * NT + jn) * 4];
-        dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aI[i].x, aI[i].y, bN[jn]);
-        dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aI[i].x, aI[i].y, bR[jn]);
-      }
-    if (kb + 1 < KB) {
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        aR[i] = nR[i];
-        aI[i] = nI[i];
-      }
-    }
-  }
-}
 
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1)
@@ -126,21 +61,17 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int lane = group * C::LPC + lic;
   const bool active = lane < lanes;
 
-  double* base = smem + (size_t)lic * C::LANE_DBL;
-  double* Bb[2] = {base, base + C::BDBL};
-  double *Ax, *Ay, *Au;
-  double* W;
-  if constexpr (C::XS) {
-    Ax = base + 2 * C::BDBL;
-    Ay = Ax + C::XDBL;
-    Au = Ax;  // 2X is dead once the powers are formed
-    W = Ay + C::XDBL;
-  } else {
-    Ax = gA + (size_t)group * 3 * C::XDBL;
-    Ay = Ax + C::XDBL;
-    Au = Ay + C::XDBL;
-    W = base + 2 * C::BDBL;
-  }
+  // smem offsets (doubles): B ping-pong, A buffers (XS), expansion weights
+  const int lbase = lic * C::LANE_DBL;
+  const int bofs0 = lbase, bofs1 = lbase + C::BDBL;
+  const int ax_off = lbase + 2 * C::BDBL;           // XS: 2X, later U
+  const int ay_off = ax_off + C::XDBL;              // XS: 2y
+  const int w_off = lbase + 2 * C::BDBL + (C::XS ? 2 * C::XDBL : 0);
+  // global A buffers (group families): 2X, 2y, U
+  double* gx = AG ? gA + (size_t)group * 3 * C::XDBL : nullptr;
+  double* gy = AG ? gx + C::XDBL : nullptr;
+  double* gu = AG ? gy + C::XDBL : nullptr;
+  auto bo = [&](int which) { return which ? bofs1 : bofs0; };
 
   const int g = ln >> 2, t4 = ln & 3;
   const int ms0 = (wil % (C::S / MT)) * MT;
@@ -172,21 +103,28 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     else
       lane_sync<C>();
   };
-  auto write_B = [&](double* B, const double(&vr)[NE], const double(&vi)[NE], double f) {
+  auto write_B = [&](int off, const double(&vr)[NE], const double(&vi)[NE], double f) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int rr = row_of(e), n = col_of(e);
-      B[bfrag_index<C>(rr, n, 0)] = f * vr[e];
-      B[bfrag_index<C>(rr, n, 1)] = f * vi[e];
+      smem[off + bfrag_index<C>(rr, n, 0)] = f * vr[e];
+      smem[off + bfrag_index<C>(rr, n, 1)] = f * vi[e];
     }
   };
-  auto write_A = [&](double* A, const double(&vr)[NE], const double(&vi)[NE], double fr,
-                     double fi) {
+  // A-native write of own positions: smem (XS) or global (group families)
+  auto write_A = [&](double* gptr, int off, const double(&vr)[NE], const double(&vi)[NE],
+                     double fr, double fi) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int rr = row_of(e), c = col0 + col_of(e);
-      A[xfrag_index(D, rr, c, 0)] = fr * vr[e] - fi * vi[e];
-      A[xfrag_index(D, rr, c, 1)] = fr * vi[e] + fi * vr[e];
+      const double xr = fr * vr[e] - fi * vi[e], xi = fr * vi[e] + fi * vr[e];
+      if constexpr (AG) {
+        gptr[xfrag_index(D, rr, c, 0)] = xr;
+        gptr[xfrag_index(D, rr, c, 1)] = xi;
+      } else {
+        smem[off + xfrag_index(D, rr, c, 0)] = xr;
+        smem[off + xfrag_index(D, rr, c, 1)] = xi;
+      }
     }
   };
   // Q_j at own positions: alpha_{j,0} I + sum_{i>=1} alpha_{j,i} T_i
@@ -212,7 +150,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   for (int64_t sl = s0; sl < s1; ++sl) {
     // ---- 1. weights, 2X assembly (A layout)
     for (int tt = tid_l; tt < T; tt += LT)
-      W[tt] = (tt == 0) ? job.xs : job.xs * slice_weight(job, sl, tt);
+      smem[w_off + tt] = (tt == 0) ? job.xs : job.xs * slice_weight(job, sl, tt);
     lane_sync<C>();
     {
       int lo, hi, first, stride;
@@ -224,13 +162,16 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
       for (int i = lo + 2 * first; i < hi; i += 2 * stride) {
         double2 h = __ldg(reinterpret_cast<const double2*>(terms + i));
-        double xr = W[0] * h.x, xi = W[0] * h.y;
+        double xr = smem[w_off] * h.x, xi = smem[w_off] * h.y;
         for (int tt = 1; tt < T; ++tt) {
           h = __ldg(reinterpret_cast<const double2*>(terms + (size_t)tt * C::XDBL + i));
-          xr = fma(W[tt], h.x, xr);
-          xi = fma(W[tt], h.y, xi);
+          xr = fma(smem[w_off + tt], h.x, xr);
+          xi = fma(smem[w_off + tt], h.y, xi);
         }
-        *reinterpret_cast<double2*>(Ax + i) = make_double2(xr, xi);
+        if constexpr (AG)
+          *reinterpret_cast<double2*>(gx + i) = make_double2(xr, xi);
+        else
+          *reinterpret_cast<double2*>(&smem[ax_off + i]) = make_double2(xr, xi);
       }
     }
     sync_all();
@@ -241,13 +182,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
         const int rr = row_of(e), c = col0 + col_of(e);
-        const double* p0 = Ax + xfrag_index(D, rr, c, 0);
-        const double* p1 = Ax + xfrag_index(D, rr, c, 1);
-        t1r[e] = 0.5 * (AG ? __ldcg(p0) : *p0);
-        t1i[e] = 0.5 * (AG ? __ldcg(p1) : *p1);
+        const int i0 = xfrag_index(D, rr, c, 0), i1 = xfrag_index(D, rr, c, 1);
+        t1r[e] = 0.5 * (AG ? __ldcg(gx + i0) : smem[ax_off + i0]);
+        t1i[e] = 0.5 * (AG ? __ldcg(gx + i1) : smem[ax_off + i1]);
         tp(0, e) = make_double2(t1r[e], t1i[e]);
       }
-      write_B(Bb[0], t1r, t1i, 1.0);
+      write_B(bofs0, t1r, t1i, 1.0);
     }
     lane_sync<C>();
     // ---- 3. powers T_k = 2X T_{k-1} - T_{k-2}, k = 2..s
@@ -267,15 +207,15 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           accI[e] = -tv.y;
         }
       }
-      ps_mma<C, AG>(Ax, Bb[pb], accR, accI, ms0, nt0, ln);
+      tile_mma<C, AG>(gx, ax_off, bo(pb), accR, accI, ms0, nt0, ln);
       if (k < s) {
-        write_B(Bb[pb ^ 1], accR, accI, 1.0);
+        write_B(bo(pb ^ 1), accR, accI, 1.0);
 #pragma unroll
         for (int e = 0; e < NE; ++e) tp(k - 1, e) = make_double2(accR[e], accI[e]);
         pb ^= 1;
         lane_sync<C>();
       } else {
-        write_A(Ay, accR, accI, 2.0, 0.0);  // 2y = 2 T_s
+        write_A(gy, ay_off, accR, accI, 2.0, 0.0);  // 2y = 2 T_s
       }
     }
     sync_all();
@@ -286,39 +226,41 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       double qr[NE], qi[NE];
       load_Q(r - 1, qr, qi);
       int pc = 0;
-      write_B(Bb[pc], qr, qi, (r - 1 == 1) ? 0.5 : 1.0);
+      write_B(bo(pc), qr, qi, (r - 1 == 1) ? 0.5 : 1.0);
       lane_sync<C>();
       for (int j = r - 2; j >= 0; --j) {
         load_Q(j, accR, accI);
         if (j + 2 <= r - 1) {
-          const double* Bo = Bb[pc ^ 1];
+          const int o = bo(pc ^ 1);
 #pragma unroll
           for (int e = 0; e < NE; ++e) {
             const int rr = row_of(e), n = col_of(e);
-            accR[e] -= Bo[bfrag_index<C>(rr, n, 0)];
-            accI[e] -= Bo[bfrag_index<C>(rr, n, 1)];
+            accR[e] -= smem[o + bfrag_index<C>(rr, n, 0)];
+            accI[e] -= smem[o + bfrag_index<C>(rr, n, 1)];
           }
         }
-        ps_mma<C, AG>(Ay, Bb[pc], accR, accI, ms0, nt0, ln);
+        tile_mma<C, AG>(gy, ay_off, bo(pc), accR, accI, ms0, nt0, ln);
         if (j >= 1) {
-          write_B(Bb[pc ^ 1], accR, accI, (j == 1) ? 0.5 : 1.0);
+          write_B(bo(pc ^ 1), accR, accI, (j == 1) ? 0.5 : 1.0);
           pc ^= 1;
           lane_sync<C>();
         }
       }
     }
-    // U (times the plan phase, 1 for equiprop's symmetric plans) to A layout
-    write_A(Au, accR, accI, phase_one ? 1.0 : job.phase[0], phase_one ? 0.0 : job.phase[1]);
+    // U (times the plan phase, 1 for equiprop's symmetric plans) to A layout;
+    // in smem it overwrites 2X, dead since the powers were formed
+    write_A(gu, ax_off, accR, accI, phase_one ? 1.0 : job.phase[0],
+            phase_one ? 0.0 : job.phase[1]);
     sync_all();
     // ---- 5. V <- U V
-    write_B(Bb[0], Pr, Pi, 1.0);
+    write_B(bofs0, Pr, Pi, 1.0);
     lane_sync<C>();
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       accR[e] = 0.0;
       accI[e] = 0.0;
     }
-    ps_mma<C, AG>(Au, Bb[0], accR, accI, ms0, nt0, ln);
+    tile_mma<C, AG>(gu, ax_off, bofs0, accR, accI, ms0, nt0, ln);
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       Pr[e] = accR[e];

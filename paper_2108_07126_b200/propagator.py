@@ -26,7 +26,8 @@ import numpy as np
 
 from ._native import MODE, REDUCTION, check, lib
 from .chebyshev import ORDER_GRID, ChebyshevPlan, make_plan
-from .errors import (ConfigError, HermiticityError, SamplingParityError, ShapeError,
+from .errors import (AmplitudeBoundError, ConfigError, HermiticityError, SamplingParityError,
+                     ShapeError, StepTooLargeError,
                      StateMachineError)
 from .hamiltonian import (ControlAmplitudes, ControlSystem, Quadrature, check_pair,
                           simpson_triplets, spectral_bound)
@@ -221,11 +222,35 @@ class IntegratorContext:
         if not isinstance(amps, ControlAmplitudes):
             raise ShapeError(f"expected ControlAmplitudes, got {type(amps).__name__}")
         count = self.slice_count(amps.pts)
-        check_pair(self._system, amps)
-        plan = self.plan_for(amps.dt)
+        if amps.n_controls != self._system.n_controls:
+            raise ShapeError(f"amplitude table has {amps.n_controls} controls, "
+                             f"system has {self._system.n_controls}")
+        # |c| <= 1 is validated inside the lane kernels (no host pass over the
+        # table); the host pass runs only where the reference's error
+        # precedence needs it before another error can be raised
+        try:
+            plan = self.plan_for(amps.dt)
+        except StepTooLargeError:
+            check_pair(self._system, amps)
+            raise
         if self.checked:
+            check_pair(self._system, amps)
             self._check_hermitian(amps)
         return count, plan
+
+    def _run_checked(self, rc: int, amps: ControlAmplitudes) -> None:
+        """Raise the device-side amplitude violation with the reference's
+        message (``hamiltonian.py:170-174``), else map the code."""
+        if rc == 3:
+            idx = ctypes.c_int64(-1)
+            lib.sp_amplitude_violation(self._handle, ctypes.byref(idx))
+            if idx.value >= 0:
+                n = max(1, amps.n_controls)
+                k, i = divmod(idx.value, n)
+                raise AmplitudeBoundError(
+                    f"control amplitude {float(amps.values[k, i])!r} at sample {k}, "
+                    f"control {i} lies outside [-1, 1]")
+        check(rc, self._handle)
 
     def _check_hermitian(self, amps: ControlAmplitudes) -> None:
         """checked=True: Hermiticity of every slice exponent in the working
@@ -281,10 +306,10 @@ class IntegratorContext:
         count, plan = self._prepare(amps)
         out = np.empty((d, d), dtype=self._out_dtype())
         native = plan.to_native()
-        check(lib.sp_equiprop(self._handle, amps.values.ctypes.data_as(ctypes.c_void_p),
-                              amps.pts, amps.n_controls, amps.dt, ctypes.byref(native),
-                              REDUCTION[reduction], out.ctypes.data_as(ctypes.c_void_p)),
-              self._handle)
+        rc = lib.sp_equiprop(self._handle, amps.values.ctypes.data_as(ctypes.c_void_p),
+                             amps.pts, amps.n_controls, amps.dt, ctypes.byref(native),
+                             REDUCTION[reduction], out.ctypes.data_as(ctypes.c_void_p))
+        self._run_checked(rc, amps)
         return PropagatorResult(u=out, slice_count=count, plan=plan.summary())
 
     def equiprop_all(self, amps: ControlAmplitudes) -> CumulativeResult:
@@ -299,9 +324,10 @@ class IntegratorContext:
         count, plan = self._prepare(amps)
         out = np.empty((count, d, d), dtype=self._out_dtype())
         native = plan.to_native()
-        check(lib.sp_equiprop_all(self._handle, amps.values.ctypes.data_as(ctypes.c_void_p),
-                                  amps.pts, amps.n_controls, amps.dt, ctypes.byref(native),
-                                  out.ctypes.data_as(ctypes.c_void_p)), self._handle)
+        rc = lib.sp_equiprop_all(self._handle, amps.values.ctypes.data_as(ctypes.c_void_p),
+                                 amps.pts, amps.n_controls, amps.dt, ctypes.byref(native),
+                                 out.ctypes.data_as(ctypes.c_void_p))
+        self._run_checked(rc, amps)
         return CumulativeResult(u_all=out, slice_count=count, plan=plan.summary())
 
     # -- device-resident entry (bench / multi-GPU sharding) -------------------
@@ -345,6 +371,15 @@ class IntegratorContext:
         if algo not in self._ALGOS:
             raise ConfigError(f"unknown algorithm {algo!r}; expected {sorted(self._ALGOS)}")
         check(lib.sp_set_algorithm(self._handle, self._ALGOS[algo]), self._handle)
+
+    def amplitude_violation(self) -> int:
+        """Row-major index of the first |c| > 1 (or NaN) sample seen by the
+        last device-resident propagation, -1 if none (synchronises)."""
+        idx = ctypes.c_int64(-1)
+        rc = lib.sp_amplitude_violation(self._handle, ctypes.byref(idx))
+        if rc not in (0, 3):
+            check(rc, self._handle)
+        return idx.value
 
     def last_algorithm(self) -> dict:
         a = ctypes.c_int()

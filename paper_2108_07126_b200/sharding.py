@@ -20,7 +20,7 @@ from __future__ import annotations
 import numpy as np
 
 from .errors import ShapeError
-from .hamiltonian import ControlAmplitudes
+from .hamiltonian import ControlAmplitudes, check_pair
 from .propagator import IntegratorContext, PropagatorResult
 
 __all__ = ["partition", "shard_rows", "local_amplitudes", "ordered_product",
@@ -90,6 +90,7 @@ def equiprop_sharded(ctx: IntegratorContext, amps: ControlAmplitudes, *, group=N
     if amps.pts == 0:
         return ctx.equiprop(amps)
     count, plan = ctx._prepare(amps)
+    check_pair(ctx._system, amps)  # global host validation on every rank
     sub, a, b = local_amplitudes(ctx, amps, rank, world)
     if sub is None:
         block = np.eye(d, dtype=np.complex128)

@@ -1,0 +1,217 @@
+"""Public-API behaviour that needs the device (reference tests/test_propagator.py
+TestEquiprop / TestLifecycle / TestMagnusMode / TestEquipropAll and
+bindings/tests/test_binding.py, run against the B200 path)."""
+
+import numpy as np
+import pytest
+
+import paper_2108_07126_b200 as sp
+from paper_2108_07126_b200 import pysliceprop
+from helpers import expm_eigh, haar_unitary, random_hermitian
+
+pytestmark = pytest.mark.gpu
+
+SZ = np.array([[1.0, 0.0], [0.0, -1.0]], dtype=complex)
+SX = np.array([[0.0, 1.0], [1.0, 0.0]], dtype=complex)
+SY = np.array([[0.0, -1.0j], [1.0j, 0.0]], dtype=complex)
+
+
+def drift_qubit():
+    return sp.ControlSystem(SZ / 2.0)
+
+
+def driven_qubit():
+    return sp.ControlSystem(SZ / 2.0, [SX / 2.0, SY / 2.0])
+
+
+def driven_amps(pts, dt=0.02, wrf=1.0):
+    t = np.arange(pts) * dt
+    return sp.ControlAmplitudes(np.column_stack([np.cos(wrf * t), np.sin(wrf * t)]), dt)
+
+
+def sequential_product(mats):
+    acc = np.eye(mats[0].shape[0], dtype=complex)
+    for m in mats:
+        acc = m @ acc
+    return acc
+
+
+def dense_reference(system, amps, quadrature="midpoint"):
+    if quadrature == "midpoint":
+        slices = [amps.dt * (system.drift + sum(c * h for c, h in zip(row, system.controls)))
+                  for row in amps.values]
+    else:
+        v = amps.values
+        avg = (v[0:-1:2] + 4.0 * v[1::2] + v[2::2]) / 6.0
+        slices = [2.0 * amps.dt * (system.drift + sum(c * h for c, h in zip(row, system.controls)))
+                  for row in avg]
+    return sequential_product([expm_eigh(g) for g in slices])
+
+
+@pytest.mark.parametrize("d", [2, 4, 16, 32, 64, 128])
+def test_amplitude_violation_raised_from_device(d, rng):
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(random_hermitian(rng, d, 1.0),
+                                         [random_hermitian(rng, d, 1.0)] * 2))
+    values = np.zeros((40, 2))
+    values[25, 1] = 1.5
+    values[31, 0] = -2.0
+    with pytest.raises(sp.AmplitudeBoundError, match=r"1\.5 at sample 25, control 1"):
+        ctx.equiprop(sp.ControlAmplitudes(values, 0.01))
+    values[25, 1] = np.nan
+    with pytest.raises(sp.AmplitudeBoundError, match="sample 25, control 1"):
+        ctx.equiprop_all(sp.ControlAmplitudes(values, 0.01))
+    # the context stays usable
+    values[25, 1] = 0.0
+    values[31, 0] = 0.0
+    u = ctx.equiprop(sp.ControlAmplitudes(values, 0.01)).u
+    assert np.allclose(u.conj().T @ u, np.eye(d), atol=1e-12)
+
+
+def test_three_point_violation_found_in_shared_endpoints():
+    ctx = sp.create()
+    ctx.set_hamiltonian(driven_qubit(), magnus=True)
+    values = driven_amps(21).values.copy()
+    values[20, 1] = 1.0000001
+    with pytest.raises(sp.AmplitudeBoundError, match="sample 20, control 1"):
+        ctx.equiprop(sp.ControlAmplitudes(values, 0.1))
+
+
+def test_constant_drift_closed_form():
+    ctx = sp.create()
+    ctx.set_hamiltonian(drift_qubit())
+    result = ctx.equiprop(sp.ControlAmplitudes(np.zeros((10, 0)), 0.1))
+    assert np.abs(result.u - np.diag([np.exp(-0.5j), np.exp(0.5j)])).max() <= 1e-12
+    assert result.slice_count == 10
+
+
+def test_zero_hamiltonian_is_exact_identity():
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(np.zeros((2, 2))))
+    assert np.array_equal(ctx.equiprop(sp.ControlAmplitudes(np.zeros((6, 0)), 0.3)).u,
+                          np.eye(2))
+    ctx.set_hamiltonian(sp.ControlSystem(np.zeros((40, 40))))
+    assert np.array_equal(ctx.equiprop(sp.ControlAmplitudes(np.zeros((6, 0)), 0.3)).u,
+                          np.eye(40))
+
+
+def test_driven_qubit_and_simpson_against_dense_reference():
+    system = driven_qubit()
+    amps = driven_amps(25)
+    ctx = sp.create()
+    ctx.set_hamiltonian(system)
+    assert np.abs(ctx.equiprop(amps).u - dense_reference(system, amps)).max() <= 1e-12
+    ctx.set_hamiltonian(system, quadrature="simpson")
+    res = ctx.equiprop(amps)
+    assert np.abs(res.u - dense_reference(system, amps, "simpson")).max() <= 1e-12
+    assert res.slice_count == 12
+
+
+def test_composition_of_halves():
+    system = driven_qubit()
+    full = driven_amps(40)
+    ctx = sp.create()
+    ctx.set_hamiltonian(system)
+    first = sp.ControlAmplitudes(full.values[:20], full.dt)
+    second = sp.ControlAmplitudes(full.values[20:], full.dt)
+    u_halves = ctx.equiprop(second).u @ ctx.equiprop(first).u
+    assert np.abs(ctx.equiprop(full).u - u_halves).max() <= 1e-12
+
+
+def test_reload_replaces_system_and_dimension(rng):
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(SZ * np.pi / 2.0))
+    amps = sp.ControlAmplitudes(np.zeros((1, 0)), 1.0)
+    assert np.allclose(ctx.equiprop(amps).u, np.diag([-1j, 1j]), atol=1e-13)
+    ctx.set_hamiltonian(sp.ControlSystem(SX * np.pi / 2.0))
+    assert np.allclose(ctx.equiprop(amps).u, -1j * SX, atol=1e-13)
+    ctx.set_hamiltonian(sp.ControlSystem(random_hermitian(rng, 7, norm=1.0)))
+    assert ctx.equiprop(sp.ControlAmplitudes(np.zeros((3, 0)), 0.1)).u.shape == (7, 7)
+
+
+def test_contexts_are_independent():
+    a = sp.create(precision="fp64")
+    b = sp.create(precision="fp32")
+    a.set_hamiltonian(drift_qubit())
+    b.set_hamiltonian(drift_qubit())
+    amps = sp.ControlAmplitudes(np.zeros((5, 0)), 0.1)
+    assert a.equiprop(amps).u.dtype == np.complex128
+    assert b.equiprop(amps).u.dtype == np.complex64
+
+
+def test_magnus_agrees_with_simpson_on_commuting_problem():
+    system = sp.ControlSystem(SZ / 2.0, [SZ / 4.0])
+    amps = sp.ControlAmplitudes(np.linspace(-1.0, 1.0, 11)[:, None], 0.05)
+    m = sp.create()
+    m.set_hamiltonian(system, magnus=True)
+    s = sp.create()
+    s.set_hamiltonian(system, quadrature="simpson")
+    assert np.abs(m.equiprop(amps).u - s.equiprop(amps).u).max() <= 1e-13
+
+
+def test_magnus_plan_uses_commutator_bound():
+    system = driven_qubit()
+    ctx = sp.create()
+    ctx.set_hamiltonian(system, magnus=True)
+    amps = driven_amps(9)
+    expected = sp.magnus_spectral_bound(sp.build_effective_system(system), amps)
+    assert ctx.equiprop(amps).plan["beta"] == pytest.approx(expected)
+
+
+def test_equiprop_all_contract():
+    ctx = sp.create()
+    ctx.set_hamiltonian(driven_qubit())
+    amps = driven_amps(12)
+    cum = ctx.equiprop_all(amps)
+    assert cum.u_all.shape == (12, 2, 2) and cum.slice_count == 12
+    single = ctx.equiprop(sp.ControlAmplitudes(amps.values[:1], amps.dt)).u
+    assert np.abs(cum.u_all[0] - single).max() <= 1e-15
+    assert np.array_equal(cum.final, ctx.equiprop(amps, reduction="sequential").u)
+    for k in (2, 5, 8):
+        prefix = sp.ControlAmplitudes(amps.values[:k + 1], amps.dt)
+        assert np.abs(cum.u_all[k] - ctx.equiprop(prefix, reduction="sequential").u).max() \
+            <= 1e-14
+    for u in cum.u_all:
+        assert sp.one_norm(u.conj().T @ u - np.eye(2)) <= 1e-11
+    ctx.set_hamiltonian(driven_qubit(), magnus=True)
+    assert ctx.equiprop_all(driven_amps(11)).u_all.shape == (5, 2, 2)
+
+
+def test_fp32_pipeline():
+    ctx = sp.create(precision="fp32")
+    ctx.set_hamiltonian(driven_qubit())
+    u = ctx.equiprop(driven_amps(21)).u
+    assert u.dtype == np.complex64
+    assert sp.one_norm(u.conj().T @ u - np.eye(2)) <= 1e-4
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 8, 33, 64, 257, 1000])
+def test_reduction_all_counts(rng, n):
+    """Ordered products at awkward counts (odd carries, single lanes)."""
+    d = 4
+    h = random_hermitian(rng, d, norm=1.0)
+    c = random_hermitian(rng, d, norm=1.0)
+    values = rng.uniform(-1, 1, (n, 1))
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(h, [c]))
+    amps = sp.ControlAmplitudes(values, 0.1)
+    ref = sequential_product([expm_eigh(0.1 * (h + v[0] * c)) for v in values])
+    for red in ("pairwise", "sequential"):
+        assert np.abs(ctx.equiprop(amps, reduction=red).u - ref).max() <= 1e-13
+
+
+def test_binding_session_and_errors():
+    problem = dict(drift=0.5 * np.kron(SZ, np.eye(2)), controls=[0.5 * np.kron(SX, np.eye(2))],
+                   c=0.7 * np.cos(np.arange(21) * 0.05)[:, None], dt=0.05)
+    u = pysliceprop.equiprop(problem["drift"], problem["controls"], problem["c"], problem["dt"],
+                             magnus=True)
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(problem["drift"], problem["controls"]), magnus=True)
+    assert np.array_equal(u, ctx.equiprop(sp.ControlAmplitudes(problem["c"], 0.05)).u)
+    with pysliceprop.Session() as s:
+        s.set_hamiltonian(SZ / 2, [SX / 2])
+        with pytest.raises(pysliceprop.BindingError) as ei:
+            s.equiprop(np.full((5, 1), 3.0), 0.1)
+        assert ei.value.code == "amplitude-bound"
+        cum = s.equiprop(np.zeros((4, 1)), 0.1, cumulative=True)
+        assert cum.shape == (4, 2, 2)
