@@ -18,6 +18,7 @@
 #include "kernels.cuh"
 #include "kernels_tc.cuh"
 #include "kernels_ps.cuh"
+#include "kernels_ps3.cuh"
 
 using namespace sp;
 
@@ -40,8 +41,14 @@ using PS32 = PSCfg<32, 32, 1, 2, 4, 1, 1, true>;
 using PS64 = PSCfg<64, 32, 1, 4, 4, 1, 2, false>;
 using PS128 = PSCfg<128, 32, 1, 4, 8, 1, 4, false>;
 using PS256 = PSCfg<256, 16, 2, 2, 8, 1, 16, false>;
+// ... and with 3-multiplication complex products (3-plane operands)
+using P3_16 = PS3Cfg<16, 16, 1, 2, 1, 4, 1, true>;
+using P3_32 = PS3Cfg<32, 32, 1, 2, 4, 1, 1, true>;
+using P3_64 = PS3Cfg<64, 32, 1, 4, 4, 1, 2, false>;
+using P3_128 = PS3Cfg<128, 32, 1, 4, 8, 1, 4, false>;
+using P3_256 = PS3Cfg<256, 16, 2, 2, 8, 1, 16, false>;
 
-enum Algo { ALGO_AUTO = 0, ALGO_CLENSHAW = 1, ALGO_PS = 2 };
+enum Algo { ALGO_AUTO = 0, ALGO_CLENSHAW = 1, ALGO_PS = 2, ALGO_PS3 = 3 };
 
 // GEMMs per slice: Clenshaw m; PS (s-1) + (r-1) + 1, r = ceil((m+1)/s)
 int ps_cost(int m, int s) {
@@ -50,8 +57,10 @@ int ps_cost(int m, int s) {
 }
 
 int ps_choose(int m) {
+  // s <= 4: the power blocks T_1..T_{s-1} live in TMEM (4 blocks per
+  // thread); larger s never lowers the cost for m <= 25
   int best = 0, cost = m;
-  for (int s = 2; s <= 6; ++s) {
+  for (int s = 2; s <= 4; ++s) {
     const int r = (m + 1 + s - 1) / s;
     if (r < 2 || r * s > PS_MAXC) continue;
     if (ps_cost(m, s) < cost) {
@@ -114,6 +123,15 @@ int family_for(int d, int* D) {
 }
 
 const char* family_kernel_name(int fam, int algo) {
+  if (algo == 3) {
+    switch (fam) {
+      case FAM_T16: return "lane_ps3_kernel<D16>";
+      case FAM_T32: return "lane_ps3_kernel<D32>";
+      case FAM_T64: return "lane_ps3_kernel<D64,group2>";
+      case FAM_T128: return "lane_ps3_kernel<D128,group4>";
+      case FAM_T256: return "lane_ps3_kernel<D256,group16>";
+    }
+  }
   if (algo == 2) {
     switch (fam) {
       case FAM_T16: return "lane_ps_kernel<D16>";
@@ -157,7 +175,7 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   int fam = FAM_NONE, D = 0;
   DevBuf terms, amps, lanes, ctab, tree0, tree1, xglob, gctr, result, out, cumP, cumE, cumO,
-      fold_scratch, psA, tpriv, viol;
+      fold_scratch, psA, tpriv, viol, terms3;
   cudaStream_t viol_stream = nullptr;
   int64_t viol_pts = 0;
   int algo = 0;          // Algo
@@ -240,6 +258,8 @@ int tc_prepare(sp_ctx* ctx) {
 
 template <class C>
 int ps_prepare(sp_ctx* ctx);
+template <class C>
+int ps3_prepare(sp_ctx* ctx);
 
 // permute + pad the host terms into the family's device layout
 int upload_terms(sp_ctx* ctx) {
@@ -270,6 +290,32 @@ int upload_terms(sp_ctx* ctx) {
   if (rc) return rc;
   CUDA_TRY(ctx, cudaMemcpy(ctx->terms.p, h.data(), h.size() * sizeof(double),
                            cudaMemcpyHostToDevice));
+  if (!(ctx->fam == FAM_S2 || ctx->fam == FAM_S4)) {
+    // 3-plane (re, im, re+im) copy for the 3-multiplication kernels
+    const size_t xd3 = (size_t)3 * D * D;
+    std::vector<double> h3((size_t)T * xd3, 0.0);
+    for (int t = 0; t < T; ++t)
+      for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+          const double* src = &ctx->terms_host[(((size_t)t * d + r) * d + c) * 2];
+          h3[t * xd3 + xfrag3_index(D, r, c, 0)] = src[0];
+          h3[t * xd3 + xfrag3_index(D, r, c, 1)] = src[1];
+          h3[t * xd3 + xfrag3_index(D, r, c, 2)] = src[0] + src[1];
+        }
+    rc = ensure(ctx, ctx->terms3, h3.size() * sizeof(double));
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaMemcpy(ctx->terms3.p, h3.data(), h3.size() * sizeof(double),
+                             cudaMemcpyHostToDevice));
+  }
+  switch (ctx->fam) {
+    case FAM_T16: rc = ps3_prepare<P3_16>(ctx); break;
+    case FAM_T32: rc = ps3_prepare<P3_32>(ctx); break;
+    case FAM_T64: rc = ps3_prepare<P3_64>(ctx); break;
+    case FAM_T128: rc = ps3_prepare<P3_128>(ctx); break;
+    case FAM_T256: rc = ps3_prepare<P3_256>(ctx); break;
+    default: break;
+  }
+  if (rc) return rc;
   switch (ctx->fam) {
     case FAM_T16: rc = tc_prepare<Cfg16>(ctx); break;
     case FAM_T32: rc = tc_prepare<Cfg32>(ctx); break;
@@ -350,18 +396,28 @@ int tc_launch(sp_ctx* ctx, const SliceJob& job, int lanes, double2* lane_out,
   return SP_OK;
 }
 
-template <class C>
+// lane_ps_kernel (4 real products per complex product) or lane_ps3_kernel (3)
+template <class C, bool M3>
+constexpr auto ps_kernel() {
+  if constexpr (M3)
+    return lane_ps3_kernel<C>;
+  else
+    return lane_ps_kernel<C>;
+}
+
+template <class C, bool M3 = false>
 int ps_prepare(sp_ctx* ctx) {
-  CUDA_TRY(ctx, cudaFuncSetAttribute(lane_ps_kernel<C>,
+  CUDA_TRY(ctx, cudaFuncSetAttribute(ps_kernel<C, M3>(),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)C::SMEM));
   return SP_OK;
 }
 
-template <class C>
+template <class C, bool M3 = false>
 int ps_lanes(sp_ctx* ctx, int64_t n) {
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_ps_kernel<C>, C::THREADS, C::SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ps_kernel<C, M3>(), C::THREADS, C::SMEM);
+  if constexpr (M3) occ = std::min(occ, 512 / C::TMEM_COLS);  // TMEM columns per SM
   if (occ < 1) occ = 1;
   int64_t ctas = (int64_t)ctx->sms * occ;
   int64_t units = (C::GPL > 1) ? ctas / C::GPL : ctas * C::LPC;
@@ -369,6 +425,11 @@ int ps_lanes(sp_ctx* ctx, int64_t n) {
 }
 
 template <class C>
+int ps3_prepare(sp_ctx* ctx) { return ps_prepare<C, true>(ctx); }
+template <class C>
+int ps3_lanes(sp_ctx* ctx, int64_t n) { return ps_lanes<C, true>(ctx, n); }
+
+template <class C, bool M3 = false>
 int ps_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double2* prefix_out,
               cudaStream_t st) {
   const int groups = (lanes + C::LPC - 1) / C::LPC;
@@ -378,7 +439,7 @@ int ps_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double
                   (size_t)grid * (pj.s - 1) * NE * C::THREADS * sizeof(double2));
   if (rc) return rc;
   double2* tpriv = (double2*)ctx->tpriv.p;
-  const double* terms = (const double*)ctx->terms.p;
+  const double* terms = (const double*)(M3 ? ctx->terms3.p : ctx->terms.p);
   double* ga = nullptr;
   unsigned* ctr = nullptr;
   if (C::GPL > 1) {
@@ -392,17 +453,23 @@ int ps_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double
     void* args[] = {(void*)&pj, (void*)&terms, (void*)&lanes, (void*)&ga, (void*)&ctr,
                     (void*)&tpriv, (void*)&lane_out, (void*)&prefix_out};
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)lane_ps_kernel<C>, dim3(grid),
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)ps_kernel<C, M3>(), dim3(grid),
                                               dim3(C::THREADS), args, C::SMEM, st));
   } else {
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-    lane_ps_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(pj, terms, lanes, ga, ctr, tpriv,
-                                                         lane_out, prefix_out);
+    ps_kernel<C, M3>()<<<grid, C::THREADS, C::SMEM, st>>>(pj, terms, lanes, ga, ctr, tpriv,
+                                                          lane_out, prefix_out);
   }
   CUDA_TRY(ctx, cudaGetLastError());
   if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
   ++ctx->launches;
   return SP_OK;
+}
+
+template <class C>
+int ps3_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double2* prefix_out,
+               cudaStream_t st) {
+  return ps_launch<C, true>(ctx, pj, lanes, lane_out, prefix_out, st);
 }
 
 template <int D>
@@ -512,8 +579,40 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     return SP_OK;
   }
   const int ps_s = (ctx->algo == ALGO_CLENSHAW) ? 0
-                   : (ctx->algo == ALGO_PS) ? std::max(2, ps_choose(job.m) ? ps_choose(job.m) : 2)
-                                            : ps_choose(job.m);
+                   : (ctx->algo == ALGO_PS || ctx->algo == ALGO_PS3)
+                         ? std::max(2, ps_choose(job.m) ? ps_choose(job.m) : 2)
+                         : ps_choose(job.m);
+  const bool three_m = ps_s > 0 && ctx->algo != ALGO_PS;  // auto: 3-multiplication form
+  if (ps_s > 0 && three_m) {
+    PSJob pj;
+    std::memset(&pj, 0, sizeof(pj));
+    pj.base = job;
+    pj.s = ps_s;
+    ps_coefficients(job.coef, job.m, ps_s, pj.alpha, &pj.r);
+    switch (ctx->fam) {
+      case FAM_T16: lanes = ps3_lanes<P3_16>(ctx, n); break;
+      case FAM_T32: lanes = ps3_lanes<P3_32>(ctx, n); break;
+      case FAM_T64: lanes = ps3_lanes<P3_64>(ctx, n); break;
+      case FAM_T128: lanes = ps3_lanes<P3_128>(ctx, n); break;
+      case FAM_T256: lanes = ps3_lanes<P3_256>(ctx, n); break;
+    }
+    int rc = ensure(ctx, ctx->lanes, (size_t)lanes * dd * sizeof(double2));
+    if (rc) return rc;
+    double2* lane_out = (double2*)ctx->lanes.p;
+    switch (ctx->fam) {
+      case FAM_T16: rc = ps3_launch<P3_16>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T32: rc = ps3_launch<P3_32>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T64: rc = ps3_launch<P3_64>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T128: rc = ps3_launch<P3_128>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T256: rc = ps3_launch<P3_256>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+    }
+    if (rc) return rc;
+    ctx->last_algo = ALGO_PS3;
+    ctx->last_gemms = ps_cost(job.m, ps_s);
+    *prods = lane_out;
+    *count = lanes;
+    return SP_OK;
+  }
   if (ps_s > 0) {
     PSJob pj;
     std::memset(&pj, 0, sizeof(pj));
@@ -655,7 +754,9 @@ int prepare_device(sp_ctx* ctx) {
 double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
   const double D = ctx->D;
   (void)m;
-  return (double)n * (8.0 * D * D * D * ctx->last_gemms + 4.0 * D * D * ctx->n_terms);
+  // 3-multiplication products execute 3/4 of the real FP64 MMA work
+  const double f = (ctx->last_algo == ALGO_PS3) ? 6.0 : 8.0;
+  return (double)n * (f * D * D * D * ctx->last_gemms + 4.0 * D * D * ctx->n_terms);
 }
 
 // total propagator on the device -> d x d in d_out (output dtype)
@@ -810,7 +911,7 @@ int sp_free(sp_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->terms, &ctx->amps,  &ctx->lanes, &ctx->ctab, &ctx->tree0,
                       &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
                       &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch,
-                      &ctx->psA,   &ctx->tpriv, &ctx->viol};
+                      &ctx->psA,   &ctx->tpriv, &ctx->viol, &ctx->terms3};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -976,8 +1077,8 @@ int sp_amplitude_violation(sp_ctx* ctx, int64_t* index) {
 
 int sp_set_algorithm(sp_ctx* ctx, int algo) {
   if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
-  if (algo < ALGO_AUTO || algo > ALGO_PS)
-    return fail(ctx, SP_E_CONFIG, "unknown algorithm %d (0 auto, 1 clenshaw, 2 ps)", algo);
+  if (algo < ALGO_AUTO || algo > ALGO_PS3)
+    return fail(ctx, SP_E_CONFIG, "unknown algorithm %d (0 auto, 1 clenshaw, 2 ps, 3 ps3m)", algo);
   ctx->algo = algo;
   return SP_OK;
 }

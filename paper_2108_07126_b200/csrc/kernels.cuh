@@ -52,6 +52,95 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   return v;
 }
 
+// ---------------------------------------------------------------------------
+// Tensor memory (TMEM) as a per-thread scratch extension of the register
+// file: tcgen05.alloc/dealloc (warp-collective), 32x32b loads/stores (thread i
+// of warp w owns TMEM lane 32*(w%4)+i).  The FP64 MMAs cannot use TMEM
+// accumulators (tcgen05 has no f64 kind), but the 256 KB per SM holds the
+// running product and the Chebyshev power blocks that would otherwise round
+// trip through L2.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// 4 complex doubles <-> 16 consecutive 32-bit columns of this thread's lane
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const double* re, const double* im) {
+  uint32_t w[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    w[4 * q + 0] = (uint32_t)__double2loint(re[q]);
+    w[4 * q + 1] = (uint32_t)__double2hiint(re[q]);
+    w[4 * q + 2] = (uint32_t)__double2loint(im[q]);
+    w[4 * q + 3] = (uint32_t)__double2hiint(im[q]);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+      "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]),
+      "r"(w[15])
+      : "memory");
+}
+// raw 16-column load; the values are valid only after tmem_wait_ld()
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&w)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+        "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
+        "=r"(w[14]), "=r"(w[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_unpack4(const uint32_t (&w)[16], double* re, double* im) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    re[q] = __hiloint2double((int)w[4 * q + 1], (int)w[4 * q + 0]);
+    im[q] = __hiloint2double((int)w[4 * q + 3], (int)w[4 * q + 2]);
+  }
+}
+// load NE complex doubles (NE % 4 == 0) from 4*NE consecutive columns
+template <int NE>
+__device__ __forceinline__ void tmem_load_block(uint32_t taddr, double (&re)[NE],
+                                                double (&im)[NE]) {
+  uint32_t w[NE / 4][16];
+#pragma unroll
+  for (int q = 0; q < NE / 4; ++q) tmem_ld16(taddr + 16 * q, w[q]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int q = 0; q < NE / 4; ++q) tmem_unpack4(w[q], &re[4 * q], &im[4 * q]);
+}
+template <int NE>
+__device__ __forceinline__ void tmem_store_block(uint32_t taddr, const double (&re)[NE],
+                                                 const double (&im)[NE]) {
+#pragma unroll
+  for (int q = 0; q < NE / 4; ++q) tmem_st4(taddr + 16 * q, &re[4 * q], &im[4 * q]);
+  tmem_wait_st();
+}
+
 // Weight of expansion term t >= 1 for slice s (term 0 = drift, weight 1).
 //   midpoint  hamiltonian.py:199-201        w = c_{s,t-1}
 //   simpson   hamiltonian.py:202-205        w = (c1 + 4 c2 + c3) / 6

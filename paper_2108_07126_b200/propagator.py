@@ -361,7 +361,7 @@ class IntegratorContext:
                                     REDUCTION[reduction], ctypes.c_void_p(out_ptr),
                                     ctypes.c_void_p(stream)), self._handle)
 
-    _ALGOS = {"auto": 0, "clenshaw": 1, "ps": 2}
+    _ALGOS = {"auto": 0, "clenshaw": 1, "ps": 2, "ps3m": 3}
 
     def set_algorithm(self, algo: str = "auto") -> None:
         """Series evaluation scheme: "auto" (Paterson-Stockmeyer in the
@@ -385,7 +385,7 @@ class IntegratorContext:
         a = ctypes.c_int()
         g = ctypes.c_int()
         check(lib.sp_last_algorithm(self._handle, ctypes.byref(a), ctypes.byref(g)), self._handle)
-        return {"algorithm": {0: "none", 1: "clenshaw", 2: "ps"}.get(a.value, "?"),
+        return {"algorithm": {0: "none", 1: "clenshaw", 2: "ps", 3: "ps3m"}.get(a.value, "?"),
                 "gemms_per_slice": g.value}
 
     def set_profiling(self, enabled: bool = True) -> None:

@@ -98,7 +98,7 @@ def test_convergence_orders_reproduced():
 TC_CASES = [c for c in CASES if c["kind"] != "zero" and c.get("d", 2) >= 5]
 
 
-@pytest.mark.parametrize("algo", ["clenshaw", "ps"])
+@pytest.mark.parametrize("algo", ["clenshaw", "ps", "ps3m"])
 @pytest.mark.parametrize("case", TC_CASES, ids=[c["name"] for c in TC_CASES])
 def test_both_series_schemes_match_reference(case, algo, golden):
     """The tensor-core families evaluate the same plan polynomial either by
