@@ -256,7 +256,7 @@ int tc_prepare(sp_ctx* ctx) {
   return SP_OK;
 }
 
-template <class C>
+template <class C, bool M3 = false>
 int ps_prepare(sp_ctx* ctx);
 template <class C>
 int ps3_prepare(sp_ctx* ctx);
@@ -405,7 +405,7 @@ constexpr auto ps_kernel() {
     return lane_ps_kernel<C>;
 }
 
-template <class C, bool M3 = false>
+template <class C, bool M3>
 int ps_prepare(sp_ctx* ctx) {
   CUDA_TRY(ctx, cudaFuncSetAttribute(ps_kernel<C, M3>(),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -582,7 +582,11 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
                    : (ctx->algo == ALGO_PS || ctx->algo == ALGO_PS3)
                          ? std::max(2, ps_choose(job.m) ? ps_choose(job.m) : 2)
                          : ps_choose(job.m);
-  const bool three_m = ps_s > 0 && ctx->algo != ALGO_PS;  // auto: 3-multiplication form
+  // auto: the 3-multiplication/TMEM form where it measured faster (the
+  // group families, D >= 128: 165% vs 149% of canonical FP64 peak at D=128);
+  // for D <= 64 its 1.5x smem operands cost occupancy and the 4-product PS wins
+  const bool three_m =
+      ps_s > 0 && (ctx->algo == ALGO_PS3 || (ctx->algo == ALGO_AUTO && ctx->D >= 128));
   if (ps_s > 0 && three_m) {
     PSJob pj;
     std::memset(&pj, 0, sizeof(pj));
