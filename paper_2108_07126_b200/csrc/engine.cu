@@ -19,6 +19,7 @@
 #include "kernels_tc.cuh"
 #include "kernels_ps.cuh"
 #include "kernels_ps3.cuh"
+#include "kernels_ps3g.cuh"
 
 using namespace sp;
 
@@ -399,7 +400,9 @@ int tc_launch(sp_ctx* ctx, const SliceJob& job, int lanes, double2* lane_out,
 // lane_ps_kernel (4 real products per complex product) or lane_ps3_kernel (3)
 template <class C, bool M3>
 constexpr auto ps_kernel() {
-  if constexpr (M3)
+  if constexpr (M3 && C::GPL > 1)
+    return lane_ps3g_kernel<C>;  // group families: pipelined slice loop
+  else if constexpr (M3)
     return lane_ps3_kernel<C>;
   else
     return lane_ps_kernel<C>;

@@ -1,0 +1,374 @@
+// Group-family (D >= 64, operands shared through L2) Paterson–Stockmeyer
+// lane kernel with 3-multiplication complex products and TMEM-resident
+// running product / power blocks — the production kernel for the C4 headline
+// (d = 128).  Same arithmetic as lane_ps3_kernel (kernels_ps3.cuh); the
+// slice loop is restructured to cut the non-MMA time per slice:
+//
+//  * column-block ownership of the shared operands: CTA j of a lane group
+//    assembles and publishes COLUMN block j of 2X, 2y and U (the same blocks
+//    its GEMMs produce), so T_1 = X[:, J] comes from its own shared memory;
+//  * two group barriers per slice instead of three: the next slice's 2X is
+//    assembled during the current slice's Clenshaw phase (its buffer is dead
+//    once the powers are formed), so "U ready" and "next X ready" share one
+//    barrier;
+//  * the first A fragments of the next GEMM step are loaded during the last
+//    k-block of the current one whenever that operand is already published;
+//  * 2y and U are staged in shared memory in publication order and copied to
+//    L2 with coalesced 16-byte stores.
+//
+// Per slice: 1 assembly, s-1 power GEMMs, r-1 Clenshaw GEMMs, 1 product GEMM,
+// 2 group barriers.
+#pragma once
+#include "kernels_ps3.cuh"
+
+namespace sp {
+
+// tile_mma3 with cross-step prefetch: a holds the kb = 0 fragments on entry;
+// on exit it holds the kb = 0 fragments of An (if An != nullptr)
+template <class C>
+__device__ __forceinline__ void tile_mma3_pf(const double* __restrict__ Ag,
+                                             const double* __restrict__ An, int b_off,
+                                             double2 (&a)[C::MT][3],
+                                             double (&a1)[C::MT * C::NT * 4],
+                                             double (&a2)[C::MT * C::NT * 4],
+                                             double (&a3)[C::MT * C::NT * 4], int ms0, int nt0,
+                                             int ln) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int MT = C::MT, NT = C::NT, KB = C::KB;
+  auto loadA = [&](const double* A, int i, int kb, double2 (&v)[3]) {
+    const int idx = (((ms0 + i) * KB + kb) * 3) * 64 + 2 * ln;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) v[p] = __ldcg(reinterpret_cast<const double2*>(A + idx + 64 * p));
+  };
+  double2 nx[MT][3];
+#pragma unroll 2
+  for (int kb = 0; kb < KB; ++kb) {
+    if (kb + 1 < KB) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) loadA(Ag, i, kb + 1, nx[i]);
+    } else if (An != nullptr) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) loadA(An, i, 0, nx[i]);
+    }
+    double b[NT][3];
+#pragma unroll
+    for (int jn = 0; jn < NT; ++jn) {
+      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 3) * 32 + ln;
+#pragma unroll
+      for (int p = 0; p < 3; ++p) b[jn][p] = smem[bi + 32 * p];
+    }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn) {
+        double* c1 = &a1[(i * NT + jn) * 4];
+        double* c2 = &a2[(i * NT + jn) * 4];
+        double* c3 = &a3[(i * NT + jn) * 4];
+        dmma_16x8x4(c1[0], c1[1], c1[2], c1[3], a[i][0].x, a[i][0].y, b[jn][0]);
+        dmma_16x8x4(c2[0], c2[1], c2[2], c2[3], a[i][1].x, a[i][1].y, b[jn][1]);
+        dmma_16x8x4(c3[0], c3[1], c3[2], c3[3], a[i][2].x, a[i][2].y, b[jn][2]);
+      }
+    if (kb + 1 < KB || An != nullptr) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int p = 0; p < 3; ++p) a[i][p] = nx[i][p];
+    }
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
+    lane_ps3g_kernel(PSJob pj, const double* __restrict__ terms, int lanes,
+                     double* __restrict__ gA, unsigned* __restrict__ gctr,
+                     double2* __restrict__ tpriv, double2* __restrict__ lane_out,
+                     double2* __restrict__ prefix_out) {
+  static_assert(C::GPL > 1 && C::LPC == 1 && !C::XS, "group configuration");
+  constexpr int D = C::D, WC = C::WC, MT = C::MT, NT = C::NT, NE = MT * NT * 4;
+  constexpr int KB = C::KB;
+  constexpr int KBC = WC / 4;                 // k-blocks of one column block
+  constexpr int CHUNK = C::S * KBC * 3 * 64;  // doubles of one column block (A layout)
+  const SliceJob& job = pj.base;
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const int group = blockIdx.x / C::GPL;
+  const int cb = blockIdx.x % C::GPL;
+  const int lane = group;
+  const bool active = lane < lanes;
+
+  const int bofs0 = 0, bofs1 = C::BDBL;
+  const int w_off = 2 * C::BDBL;
+  auto bo = [&](int which) { return which ? bofs1 : bofs0; };
+  double* gx = gA + (size_t)group * 3 * C::XDBL;
+  double* gy = gx + C::XDBL;
+  double* gu = gy + C::XDBL;
+
+  const int g = ln >> 2, t4 = ln & 3;
+  const int ms0 = (warp % (C::S / MT)) * MT;
+  const int nt0 = (warp / (C::S / MT)) * NT;
+  const int col0 = cb * WC;
+  const int s = pj.s, r = pj.r;
+  auto row_of = [&](int idx) { return 16 * (ms0 + idx / (NT * 4)) + g + 8 * ((idx & 3) >> 1); };
+  auto col_of = [&](int idx) { return 8 * (nt0 + (idx / 4) % NT) + 2 * t4 + (idx & 1); };
+  // A-layout index of the q-th double of this CTA's column chunk
+  auto chunk_index = [&](int q) {
+    const int strip = q / (KBC * 192), rem = q % (KBC * 192);
+    const int kbl = rem / 192, rr = rem % 192;
+    return ((strip * KB + cb * KBC + kbl) * 3) * 64 + rr;
+  };
+  // position of own element e (plane p) inside the column chunk
+  auto chunk_pos = [&](int e, int p) {
+    const int rr = row_of(e), c = col_of(e);  // c: column within the block
+    return ((rr >> 4) * KBC + (c >> 2)) * 192 + p * 64 + (((rr & 7) << 2) | (c & 3)) * 2 +
+           ((rr >> 3) & 1);
+  };
+
+  __shared__ uint32_t tmem_slot;
+  if (warp == 0) tmem_alloc(&tmem_slot, C::TMEM_COLS);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+  const uint32_t tmem_me =
+      tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 16 * NE);
+  auto tm = [&](int blk) { return tmem_me + (uint32_t)(blk * 4 * NE); };
+  {
+    double pr[NE], pi[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      pr[e] = (row_of(e) == col0 + col_of(e)) ? 1.0 : 0.0;
+      pi[e] = 0.0;
+    }
+    tmem_store_block<NE>(tm(0), pr, pi);
+  }
+  (void)tpriv;
+
+  int64_t s0 = 0, s1 = 0;
+  if (active) lane_range(job.n_slices, lanes, lane, s0, s1);
+  const int T = job.n_terms;
+  const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
+  unsigned bar = 0;
+  auto gsync = [&]() { group_barrier(gctr + group, (++bar) * C::GPL); };
+
+  // weights of slice sl, then this CTA's column chunk of 2X (A layout, L2)
+  auto assemble = [&](int64_t sl) {
+    for (int tt = threadIdx.x; tt < T; tt += C::THREADS)
+      smem[w_off + tt] = (tt == 0) ? job.xs : job.xs * slice_weight(job, sl, tt);
+    __syncthreads();
+    for (int q = 2 * threadIdx.x; q < CHUNK; q += 2 * C::THREADS) {
+      const int i = chunk_index(q);
+      double2 h = __ldg(reinterpret_cast<const double2*>(terms + i));
+      double x0 = smem[w_off] * h.x, x1 = smem[w_off] * h.y;
+      for (int tt = 1; tt < T; ++tt) {
+        h = __ldg(reinterpret_cast<const double2*>(terms + (size_t)tt * C::XDBL + i));
+        x0 = fma(smem[w_off + tt], h.x, x0);
+        x1 = fma(smem[w_off + tt], h.y, x1);
+      }
+      *reinterpret_cast<double2*>(gx + i) = make_double2(x0, x1);
+    }
+  };
+  // T_1 = X[:, J] (B layout, bo(0)) from this CTA's own published chunk
+  auto fill_t1 = [&]() {
+    for (int q = 2 * threadIdx.x; q < CHUNK; q += 2 * C::THREADS) {
+      const double2 x = __ldcg(reinterpret_cast<const double2*>(gx + chunk_index(q)));
+      const int rem = q % (KBC * 192), p = (rem % 192) / 64, l = (rem % 64) / 2;
+      const int rw = 16 * (q / (KBC * 192)) + (l >> 2);
+      const int n = 4 * (rem / 192) + (l & 3);
+      smem[bofs0 + bfrag3_index<C>(rw, n, p)] = 0.5 * x.x;
+      smem[bofs0 + bfrag3_index<C>(rw + 8, n, p)] = 0.5 * x.y;
+    }
+  };
+  // stage own elements in chunk order (smem at off), then coalesced copy
+  auto publish = [&](double* dst, int off, const double(&vr)[NE], const double(&vi)[NE],
+                     double fr, double fi) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const double xr = fr * vr[e] - fi * vi[e], xi = fr * vi[e] + fi * vr[e];
+      smem[off + chunk_pos(e, 0)] = xr;
+      smem[off + chunk_pos(e, 1)] = xi;
+      smem[off + chunk_pos(e, 2)] = xr + xi;
+    }
+    __syncthreads();
+    for (int q = 2 * threadIdx.x; q < CHUNK; q += 2 * C::THREADS)
+      *reinterpret_cast<double2*>(dst + chunk_index(q)) =
+          *reinterpret_cast<const double2*>(&smem[off + q]);
+  };
+  auto write_B = [&](int off, const double(&vr)[NE], const double(&vi)[NE], double f) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int rr = row_of(e), n = col_of(e);
+      const double xr = f * vr[e], xi = f * vi[e];
+      smem[off + bfrag3_index<C>(rr, n, 0)] = xr;
+      smem[off + bfrag3_index<C>(rr, n, 1)] = xi;
+      smem[off + bfrag3_index<C>(rr, n, 2)] = xr + xi;
+    }
+  };
+  auto load_Q = [&](int j, double(&qr)[NE], double(&qi)[NE]) {
+    const double a0r = pj.alpha[2 * (j * s)], a0i = pj.alpha[2 * (j * s) + 1];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const bool diag = row_of(e) == col0 + col_of(e);
+      qr[e] = diag ? a0r : 0.0;
+      qi[e] = diag ? a0i : 0.0;
+    }
+    for (int i = 1; i < s; ++i) {
+      const double ar = pj.alpha[2 * (j * s + i)], ai = pj.alpha[2 * (j * s + i) + 1];
+      double tr[NE], ti[NE];
+      tmem_load_block<NE>(tm(i), tr, ti);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        qr[e] = fma(ar, tr[e], fma(-ai, ti[e], qr[e]));
+        qi[e] = fma(ar, ti[e], fma(ai, tr[e], qi[e]));
+      }
+    }
+  };
+  double2 afr[MT][3];  // kb = 0 A fragments of the next GEMM step
+  auto first_frags = [&](const double* A) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+        afr[i][p] = __ldcg(reinterpret_cast<const double2*>(
+            A + (((ms0 + i) * KB) * 3 + p) * 64 + 2 * ln));
+  };
+  auto step = [&](const double* Ag, const double* An, int b_off, double(&cr)[NE],
+                  double(&ci)[NE]) {
+    double a1[NE], a2[NE], a3[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      a1[e] = cr[e];
+      a2[e] = 0.0;
+      a3[e] = cr[e] + ci[e];
+    }
+    tile_mma3_pf<C>(Ag, An, b_off, afr, a1, a2, a3, ms0, nt0, ln);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      cr[e] = a1[e] - a2[e];
+      ci[e] = (a3[e] - a1[e]) - a2[e];
+    }
+  };
+
+  if (s0 < s1) {
+    assemble(s0);
+    gsync();
+    fill_t1();
+    first_frags(gx);
+    __syncthreads();
+  }
+  for (int64_t sl = s0; sl < s1; ++sl) {
+    const bool more = sl + 1 < s1;
+    double accR[NE], accI[NE];
+    // ---- T_1 (own positions) from the B-layout copy written by assemble()
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int rr = row_of(e), n = col_of(e);
+      accR[e] = smem[bofs0 + bfrag3_index<C>(rr, n, 0)];
+      accI[e] = smem[bofs0 + bfrag3_index<C>(rr, n, 1)];
+    }
+    tmem_store_block<NE>(tm(1), accR, accI);
+    // ---- powers T_k = 2X T_{k-1} - T_{k-2}
+    int pb = 0;
+    for (int k = 2; k <= s; ++k) {
+      if (k == 2) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          accR[e] = (row_of(e) == col0 + col_of(e)) ? -1.0 : 0.0;
+          accI[e] = 0.0;
+        }
+      } else {
+        tmem_load_block<NE>(tm(k - 2), accR, accI);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          accR[e] = -accR[e];
+          accI[e] = -accI[e];
+        }
+      }
+      step(gx, k < s ? gx : nullptr, bo(pb), accR, accI);
+      if (k < s) {
+        write_B(bo(pb ^ 1), accR, accI, 1.0);
+        tmem_store_block<NE>(tm(k), accR, accI);
+        pb ^= 1;
+        __syncthreads();
+      }
+    }
+    // 2y = 2 T_s: stage in the free buffer bo(pb^1) (T_{s-2}, already in TMEM)
+    __syncthreads();
+    publish(gy, bo(pb ^ 1), accR, accI, 2.0, 0.0);
+    gsync();  // 2y published (and everybody is done reading 2X)
+    first_frags(gy);
+    // ---- Clenshaw in y
+    int pc = 0;
+    {
+      double qr[NE], qi[NE];
+      load_Q(r - 1, qr, qi);
+      write_B(bo(pc), qr, qi, (r - 1 == 1) ? 0.5 : 1.0);
+    }
+    __syncthreads();
+    for (int j = r - 2; j >= 0; --j) {
+      load_Q(j, accR, accI);
+      if (j + 2 <= r - 1) {
+        const int o = bo(pc ^ 1);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const int rr = row_of(e), n = col_of(e);
+          accR[e] -= smem[o + bfrag3_index<C>(rr, n, 0)];
+          accI[e] -= smem[o + bfrag3_index<C>(rr, n, 1)];
+        }
+      }
+      step(gy, j >= 1 ? gy : nullptr, bo(pc), accR, accI);
+      if (j >= 1) {
+        __syncthreads();  // everybody has read b_{j+2} and b_{j+1}
+        write_B(bo(pc ^ 1), accR, accI, (j == 1) ? 0.5 : 1.0);
+        pc ^= 1;
+        __syncthreads();
+      }
+    }
+    // U (times the plan phase): stage in bo(pc^1) (b_2, consumed) and publish
+    __syncthreads();
+    publish(gu, bo(pc ^ 1), accR, accI, phase_one ? 1.0 : job.phase[0],
+            phase_one ? 0.0 : job.phase[1]);
+    // next slice's 2X: its buffer is dead since the powers phase
+    if (more) assemble(sl + 1);
+    // P (running product) into bo(pc) as the B operand of the product GEMM
+    {
+      double pr[NE], pi[NE];
+      tmem_load_block<NE>(tm(0), pr, pi);
+      write_B(bo(pc), pr, pi, 1.0);
+    }
+    gsync();  // U and the next 2X published; P staged
+    first_frags(gu);
+    // ---- V <- U V  (prefetches the next slice's first 2X fragments)
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      accR[e] = 0.0;
+      accI[e] = 0.0;
+    }
+    step(gu, more ? gx : nullptr, bo(pc), accR, accI);
+    tmem_store_block<NE>(tm(0), accR, accI);
+    if (prefix_out) {
+      double2* o = prefix_out + (size_t)sl * D * D;
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(accR[e], accI[e]);
+    }
+    __syncthreads();  // product GEMM done reading bo(pc)
+    if (more) {
+      fill_t1();
+      __syncthreads();
+    }
+  }
+  if (active) {
+    double pr[NE], pi[NE];
+    tmem_load_block<NE>(tm(0), pr, pi);
+    double2* o = lane_out + (size_t)lane * D * D;
+#pragma unroll
+    for (int e = 0; e < NE; ++e)
+      o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(pr[e], pi[e]);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc(tmem_base, C::TMEM_COLS);
+}
+
+}  // namespace sp
