@@ -7,8 +7,8 @@ import paper_2108_07126_b200 as sp
 from cases import random_inputs, qubit_inputs
 
 PEAK = 37.0e12
-def run(label, h0, hs, v, dt, mode="midpoint", reps=3):
-    ctx = sp.create(); ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+def run(label, h0, hs, v, dt, mode="midpoint", reps=3, algo="auto"):
+    ctx = sp.create(); ctx.set_algorithm(algo); ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
                                            quadrature=None if mode == "magnus" else mode)
     ctx.set_profiling(True)
     amps = sp.ControlAmplitudes(v, dt)
@@ -33,3 +33,8 @@ run("d32 rand 1e5", *random_inputs(32, 2, 100000, 1))
 run("d64 rand 2e4", *random_inputs(64, 2, 20000, 1))
 run("d128 rand 4e3", *random_inputs(128, 4, 4000, 1))
 run("d256 rand 500", *random_inputs(256, 4, 500, 1))
+if len(sys.argv) > 1 and sys.argv[1] == "algos":
+    for a in ("ps", "ps3m"):
+        run(f"d32 rand 1e5 {a}", *random_inputs(32, 2, 100000, 1), algo=a)
+        run(f"d64 rand 2e4 {a}", *random_inputs(64, 2, 20000, 1), algo=a)
+        run(f"d128 rand 4e3 {a}", *random_inputs(128, 4, 4000, 1), algo=a)
