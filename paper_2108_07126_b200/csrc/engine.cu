@@ -549,7 +549,7 @@ int reduce_pairwise_dev(sp_ctx* ctx, const double2* in, int cnt, int D, cudaStre
 // Run the lane pass.  Returns the lane products (lane_count of them) on the
 // device, or (small families, pairwise) the per-CTA products.
 int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix_out,
-              cudaStream_t st, const double2** prods, int* count) {
+              cudaStream_t st, const double2** prods, int* count, void* fused_out = nullptr) {
   const int64_t n = job.n_slices;
   const int D = ctx->D;
   const size_t dd = (size_t)D * D;
@@ -565,13 +565,21 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     if (rc) return rc;
     double2* lane_out = (double2*)ctx->lanes.p;
     double2* cta_out = cta_reduce ? lane_out : nullptr;
+    SmallTail tail{nullptr, nullptr, ctx->dim, ctx->bits == 32};
+    if (fused_out) {
+      rc = ensure(ctx, ctx->gctr, sizeof(unsigned));
+      if (rc) return rc;
+      CUDA_TRY(ctx, cudaMemsetAsync(ctx->gctr.p, 0, sizeof(unsigned), st));
+      tail.ctr = (unsigned*)ctx->gctr.p;
+      tail.out = fused_out;
+    }
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
     if (ctx->fam == FAM_S2)
       lane_small_kernel<2, 1><<<blocks, 256, 0, st>>>(job, (const double2*)ctx->terms.p, lanes,
-                                                      lane_out, cta_out, prefix_out);
+                                                      lane_out, cta_out, prefix_out, tail);
     else
       lane_small_kernel<4, 4><<<blocks, 256, 0, st>>>(job, (const double2*)ctx->terms.p, lanes,
-                                                      lane_out, cta_out, prefix_out);
+                                                      lane_out, cta_out, prefix_out, tail);
     CUDA_TRY(ctx, cudaGetLastError());
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
     ++ctx->launches;
@@ -795,11 +803,13 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
     const bool cta_reduce = small && reduction == SP_REDUCE_PAIRWISE;
     const double2* prods = nullptr;
     int cnt = 0;
-    rc = run_lanes(ctx, job, cta_reduce, nullptr, st, &prods, &cnt);
+    // small families + pairwise: one launch does everything (fused tail)
+    rc = run_lanes(ctx, job, cta_reduce, nullptr, st, &prods, &cnt, cta_reduce ? d_out : nullptr);
     if (rc) return rc;
     ctx->ev_pending = ctx->prof;
     ctx->kname = family_kernel_name(ctx->fam, ctx->last_algo);
     ctx->flops = executed_flops(ctx, job.n_slices, job.m);
+    if (cta_reduce) return SP_OK;
     if (reduction == SP_REDUCE_PAIRWISE) {
       rc = reduce_pairwise_dev(ctx, prods, cnt, D, st, &total);
       if (rc) return rc;

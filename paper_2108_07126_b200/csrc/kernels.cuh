@@ -213,12 +213,21 @@ __device__ __forceinline__ void lane_range(int64_t n, int lanes, int lane, int64
 // ---------------------------------------------------------------------------
 // Family S: D in {2, 4}.  TPL threads per lane, CPT = D / TPL columns each.
 // ---------------------------------------------------------------------------
+// optional fused tail (pairwise reduction of the CTA products + output)
+struct SmallTail {
+  unsigned* ctr;  // zeroed before the launch; nullptr = no fused tail
+  void* out;      // d x d result, complex128 or complex64
+  int d;
+  int to_fp32;
+};
+
 template <int D, int TPL>
 __global__ void __launch_bounds__(256) lane_small_kernel(SliceJob job,
                                                          const double2* __restrict__ terms,
                                                          int lanes, double2* __restrict__ lane_out,
-                                                         double2* __restrict__ cta_out,
-                                                         double2* __restrict__ prefix_out) {
+                                                         double2* cta_out,
+                                                         double2* __restrict__ prefix_out,
+                                                         SmallTail tail) {
   constexpr int CPT = D / TPL;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = gtid / TPL;
@@ -358,6 +367,55 @@ __global__ void __launch_bounds__(256) lane_small_kernel(SliceJob job,
   }
   for (int e = threadIdx.x; e < D * D; e += blockDim.x)
     cta_out[(size_t)blockIdx.x * D * D + e] = buf[src][e];
+  if (tail.ctr == nullptr) return;
+
+  // ---- fused tail: the last CTA to finish multiplies the CTA products in
+  // time order (chunks of LPB by the same smem tree, later chunks on the
+  // left) and writes the d x d result — the whole equiprop in one launch
+  __shared__ bool is_last;
+  __shared__ double2 carry[D * D];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = (atomicAdd(tail.ctr, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < D * D; e += blockDim.x)
+    carry[e] = make_double2((e / D) == (e % D) ? 1.0 : 0.0, 0.0);
+  for (int base = 0; base < (int)gridDim.x; base += LPB) {
+    const int here = min(LPB, (int)gridDim.x - base);
+    for (int e = threadIdx.x; e < here * D * D; e += blockDim.x)
+      buf[0][e] = __ldcg(&cta_out[(size_t)base * D * D + e]);
+    __syncthreads();
+    int c2 = here, sr = 0;
+    while (c2 > 1) {
+      const int pairs = c2 >> 1;
+      for (int e = threadIdx.x; e < pairs * D * D; e += blockDim.x) {
+        const int p = e / (D * D), rc = e % (D * D), r = rc / D, c = rc % D;
+        buf[sr ^ 1][p * D * D + rc] =
+            cdot(&buf[sr][(2 * p + 1) * D * D + r * D], &buf[sr][(2 * p) * D * D], D, c, D);
+      }
+      if (c2 & 1)
+        for (int e = threadIdx.x; e < D * D; e += blockDim.x)
+          buf[sr ^ 1][pairs * D * D + e] = buf[sr][(c2 - 1) * D * D + e];
+      __syncthreads();
+      c2 = pairs + (c2 & 1);
+      sr ^= 1;
+    }
+    // carry <- chunk product * carry
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x)
+      buf[sr ^ 1][e] = cdot(&buf[sr][(e / D) * D], carry, D, e % D, D);
+    __syncthreads();
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x) carry[e] = buf[sr ^ 1][e];
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < tail.d * tail.d; e += blockDim.x) {
+    const double2 v = carry[(e / tail.d) * D + (e % tail.d)];
+    if (tail.to_fp32)
+      reinterpret_cast<float2*>(tail.out)[e] = make_float2((float)v.x, (float)v.y);
+    else
+      reinterpret_cast<double2*>(tail.out)[e] = v;
+  }
 }
 
 // ---------------------------------------------------------------------------
