@@ -128,9 +128,9 @@ const char* family_kernel_name(int fam, int algo) {
     switch (fam) {
       case FAM_T16: return "lane_ps3_kernel<D16>";
       case FAM_T32: return "lane_ps3_kernel<D32>";
-      case FAM_T64: return "lane_ps3_kernel<D64,group2>";
-      case FAM_T128: return "lane_ps3_kernel<D128,group4>";
-      case FAM_T256: return "lane_ps3_kernel<D256,group16>";
+      case FAM_T64: return "lane_ps3g_kernel<D64,group2>";
+      case FAM_T128: return "lane_ps3g_kernel<D128,group4>";
+      case FAM_T256: return "lane_ps3g_kernel<D256,group16>";
     }
   }
   if (algo == 2) {
