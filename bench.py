@@ -192,6 +192,14 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def max_over_ranks(dist, vals, dev):
+    import torch
+    on = dev if dist.get_backend() == "nccl" else "cpu"
+    red = torch.tensor(vals, dtype=torch.float64, device=on)
+    dist.all_reduce(red, op=dist.ReduceOp.MAX)
+    return red.tolist()
+
+
 def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
     import torch
 
@@ -254,9 +262,7 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
     total_ms = sum(step_ms)
     kern = statistics.mean(kernel_ms)
     if dist is not None:
-        red = torch.tensor([total_ms, kern], dtype=torch.float64, device=dev)
-        dist.all_reduce(red, op=dist.ReduceOp.MAX)
-        total_ms, kern = red.tolist()
+        total_ms, kern = max_over_ranks(dist, [total_ms, kern], dev)
     value = n * args.steps / (total_ms / 1e3)
     local_slices = b - a
     F = canonical_flops(d, plan.m_max, 1 + wl["n_ctrl"])
@@ -304,9 +310,7 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
             e2e_times.append(t1 - t0)
     e2e_s = sum(e2e_times)
     if dist is not None:
-        red = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(red, op=dist.ReduceOp.MAX)
-        e2e_s = red.item()
+        (e2e_s,) = max_over_ranks(dist, [e2e_s], dev)
     e2e = {"value": n * args.steps / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(local.nbytes), "d2h_bytes_per_step": int(d * d * 16),
            "ms_per_step": e2e_s / args.steps * 1e3}
@@ -350,12 +354,18 @@ def main():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; BENCH_DIST_BACKEND=gloo folds several ranks onto the
+    # visible GPUs (a functional check of the multi-rank path on a 1-GPU box)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local_rank = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     dist = None
     torch.cuda.set_device(local_rank)
     if world > 1:
         import torch.distributed as dist_mod
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist_mod.init_process_group(backend)
         dist = dist_mod
 
     head = measure_gpu(args, WORKLOADS[args.workload], rank, world, local_rank, dist, True)

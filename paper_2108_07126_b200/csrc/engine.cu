@@ -176,7 +176,7 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   int fam = FAM_NONE, D = 0;
   DevBuf terms, amps, lanes, ctab, tree0, tree1, xglob, gctr, result, out, cumP, cumE, cumO,
-      fold_scratch, psA, tpriv, viol, terms3;
+      fold_scratch, psA, tpriv, viol, terms3, tailctr;
   cudaStream_t viol_stream = nullptr;
   int64_t viol_pts = 0;
   int algo = 0;          // Algo
@@ -567,10 +567,13 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     double2* cta_out = cta_reduce ? lane_out : nullptr;
     SmallTail tail{nullptr, nullptr, ctx->dim, ctx->bits == 32};
     if (fused_out) {
-      rc = ensure(ctx, ctx->gctr, sizeof(unsigned));
-      if (rc) return rc;
-      CUDA_TRY(ctx, cudaMemsetAsync(ctx->gctr.p, 0, sizeof(unsigned), st));
-      tail.ctr = (unsigned*)ctx->gctr.p;
+      // arrival counter: zeroed once at allocation, reset by the last CTA
+      if (!ctx->tailctr.p) {
+        rc = ensure(ctx, ctx->tailctr, sizeof(unsigned));
+        if (rc) return rc;
+        CUDA_TRY(ctx, cudaMemsetAsync(ctx->tailctr.p, 0, sizeof(unsigned), st));
+      }
+      tail.ctr = (unsigned*)ctx->tailctr.p;
       tail.out = fused_out;
     }
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
@@ -928,7 +931,7 @@ int sp_free(sp_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->terms, &ctx->amps,  &ctx->lanes, &ctx->ctab, &ctx->tree0,
                       &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
                       &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch,
-                      &ctx->psA,   &ctx->tpriv, &ctx->viol, &ctx->terms3};
+                      &ctx->psA,   &ctx->tpriv, &ctx->viol, &ctx->terms3, &ctx->tailctr};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);

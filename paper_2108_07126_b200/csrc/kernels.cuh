@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(256) lane_small_kernel(SliceJob job,
     else
       reinterpret_cast<double2*>(tail.out)[e] = v;
   }
+  if (threadIdx.x == 0) *tail.ctr = 0;  // ready for the next launch
 }
 
 // ---------------------------------------------------------------------------

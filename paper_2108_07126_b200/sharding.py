@@ -130,7 +130,12 @@ def equiprop_sharded_device(ctx: IntegratorContext, local_amps, dt: float, n_sli
                                 local_amps.shape[1], dt, block.data_ptr(),
                                 stream=st.cuda_stream, reduction=reduction, plan=plan)
     gathered = torch.empty((world, d, d), dtype=torch.complex128, device=local_amps.device)
-    dist.all_gather_into_tensor(gathered, block, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(gathered, block, group=group)
+    else:  # gloo (CPU-side collective; used to exercise several ranks on one GPU)
+        parts = [torch.empty((d, d), dtype=torch.complex128) for _ in range(world)]
+        dist.all_gather(parts, block.cpu(), group=group)
+        gathered.copy_(torch.stack(parts))
     out = torch.empty((d, d), dtype=torch.complex128, device=local_amps.device)
     ctx.product_device_ptr(world, gathered.data_ptr(), out.data_ptr(), stream=st.cuda_stream,
                            reduction=reduction)

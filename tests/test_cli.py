@@ -63,7 +63,7 @@ def test_propagate_matches_library(tmp_path, capsys):
 
 @pytest.mark.gpu
 def test_converge_subcommand(capsys):
-    assert cli.main(["converge", "--steps-list", "10,32,100,316", "--skip-oracle"]) == 0
+    assert cli.main(["converge", "--steps-list", "10,32,100,316,1000", "--skip-oracle"]) == 0
     cap = capsys.readouterr()
     assert cap.out.splitlines()[0] == "pts,error"
     assert "fitted order" in cap.err
