@@ -28,7 +28,9 @@ namespace {
 const char* kVersion = "sliceprop_b200 0.1.0 (sm_100a)";
 thread_local char g_err[512] = "";
 
-enum Family { FAM_NONE = 0, FAM_S2, FAM_S4, FAM_T16, FAM_T32, FAM_T64, FAM_T128, FAM_T256 };
+enum Family {
+  FAM_NONE = 0, FAM_S2, FAM_S4, FAM_T16, FAM_T32, FAM_T64, FAM_T128, FAM_T256, FAM_T512
+};
 
 // tensor-core configurations (see TCCfg): D, WC, MT, NT, WPL, LPC, GPL, X-in-smem
 using Cfg16 = TCCfg<16, 16, 1, 2, 1, 4, 1, true>;
@@ -36,18 +38,23 @@ using Cfg32 = TCCfg<32, 32, 1, 2, 4, 1, 1, true>;
 using Cfg64 = TCCfg<64, 64, 1, 4, 8, 1, 1, true>;
 using Cfg128 = TCCfg<128, 32, 1, 4, 8, 1, 4, false>;
 using Cfg256 = TCCfg<256, 16, 2, 2, 8, 1, 16, false>;
+// d <= 512: 64 CTAs x 8 columns per lane (2 lanes on 148 SMs); each CTA reads
+// the whole A operand per GEMM for 8 columns, so this family is L2-bound
+using Cfg512 = TCCfg<512, 8, 4, 1, 8, 1, 64, false>;
 // Paterson-Stockmeyer configurations (A operands: smem for D <= 32, else L2)
 using PS16 = PSCfg<16, 16, 1, 2, 1, 4, 1, true>;
 using PS32 = PSCfg<32, 32, 1, 2, 4, 1, 1, true>;
 using PS64 = PSCfg<64, 32, 1, 4, 4, 1, 2, false>;
 using PS128 = PSCfg<128, 32, 1, 4, 8, 1, 4, false>;
 using PS256 = PSCfg<256, 16, 2, 2, 8, 1, 16, false>;
+using PS512 = PSCfg<512, 8, 4, 1, 8, 1, 64, false>;
 // ... and with 3-multiplication complex products (3-plane operands)
 using P3_16 = PS3Cfg<16, 16, 1, 2, 1, 4, 1, true>;
 using P3_32 = PS3Cfg<32, 32, 1, 2, 4, 1, 1, true>;
 using P3_64 = PS3Cfg<64, 32, 1, 4, 4, 1, 2, false>;
 using P3_128 = PS3Cfg<128, 32, 1, 4, 8, 1, 4, false>;
 using P3_256 = PS3Cfg<256, 16, 2, 2, 8, 1, 16, false>;
+using P3_512 = PS3Cfg<512, 8, 4, 1, 8, 1, 64, false>;
 
 enum Algo { ALGO_AUTO = 0, ALGO_CLENSHAW = 1, ALGO_PS = 2, ALGO_PS3 = 3 };
 
@@ -119,6 +126,7 @@ int family_for(int d, int* D) {
   if (d <= 64) { *D = 64; return FAM_T64; }
   if (d <= 128) { *D = 128; return FAM_T128; }
   if (d <= 256) { *D = 256; return FAM_T256; }
+  if (d <= 512) { *D = 512; return FAM_T512; }
   *D = 0;
   return FAM_NONE;
 }
@@ -131,6 +139,7 @@ const char* family_kernel_name(int fam, int algo) {
       case FAM_T64: return "lane_ps3g_kernel<D64,group2>";
       case FAM_T128: return "lane_ps3g_kernel<D128,group4>";
       case FAM_T256: return "lane_ps3g_kernel<D256,group16>";
+      case FAM_T512: return "lane_ps3g_kernel<D512,group64>";
     }
   }
   if (algo == 2) {
@@ -140,6 +149,7 @@ const char* family_kernel_name(int fam, int algo) {
       case FAM_T64: return "lane_ps_kernel<D64,group2>";
       case FAM_T128: return "lane_ps_kernel<D128,group4>";
       case FAM_T256: return "lane_ps_kernel<D256,group16>";
+      case FAM_T512: return "lane_ps_kernel<D512,group64>";
     }
   }
   switch (fam) {
@@ -150,6 +160,7 @@ const char* family_kernel_name(int fam, int algo) {
     case FAM_T64: return "lane_tc_kernel<D64>";
     case FAM_T128: return "lane_tc_kernel<D128,group4>";
     case FAM_T256: return "lane_tc_kernel<D256,group16>";
+    case FAM_T512: return "lane_tc_kernel<D512,group64>";
   }
   return "none";
 }
@@ -314,6 +325,7 @@ int upload_terms(sp_ctx* ctx) {
     case FAM_T64: rc = ps3_prepare<P3_64>(ctx); break;
     case FAM_T128: rc = ps3_prepare<P3_128>(ctx); break;
     case FAM_T256: rc = ps3_prepare<P3_256>(ctx); break;
+    case FAM_T512: rc = ps3_prepare<P3_512>(ctx); break;
     default: break;
   }
   if (rc) return rc;
@@ -323,6 +335,7 @@ int upload_terms(sp_ctx* ctx) {
     case FAM_T64: rc = tc_prepare<Cfg64>(ctx); break;
     case FAM_T128: rc = tc_prepare<Cfg128>(ctx); break;
     case FAM_T256: rc = tc_prepare<Cfg256>(ctx); break;
+    case FAM_T512: rc = tc_prepare<Cfg512>(ctx); break;
     default: break;
   }
   if (rc) return rc;
@@ -332,6 +345,7 @@ int upload_terms(sp_ctx* ctx) {
     case FAM_T64: rc = ps_prepare<PS64>(ctx); break;
     case FAM_T128: rc = ps_prepare<PS128>(ctx); break;
     case FAM_T256: rc = ps_prepare<PS256>(ctx); break;
+    case FAM_T512: rc = ps_prepare<PS512>(ctx); break;
     default: break;
   }
   if (rc) return rc;
@@ -613,6 +627,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
       case FAM_T64: lanes = ps3_lanes<P3_64>(ctx, n); break;
       case FAM_T128: lanes = ps3_lanes<P3_128>(ctx, n); break;
       case FAM_T256: lanes = ps3_lanes<P3_256>(ctx, n); break;
+      case FAM_T512: lanes = ps3_lanes<P3_512>(ctx, n); break;
     }
     int rc = ensure(ctx, ctx->lanes, (size_t)lanes * dd * sizeof(double2));
     if (rc) return rc;
@@ -623,6 +638,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
       case FAM_T64: rc = ps3_launch<P3_64>(ctx, pj, lanes, lane_out, prefix_out, st); break;
       case FAM_T128: rc = ps3_launch<P3_128>(ctx, pj, lanes, lane_out, prefix_out, st); break;
       case FAM_T256: rc = ps3_launch<P3_256>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T512: rc = ps3_launch<P3_512>(ctx, pj, lanes, lane_out, prefix_out, st); break;
     }
     if (rc) return rc;
     ctx->last_algo = ALGO_PS3;
@@ -643,6 +659,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
       case FAM_T64: lanes = ps_lanes<PS64>(ctx, n); break;
       case FAM_T128: lanes = ps_lanes<PS128>(ctx, n); break;
       case FAM_T256: lanes = ps_lanes<PS256>(ctx, n); break;
+      case FAM_T512: lanes = ps_lanes<PS512>(ctx, n); break;
     }
     int rc = ensure(ctx, ctx->lanes, (size_t)lanes * dd * sizeof(double2));
     if (rc) return rc;
@@ -653,6 +670,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
       case FAM_T64: rc = ps_launch<PS64>(ctx, pj, lanes, lane_out, prefix_out, st); break;
       case FAM_T128: rc = ps_launch<PS128>(ctx, pj, lanes, lane_out, prefix_out, st); break;
       case FAM_T256: rc = ps_launch<PS256>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T512: rc = ps_launch<PS512>(ctx, pj, lanes, lane_out, prefix_out, st); break;
     }
     if (rc) return rc;
     ctx->last_algo = ALGO_PS;
@@ -669,6 +687,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     case FAM_T64: lanes = tc_lanes<Cfg64>(ctx, n); break;
     case FAM_T128: lanes = tc_lanes<Cfg128>(ctx, n); break;
     case FAM_T256: lanes = tc_lanes<Cfg256>(ctx, n); break;
+    case FAM_T512: lanes = tc_lanes<Cfg512>(ctx, n); break;
   }
   int rc = ensure(ctx, ctx->lanes, (size_t)lanes * dd * sizeof(double2));
   if (rc) return rc;
@@ -679,6 +698,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     case FAM_T64: rc = tc_launch<Cfg64>(ctx, job, lanes, lane_out, prefix_out, st); break;
     case FAM_T128: rc = tc_launch<Cfg128>(ctx, job, lanes, lane_out, prefix_out, st); break;
     case FAM_T256: rc = tc_launch<Cfg256>(ctx, job, lanes, lane_out, prefix_out, st); break;
+    case FAM_T512: rc = tc_launch<Cfg512>(ctx, job, lanes, lane_out, prefix_out, st); break;
   }
   if (rc) return rc;
   *prods = lane_out;
@@ -959,7 +979,7 @@ int sp_set_hamiltonian(sp_ctx* ctx, int dim, int n_ctrl, int n_terms, int mode,
   int D = 0;
   const int fam = family_for(dim, &D);
   if (fam == FAM_NONE)
-    return fail(ctx, SP_E_CONFIG, "dimension %d not supported (max 256)", dim);
+    return fail(ctx, SP_E_CONFIG, "dimension %d not supported (max 512)", dim);
   if (!terms) return fail(ctx, SP_E_SHAPE, "null terms");
   ctx->dim = dim;
   ctx->n_ctrl = n_ctrl;

@@ -291,8 +291,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         __syncthreads();
       }
     }
-    // 2y = 2 T_s: stage in the free buffer bo(pb^1) (T_{s-2}, already in TMEM)
-    __syncthreads();
+    // 2y = 2 T_s: stage in the free buffer bo(pb^1) (T_{s-2}, already in
+    // TMEM; nobody reads it in the last power step)
     publish(gy, bo(pb ^ 1), accR, accI, 2.0, 0.0);
     gsync();  // 2y published (and everybody is done reading 2X)
     first_frags(gy);
@@ -317,7 +317,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
       step(gy, j >= 1 ? gy : nullptr, bo(pc), accR, accI);
       if (j >= 1) {
-        __syncthreads();  // everybody has read b_{j+2} and b_{j+1}
+        // b_j overwrites b_{j+2} at own positions only (read above by the
+        // owner); every warp finished reading bo(pc^1) as the previous
+        // step's B operand before the barrier that ended that step
         write_B(bo(pc ^ 1), accR, accI, (j == 1) ? 0.5 : 1.0);
         pc ^= 1;
         __syncthreads();

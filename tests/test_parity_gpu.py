@@ -122,3 +122,25 @@ def test_both_series_schemes_match_reference(case, algo, golden):
             assert rel_fro(cum.u_all[k], golden[f"{key}__u_all"][k]) <= tol
         assert np.array_equal(cum.final, ctx.equiprop(amps, reduction="sequential").u)
     ctx.close()
+
+
+@pytest.mark.parametrize("d,n_ctrl,pts,mode", [(200, 2, 6, "midpoint"), (300, 3, 5, "simpson"),
+                                               (512, 2, 4, "midpoint"), (384, 2, 5, "magnus")])
+@pytest.mark.parametrize("algo", ["auto", "clenshaw", "ps"])
+def test_large_dims_against_oracle(d, n_ctrl, pts, mode, algo):
+    """d > 128 (families D256/D512) against the CPU oracle (bit-exact
+    restatement of the reference) on the same inputs."""
+    import oracle
+    from cases import random_inputs
+    h0, hs, values, dt = random_inputs(d, n_ctrl, pts, 4242 + d)
+    ref, n, _ = oracle.equiprop(h0, hs, values, dt, mode=mode)
+    ref_seq, _, _ = oracle.equiprop(h0, hs, values, dt, mode=mode, reduction="sequential")
+    tol, _ = parity_tolerance(ref, ref_seq, "fp64")
+    ctx = sp.create()
+    ctx.set_algorithm(algo)
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                        quadrature=None if mode == "magnus" else mode)
+    res = ctx.equiprop(sp.ControlAmplitudes(values, dt))
+    assert res.slice_count == n
+    assert rel_fro(res.u, ref) <= tol
+    ctx.close()
