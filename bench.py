@@ -238,6 +238,29 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
+    t = ctx.last_timing()
+    launches_per_step = t["launches"]
+    # launch-latency-bound secondary workloads (C1: ~10 us of GPU work per
+    # step) replay the step as a CUDA graph, the way a serving loop would;
+    # the headline step (seconds of GPU work) is launched directly
+    graph = None
+    if world == 1 and not headline and not args.no_graph:
+        try:
+            ctx.set_profiling(False)
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(stream)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cap):
+                ctx.equiprop_device_ptr(d_amps.data_ptr(), hi - lo, wl["n_ctrl"], dt,
+                                        out.data_ptr(), stream=cap.cuda_stream, plan=plan)
+            for _ in range(args.warmup):
+                graph.replay()
+            torch.cuda.synchronize(dev)
+        except Exception as exc:  # capture not possible: time direct launches
+            print(f"[bench] CUDA graph capture failed ({exc}); direct launches",
+                  file=sys.stderr)
+            graph = None
+            ctx.set_profiling(True)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -248,13 +271,22 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
         for k in range(args.steps):
             flush.fill_(float(k))
             evs[k][0].record(stream)
-            step()
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
             evs[k][1].record(stream)
-            t = ctx.last_timing()
-            kernel_ms.append(t["main_kernel_ms"])
-            launches += t["launches"]
+            if graph is not None:
+                stream.synchronize()
+                launches += launches_per_step
+            else:
+                t = ctx.last_timing()
+                kernel_ms.append(t["main_kernel_ms"])
+                launches += t["launches"]
             validate()
         torch.cuda.synchronize(dev)
+    if graph is not None:  # kernel time bounded by the replayed step
+        kernel_ms = [s.elapsed_time(e) for s, e in evs]
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -321,7 +353,8 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
                                        "n_ctrl": wl["n_ctrl"], "slices": n,
                                        "mode": "midpoint", "m": plan.m_max,
                                        "l2": "flushed between timed steps (256 MiB write)",
-                                       "parallelism": f"time-sharded x{world}"}}
+                                       "parallelism": f"time-sharded x{world}",
+                                       "cuda_graph": graph is not None}}
     res["cpu_sample"] = None
     if headline and rank == 0 and world == 1 and not args.no_cpu:
         rate, ns, sec, threads = cpu_sample_rate(system, values, dt, target_s=args.cpu_seconds)
@@ -344,6 +377,8 @@ def main():
                     help="extra workloads reported under per_dim ('' for none)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the secondary workloads directly instead of as CUDA graphs")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -374,7 +409,9 @@ def main():
         r = measure_gpu(args, WORKLOADS[name], rank, world, local_rank, dist, False)
         per_dim[name] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
                          "e2e": r["e2e"], "roofline_frac": r["roofline"]["frac"],
-                         "kernel": r["roofline"]["kernel"], "workload": r["config"]["workload"]}
+                         "executed_frac": r["roofline"]["executed_frac"],
+                         "kernel": r["roofline"]["kernel"], "workload": r["config"]["workload"],
+                         "cuda_graph": r["config"]["cuda_graph"]}
     if rank == 0:
         line = {
             "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world,

@@ -38,3 +38,6 @@ if len(sys.argv) > 1 and sys.argv[1] == "algos":
         run(f"d32 rand 1e5 {a}", *random_inputs(32, 2, 100000, 1), algo=a)
         run(f"d64 rand 2e4 {a}", *random_inputs(64, 2, 20000, 1), algo=a)
         run(f"d128 rand 4e3 {a}", *random_inputs(128, 4, 4000, 1), algo=a)
+if len(sys.argv) > 1 and sys.argv[1] == "big":
+    run("d512 rand 64", *random_inputs(512, 4, 64, 1), reps=2)
+    run("d384 rand 64", *random_inputs(384, 4, 64, 1), reps=2)
