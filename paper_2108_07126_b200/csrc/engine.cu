@@ -20,6 +20,7 @@
 #include "kernels_ps.cuh"
 #include "kernels_ps3.cuh"
 #include "kernels_ps3g.cuh"
+#include "kernels_apply.cuh"
 
 using namespace sp;
 
@@ -52,6 +53,9 @@ using PS512 = PSCfg<512, 8, 4, 1, 8, 1, 64, false>;
 using P3_16 = PS3Cfg<16, 16, 1, 2, 1, 4, 1, true>;
 using P3_32 = PS3Cfg<32, 32, 1, 2, 4, 1, 1, true>;
 using P3_64 = PS3Cfg<64, 32, 1, 4, 4, 1, 2, false>;
+// D=128: 4 CTAs x 32 columns per lane, 8 warps, 1 CTA per SM.  (Measured:
+// 8 CTAs x 16 columns with 2 CTAs/SM is 1.4x slower — twice the L2 operand
+// traffic and an 8-way group barrier outweigh the barrier overlap.)
 using P3_128 = PS3Cfg<128, 32, 1, 4, 8, 1, 4, false>;
 using P3_256 = PS3Cfg<256, 16, 2, 2, 8, 1, 16, false>;
 using P3_512 = PS3Cfg<512, 8, 4, 1, 8, 1, 64, false>;
@@ -187,7 +191,7 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   int fam = FAM_NONE, D = 0;
   DevBuf terms, amps, lanes, ctab, tree0, tree1, xglob, gctr, result, out, cumP, cumE, cumO,
-      fold_scratch, psA, tpriv, viol, terms3, tailctr;
+      fold_scratch, psA, tpriv, viol, terms3, tailctr, seqA;
   cudaStream_t viol_stream = nullptr;
   int64_t viol_pts = 0;
   int algo = 0;          // Algo
@@ -487,6 +491,43 @@ template <class C>
 int ps3_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double2* prefix_out,
                cudaStream_t st) {
   return ps_launch<C, true>(ctx, pj, lanes, lane_out, prefix_out, st);
+}
+
+// ---- tensor-core prefix application (equiprop_all / sequential total)
+using AP16 = TCCfg<16, 16, 1, 2, 1, 1, 1, false>;
+using AP32 = TCCfg<32, 32, 1, 2, 4, 1, 1, false>;
+using AP64 = TCCfg<64, 64, 1, 4, 8, 1, 1, false>;
+using AP128 = TCCfg<128, 32, 1, 4, 8, 1, 4, false>;
+using AP256 = TCCfg<256, 16, 2, 2, 8, 1, 16, false>;
+using AP512 = TCCfg<512, 8, 4, 1, 8, 1, 64, false>;
+
+template <class C>
+int ap_launch(sp_ctx* ctx, const double* P, const double2* E, int64_t n, int lanes, void* out,
+              cudaStream_t st) {
+  const size_t smem = (size_t)C::BDBL * sizeof(double);
+  CUDA_TRY(ctx, cudaFuncSetAttribute(apply_prefix_tc_kernel<C>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t target = std::max<int64_t>(1, (int64_t)ctx->sms * 4 / C::GPL);
+  const int64_t spb = std::max<int64_t>(1, (n + target - 1) / target);
+  const int64_t chunks = (n + spb - 1) / spb;
+  apply_prefix_tc_kernel<C><<<dim3((unsigned)chunks, C::GPL), C::THREADS, smem, st>>>(
+      P, E, n, lanes, spb, ctx->dim, ctx->bits == 32, out);
+  CUDA_TRY(ctx, cudaGetLastError());
+  ++ctx->launches;
+  return SP_OK;
+}
+
+int tc_apply(sp_ctx* ctx, const double* P, const double2* E, int64_t n, int lanes, void* out,
+             cudaStream_t st) {
+  switch (ctx->fam) {
+    case FAM_T16: return ap_launch<AP16>(ctx, P, E, n, lanes, out, st);
+    case FAM_T32: return ap_launch<AP32>(ctx, P, E, n, lanes, out, st);
+    case FAM_T64: return ap_launch<AP64>(ctx, P, E, n, lanes, out, st);
+    case FAM_T128: return ap_launch<AP128>(ctx, P, E, n, lanes, out, st);
+    case FAM_T256: return ap_launch<AP256>(ctx, P, E, n, lanes, out, st);
+    case FAM_T512: return ap_launch<AP512>(ctx, P, E, n, lanes, out, st);
+  }
+  return fail(ctx, SP_E_INTERNAL, "no tensor-core apply for this family");
 }
 
 template <int D>
@@ -833,6 +874,25 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
     ctx->kname = family_kernel_name(ctx->fam, ctx->last_algo);
     ctx->flops = executed_flops(ctx, job.n_slices, job.m);
     if (cta_reduce) return SP_OK;
+    if (reduction == SP_REDUCE_SEQUENTIAL && !small) {
+      // left fold to E_{L-1} = P_{L-2} ... P_0, then P_{L-1} E_{L-1} with the
+      // same tensor-core routine equiprop_all uses for its last entry
+      rc = ensure(ctx, ctx->cumE, (size_t)cnt * dd * sizeof(double2));
+      if (rc) return rc;
+      rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
+      if (rc) return rc;
+      rc = ensure(ctx, ctx->seqA, dd * sizeof(double2));
+      if (rc) return rc;
+      fold_kernel<<<1, 1024, 0, st>>>(prods, cnt, D, (double2*)ctx->fold_scratch.p,
+                                       (double2*)ctx->cumE.p, (double2*)ctx->result.p);
+      CUDA_TRY(ctx, cudaGetLastError());
+      to_afrag_kernel<<<grid_for((int64_t)dd, 256), 256, 0, st>>>(
+          prods + (size_t)(cnt - 1) * dd, D, (double*)ctx->seqA.p);
+      CUDA_TRY(ctx, cudaGetLastError());
+      ctx->launches += 2;
+      return tc_apply(ctx, (const double*)ctx->seqA.p,
+                      (const double2*)ctx->cumE.p + (size_t)(cnt - 1) * dd, 1, 1, d_out, st);
+    }
     if (reduction == SP_REDUCE_PAIRWISE) {
       rc = reduce_pairwise_dev(ctx, prods, cnt, D, st, &total);
       if (rc) return rc;
@@ -951,7 +1011,8 @@ int sp_free(sp_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->terms, &ctx->amps,  &ctx->lanes, &ctx->ctab, &ctx->tree0,
                       &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
                       &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch,
-                      &ctx->psA,   &ctx->tpriv, &ctx->viol, &ctx->terms3, &ctx->tailctr};
+                      &ctx->psA,   &ctx->tpriv, &ctx->viol, &ctx->terms3, &ctx->tailctr,
+                      &ctx->seqA};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1081,19 +1142,27 @@ int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, do
   fold_kernel<<<1, 1024, 0, st>>>(prods, cnt, D, (double2*)ctx->fold_scratch.p,
                                    (double2*)ctx->cumE.p, (double2*)ctx->result.p);
   CUDA_TRY(ctx, cudaGetLastError());
-  rc = ensure(ctx, ctx->cumO, (size_t)n * dd * sizeof(double2));
-  if (rc) return rc;
-  apply_prefix_kernel<<<grid_for((int64_t)n * dd, 256), 256, 0, st>>>(
-      (const double2*)ctx->cumP.p, (const double2*)ctx->cumE.p, n, cnt, D,
-      (double2*)ctx->cumO.p);
-  CUDA_TRY(ctx, cudaGetLastError());
   const size_t obytes = (size_t)n * d * d * (ctx->bits == 32 ? 8 : 16);
   rc = ensure(ctx, ctx->out, obytes);
   if (rc) return rc;
-  extract_kernel<<<grid_for((int64_t)n * d * d, 256), 256, 0, st>>>(
-      (const double2*)ctx->cumO.p, n, D, d, ctx->bits == 32, ctx->out.p);
-  CUDA_TRY(ctx, cudaGetLastError());
-  ctx->launches += 3;
+  ctx->launches += 1;
+  if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
+    rc = ensure(ctx, ctx->cumO, (size_t)n * dd * sizeof(double2));
+    if (rc) return rc;
+    apply_prefix_kernel<<<grid_for((int64_t)n * dd, 256), 256, 0, st>>>(
+        (const double2*)ctx->cumP.p, (const double2*)ctx->cumE.p, n, cnt, D,
+        (double2*)ctx->cumO.p);
+    CUDA_TRY(ctx, cudaGetLastError());
+    extract_kernel<<<grid_for((int64_t)n * d * d, 256), 256, 0, st>>>(
+        (const double2*)ctx->cumO.p, n, D, d, ctx->bits == 32, ctx->out.p);
+    CUDA_TRY(ctx, cudaGetLastError());
+    ctx->launches += 2;
+  } else {
+    // tensor-core prefix application straight into the output dtype
+    rc = tc_apply(ctx, (const double*)ctx->cumP.p, (const double2*)ctx->cumE.p, n, cnt,
+                  ctx->out.p, st);
+    if (rc) return rc;
+  }
   CUDA_TRY(ctx, cudaMemcpyAsync(u_all_out, ctx->out.p, obytes, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   return read_violation(ctx, amps, nullptr);

@@ -452,6 +452,16 @@ __host__ __device__ constexpr int xfrag_index(int D, int r, int c, int plane) {
          ((r >> 3) & 1);
 }
 
+// cumulative mode: per-slice in-lane prefixes are stored in the A-native
+// 2-plane layout (2 D^2 doubles per slice) so that the prefix application
+// (apply_prefix_tc_kernel) reads them as tensor-core A operands
+__device__ __forceinline__ void store_prefix(double2* base, int D, int64_t slice, int r, int c,
+                                             double re, double im) {
+  double* o = reinterpret_cast<double*>(base) + (size_t)slice * 2 * D * D;
+  o[xfrag_index(D, r, c, 0)] = re;
+  o[xfrag_index(D, r, c, 1)] = im;
+}
+
 template <class C>
 __device__ __forceinline__ int bfrag_index(int r, int n, int plane) {
   return (((r >> 2) * C::NTC + (n >> 3)) * 2 + plane) * 32 + ((n & 7) << 2) + (r & 3);

@@ -267,10 +267,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       Pi[e] = accI[e];
     }
     if (prefix_out) {
-      double2* o = prefix_out + (size_t)sl * D * D;
 #pragma unroll
       for (int e = 0; e < NE; ++e)
-        o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(Pr[e], Pi[e]);
+        store_prefix(prefix_out, D, sl, row_of(e), col0 + col_of(e), Pr[e], Pi[e]);
     }
     // smem A buffers (XS) and B buffers are rewritten by the next slice
     lane_sync<C>();

@@ -348,10 +348,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     step(gu, more ? gx : nullptr, bo(pc), accR, accI);
     tmem_store_block<NE>(tm(0), accR, accI);
     if (prefix_out) {
-      double2* o = prefix_out + (size_t)sl * D * D;
 #pragma unroll
       for (int e = 0; e < NE; ++e)
-        o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(accR[e], accI[e]);
+        store_prefix(prefix_out, D, sl, row_of(e), col0 + col_of(e), accR[e], accI[e]);
     }
     __syncthreads();  // product GEMM done reading bo(pc)
     if (more) {

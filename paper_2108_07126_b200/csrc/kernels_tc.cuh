@@ -211,10 +211,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
     }
     if (prefix_out) {
-      double2* o = prefix_out + (size_t)s * D * D;
 #pragma unroll
       for (int e = 0; e < NE; ++e)
-        o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(Vr[e], Vi[e]);
+        store_prefix(prefix_out, D, s, row_of(e), col0 + col_of(e), Vr[e], Vi[e]);
     }
     // X (smem) and the weights are rewritten by the next slice
     if constexpr (C::GPL == 1) lane_sync<C>();
