@@ -41,3 +41,17 @@ if len(sys.argv) > 1 and sys.argv[1] == "algos":
 if len(sys.argv) > 1 and sys.argv[1] == "big":
     run("d512 rand 64", *random_inputs(512, 4, 64, 1), reps=2)
     run("d384 rand 64", *random_inputs(384, 4, 64, 1), reps=2)
+if len(sys.argv) > 1 and sys.argv[1] == "cum":
+    for d, n_ctrl, n in ((2, 2, 1000000), (4, 2, 200000), (16, 2, 100000), (32, 2, 50000),
+                         (64, 2, 10000), (128, 4, 2000)):
+        h0, hs, v, dt = random_inputs(d, n_ctrl, n, 1)
+        ctx = sp.create(); ctx.set_hamiltonian(sp.ControlSystem(h0, hs)); ctx.set_profiling(True)
+        amps = sp.ControlAmplitudes(v, dt)
+        ctx.equiprop_all(amps)
+        t0 = time.perf_counter(); cum = ctx.equiprop_all(amps); wall = time.perf_counter() - t0
+        lane_ms = ctx.last_timing()["main_kernel_ms"]
+        seq = ctx.equiprop(amps, reduction="sequential").u
+        out_gb = cum.u_all.nbytes / 1e9
+        print(f"cum d{d} n={n}: wall {wall*1e3:.2f} ms (lane kernel {lane_ms:.2f} ms), output "
+              f"{out_gb:.3f} GB, final==seq {np.array_equal(cum.final, seq)}", flush=True)
+        ctx.close()
