@@ -438,7 +438,7 @@ template <class C, bool M3 = false>
 int ps_lanes(sp_ctx* ctx, int64_t n) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ps_kernel<C, M3>(), C::THREADS, C::SMEM);
-  occ = std::min(occ, 512 / C::TMEM_COLS);  // TMEM columns per SM
+  if constexpr (M3) occ = std::min(occ, 512 / C::TMEM_COLS);  // TMEM columns per SM
   if (occ < 1) occ = 1;
   int64_t ctas = (int64_t)ctx->sms * occ;
   int64_t units = (C::GPL > 1) ? ctas / C::GPL : ctas * C::LPC;

@@ -33,16 +33,6 @@ struct PSCfg : TCCfg<D_, WC_, MT_, NT_, WPL_, LPC_, GPL_, XS_> {
   using B = TCCfg<D_, WC_, MT_, NT_, WPL_, LPC_, GPL_, XS_>;
   static constexpr int LANE_DBL = 2 * B::BDBL + (XS_ ? 2 * B::XDBL : 0) + B::WMAX;
   static constexpr size_t SMEM = (size_t)LANE_DBL * LPC_ * sizeof(double);
-  // TMEM: per thread 4 blocks (P, T_1..T_3) of 4*NE 32-bit columns
-  static constexpr int NE = MT_ * NT_ * 4;
-  static constexpr int TMEM_NEED = 16 * NE * ((WPL_ * LPC_ + 3) / 4);
-  static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64
-                                   : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
-  static_assert(TMEM_NEED <= 512, "TMEM budget");
-  // smem-resident configurations: ask the register allocator for the CTA
-  // residency the shared memory allows (at most 3 per SM)
-  static constexpr int SMEM_FIT = (int)((227 * 1024) / SMEM);
-  static constexpr int MINB = XS_ ? (SMEM_FIT >= 3 ? 3 : (SMEM_FIT >= 2 ? 2 : 1)) : 1;
 };
 
 struct PSJob {
@@ -52,7 +42,7 @@ struct PSJob {
 };
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS, C::MINB)
+__global__ void __launch_bounds__(C::THREADS, 1)
     lane_ps_kernel(PSJob pj, const double* __restrict__ terms, int lanes,
                    double* __restrict__ gA, unsigned* __restrict__ gctr,
                    double2* __restrict__ tpriv, double2* __restrict__ lane_out,
@@ -88,30 +78,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   const int nt0 = (wil / (C::S / MT)) * NT;
   const int col0 = cb * WC;
   const int s = pj.s, r = pj.r;
+  // private column blocks of T_1..T_{s-1}, acc-native, coalesced per thread
+  auto tp = [&](int kk, int e) -> double2& {
+    return tpriv[(((size_t)blockIdx.x * (s - 1) + kk) * NE + e) * C::THREADS + threadIdx.x];
+  };
   auto row_of = [&](int idx) { return 16 * (ms0 + idx / (NT * 4)) + g + 8 * ((idx & 3) >> 1); };
   auto col_of = [&](int idx) { return 8 * (nt0 + (idx / 4) % NT) + 2 * t4 + (idx & 1); };
 
-  // TMEM: running product P (block 0) and the powers T_1..T_{s-1} (blocks
-  // 1..s-1, s <= 4) live in tensor memory between uses
-  __shared__ uint32_t tmem_slot;
-  if (warp == 0) tmem_alloc(&tmem_slot, C::TMEM_COLS);
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t tmem_base = tmem_slot;
-  const uint32_t tmem_me =
-      tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 16 * NE);
-  auto tm = [&](int blk) { return tmem_me + (uint32_t)(blk * 4 * NE); };
-  {
-    double pr[NE], pi[NE];
+  double Pr[NE], Pi[NE];
 #pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      pr[e] = (row_of(e) == col0 + col_of(e)) ? 1.0 : 0.0;
-      pi[e] = 0.0;
-    }
-    tmem_store_block<NE>(tm(0), pr, pi);
+  for (int e = 0; e < NE; ++e) {
+    Pr[e] = (row_of(e) == col0 + col_of(e)) ? 1.0 : 0.0;
+    Pi[e] = 0.0;
   }
-  (void)tpriv;
   int64_t s0 = 0, s1 = 0;
   if (active) lane_range(job.n_slices, lanes, lane, s0, s1);
   const int T = job.n_terms;
@@ -159,12 +138,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     }
     for (int i = 1; i < s; ++i) {
       const double ar = pj.alpha[2 * (j * s + i)], ai = pj.alpha[2 * (j * s + i) + 1];
-      double tr[NE], ti[NE];
-      tmem_load_block<NE>(tm(i), tr, ti);
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
-        qr[e] = fma(ar, tr[e], fma(-ai, ti[e], qr[e]));
-        qi[e] = fma(ar, ti[e], fma(ai, tr[e], qi[e]));
+        const double2 tv = __ldcg(&tp(i - 1, e));
+        qr[e] = fma(ar, tv.x, fma(-ai, tv.y, qr[e]));
+        qi[e] = fma(ar, tv.y, fma(ai, tv.x, qi[e]));
       }
     }
   };
@@ -207,8 +185,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         const int i0 = xfrag_index(D, rr, c, 0), i1 = xfrag_index(D, rr, c, 1);
         t1r[e] = 0.5 * (AG ? __ldcg(gx + i0) : smem[ax_off + i0]);
         t1i[e] = 0.5 * (AG ? __ldcg(gx + i1) : smem[ax_off + i1]);
+        tp(0, e) = make_double2(t1r[e], t1i[e]);
       }
-      tmem_store_block<NE>(tm(1), t1r, t1i);
       write_B(bofs0, t1r, t1i, 1.0);
     }
     lane_sync<C>();
@@ -222,17 +200,18 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
           accI[e] = 0.0;
         }
       } else {
-        tmem_load_block<NE>(tm(k - 2), accR, accI);
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
-          accR[e] = -accR[e];
-          accI[e] = -accI[e];
+          const double2 tv = __ldcg(&tp(k - 3, e));
+          accR[e] = -tv.x;
+          accI[e] = -tv.y;
         }
       }
       tile_mma<C, AG>(gx, ax_off, bo(pb), accR, accI, ms0, nt0, ln);
       if (k < s) {
         write_B(bo(pb ^ 1), accR, accI, 1.0);
-        tmem_store_block<NE>(tm(k), accR, accI);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) tp(k - 1, e) = make_double2(accR[e], accI[e]);
         pb ^= 1;
         lane_sync<C>();
       } else {
@@ -273,9 +252,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     write_A(gu, ax_off, accR, accI, phase_one ? 1.0 : job.phase[0],
             phase_one ? 0.0 : job.phase[1]);
     sync_all();
-    // ---- 5. V <- U V   (P lives in TMEM between slices)
-    tmem_load_block<NE>(tm(0), accR, accI);
-    write_B(bofs0, accR, accI, 1.0);
+    // ---- 5. V <- U V
+    write_B(bofs0, Pr, Pi, 1.0);
     lane_sync<C>();
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
@@ -283,27 +261,25 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       accI[e] = 0.0;
     }
     tile_mma<C, AG>(gu, ax_off, bofs0, accR, accI, ms0, nt0, ln);
-    tmem_store_block<NE>(tm(0), accR, accI);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      Pr[e] = accR[e];
+      Pi[e] = accI[e];
+    }
     if (prefix_out) {
 #pragma unroll
       for (int e = 0; e < NE; ++e)
-        store_prefix(prefix_out, D, sl, row_of(e), col0 + col_of(e), accR[e], accI[e]);
+        store_prefix(prefix_out, D, sl, row_of(e), col0 + col_of(e), Pr[e], Pi[e]);
     }
     // smem A buffers (XS) and B buffers are rewritten by the next slice
     lane_sync<C>();
   }
   if (active) {
-    double pr[NE], pi[NE];
-    tmem_load_block<NE>(tm(0), pr, pi);
     double2* o = lane_out + (size_t)lane * D * D;
 #pragma unroll
     for (int e = 0; e < NE; ++e)
-      o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(pr[e], pi[e]);
+      o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(Pr[e], Pi[e]);
   }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  if (warp == 0) tmem_dealloc(tmem_base, C::TMEM_COLS);
 }
 
 }  // namespace sp
