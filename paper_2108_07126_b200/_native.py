@@ -15,7 +15,9 @@ from .errors import raise_for
 
 __all__ = ["lib", "SpPlan", "LIB_PATH", "HEADER_SYMBOLS", "check", "MODE", "REDUCTION"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsliceprop_b200.so")
+# SLICEPROP_B200_LIB selects an instrumented build of the same sources (tools/)
+LIB_PATH = os.environ.get("SLICEPROP_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libsliceprop_b200.so")
 
 MODE = {"midpoint": 0, "simpson": 1, "magnus": 2}
 REDUCTION = {"pairwise": 0, "sequential": 1}

@@ -42,30 +42,32 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(OUT):
+def up_to_date(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return False
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     return all(os.path.getmtime(p) <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *SOURCES, "-o", OUT + ".tmp"]
+def build(force: bool = False, verbose: bool = False, out: str = OUT,
+          defines: tuple = ()) -> str:
+    """Build the library (``out``/``defines``: instrumented variants for tools/)."""
+    if not force and up_to_date(out):
+        return out
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+           "-I", CSRC, *SOURCES, "-o", out + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
-    with open(os.path.join(HERE, "build.log"), "w") as fh:
+    with open(os.path.join(HERE, "build.log" if out == OUT else "build_variant.log"), "w") as fh:
         fh.write(" ".join(cmd) + "\n" + log)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{log[-4000:]}")
     if any(int(n) > 0 for n in re.findall(r"(\d+) bytes spill stores", log)):
         print("warning: register spills in the sm_100a build (see build.log)", file=sys.stderr)
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(out + ".tmp", out)
     if verbose:
         print(log)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -460,7 +460,9 @@ int ps_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double
                   (size_t)grid * (pj.s - 1) * NE * C::THREADS * sizeof(double2));
   if (rc) return rc;
   double2* tpriv = (double2*)ctx->tpriv.p;
-  const double* terms = (const double*)(M3 ? ctx->terms3.p : ctx->terms.p);
+  // the group PS3 kernel assembles from the 2-plane terms (and forms the sum
+  // plane itself); the single-CTA PS3 kernel reads the 3-plane copy
+  const double* terms = (const double*)((M3 && C::GPL == 1) ? ctx->terms3.p : ctx->terms.p);
   double* ga = nullptr;
   unsigned* ctr = nullptr;
   if (C::GPL > 1) {
@@ -965,6 +967,17 @@ int product_dev(sp_ctx* ctx, int count, const double2* d_mats, int reduction, vo
 extern "C" {
 
 const char* sp_version(void) { return kVersion; }
+
+#ifdef SP_PHASE_PROF
+// profiling builds only (tools/phase_prof.py): read and clear the per-phase
+// clock totals of lane_ps3g_kernel
+int sp_phase_prof(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, sp::g_phase, 16 * sizeof(unsigned long long)) != cudaSuccess)
+    return 1;
+  unsigned long long z[16] = {0};
+  return cudaMemcpyToSymbol(sp::g_phase, z, sizeof(z)) != cudaSuccess;
+}
+#endif
 
 int sp_bessel_j(int k, double x, double* out) {
   if (!out) return fail(nullptr, SP_E_CONFIG, "null output");

@@ -23,6 +23,18 @@
 
 namespace sp {
 
+#ifdef SP_PHASE_PROF
+// per-phase SM clock totals of thread 0 of every CTA (tools/phase_prof.py)
+__device__ unsigned long long g_phase[16];
+#define PH_INIT long long ph_t = clock64(); unsigned long long ph_acc[10] = {0};
+#define PH(k) do { const long long t_ = clock64(); ph_acc[k] += t_ - ph_t; ph_t = t_; } while (0)
+#define PH_DONE if (threadIdx.x == 0) for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]);
+#else
+#define PH_INIT
+#define PH(k) do {} while (0)
+#define PH_DONE
+#endif
+
 // tile_mma3 with cross-step prefetch: a holds the kb = 0 fragments on entry;
 // on exit it holds the kb = 0 fragments of An (if An != nullptr)
 template <class C>
@@ -150,32 +162,84 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   unsigned bar = 0;
   auto gsync = [&]() { group_barrier(gctr + group, (++bar) * C::GPL); };
 
-  // weights of slice sl, then this CTA's column chunk of 2X (A layout, L2)
-  auto assemble = [&](int64_t sl) {
+  // weights of slice sl, then this CTA's column chunk of 2X (3-plane A
+  // layout, L2) from the 2-plane terms, and T_1 = X[:, J] (B layout) into
+  // smem at t1_off.  One unit = one lane's pair of A-fragment elements (rows
+  // 16 strip + l/4 and +8, column 4 kbl + l%4); two terms of QB units are in
+  // flight per thread (the loop is L2-latency bound otherwise).
+  constexpr int UNITS = C::S * KBC * 32;
+  constexpr int UPT = UNITS / C::THREADS;
+  constexpr int QB = UPT < 4 ? UPT : (C::MT >= 4 ? 2 : 4);  // (D512: register budget)
+  static_assert(UNITS % C::THREADS == 0 && UPT % QB == 0, "assembly tiling");
+  constexpr size_t TD = (size_t)2 * D * D;  // doubles per 2-plane term
+  auto assemble = [&](int64_t sl, int t1_off) {
     for (int tt = threadIdx.x; tt < T; tt += C::THREADS)
       smem[w_off + tt] = (tt == 0) ? job.xs : job.xs * slice_weight(job, sl, tt);
     __syncthreads();
-    for (int q = 2 * threadIdx.x; q < CHUNK; q += 2 * C::THREADS) {
-      const int i = chunk_index(q);
-      double2 h = __ldg(reinterpret_cast<const double2*>(terms + i));
-      double x0 = smem[w_off] * h.x, x1 = smem[w_off] * h.y;
-      for (int tt = 1; tt < T; ++tt) {
-        h = __ldg(reinterpret_cast<const double2*>(terms + (size_t)tt * C::XDBL + i));
-        x0 = fma(smem[w_off + tt], h.x, x0);
-        x1 = fma(smem[w_off + tt], h.y, x1);
+#pragma unroll 1
+    for (int b = 0; b < UPT; b += QB) {
+      int blk[QB];
+      double2 xr[QB], xi[QB];
+#pragma unroll
+      for (int u = 0; u < QB; ++u) {
+        const int unit = threadIdx.x + (b + u) * C::THREADS;
+        blk[u] = (unit / (KBC * 32)) * KB + cb * KBC + (unit / 32) % KBC;
       }
-      *reinterpret_cast<double2*>(gx + i) = make_double2(x0, x1);
-    }
-  };
-  // T_1 = X[:, J] (B layout, bo(0)) from this CTA's own published chunk
-  auto fill_t1 = [&]() {
-    for (int q = 2 * threadIdx.x; q < CHUNK; q += 2 * C::THREADS) {
-      const double2 x = __ldcg(reinterpret_cast<const double2*>(gx + chunk_index(q)));
-      const int rem = q % (KBC * 192), p = (rem % 192) / 64, l = (rem % 64) / 2;
-      const int rw = 16 * (q / (KBC * 192)) + (l >> 2);
-      const int n = 4 * (rem / 192) + (l & 3);
-      smem[bofs0 + bfrag3_index<C>(rw, n, p)] = 0.5 * x.x;
-      smem[bofs0 + bfrag3_index<C>(rw + 8, n, p)] = 0.5 * x.y;
+      {
+        const double w = smem[w_off];
+#pragma unroll
+        for (int u = 0; u < QB; ++u) {
+          const double* h = terms + (size_t)blk[u] * 128 + 2 * ln;
+          const double2 hr = __ldg(reinterpret_cast<const double2*>(h));
+          const double2 hi = __ldg(reinterpret_cast<const double2*>(h + 64));
+          xr[u] = make_double2(w * hr.x, w * hr.y);
+          xi[u] = make_double2(w * hi.x, w * hi.y);
+        }
+      }
+#pragma unroll 1
+      for (int tt = 1; tt < T; tt += 2) {
+        const bool two = tt + 1 < T;
+        double2 hr[2][QB], hi[2][QB];
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int u = 0; u < QB; ++u) {
+            if (k == 0 || two) {
+              const double* h = terms + (size_t)(tt + k) * TD + (size_t)blk[u] * 128 + 2 * ln;
+              hr[k][u] = __ldg(reinterpret_cast<const double2*>(h));
+              hi[k][u] = __ldg(reinterpret_cast<const double2*>(h + 64));
+            }
+          }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (k == 1 && !two) break;
+          const double w = smem[w_off + tt + k];
+#pragma unroll
+          for (int u = 0; u < QB; ++u) {
+            xr[u].x = fma(w, hr[k][u].x, xr[u].x);
+            xr[u].y = fma(w, hr[k][u].y, xr[u].y);
+            xi[u].x = fma(w, hi[k][u].x, xi[u].x);
+            xi[u].y = fma(w, hi[k][u].y, xi[u].y);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < QB; ++u) {
+        const int unit = threadIdx.x + (b + u) * C::THREADS;
+        double* o = gx + (size_t)blk[u] * 192 + 2 * ln;
+        *reinterpret_cast<double2*>(o) = xr[u];
+        *reinterpret_cast<double2*>(o + 64) = xi[u];
+        *reinterpret_cast<double2*>(o + 128) =
+            make_double2(xr[u].x + xi[u].x, xr[u].y + xi[u].y);
+        const int rw = 16 * (unit / (KBC * 32)) + (ln >> 2);
+        const int n = 4 * ((unit / 32) % KBC) + (ln & 3);
+        smem[t1_off + bfrag3_index<C>(rw, n, 0)] = 0.5 * xr[u].x;
+        smem[t1_off + bfrag3_index<C>(rw, n, 1)] = 0.5 * xi[u].x;
+        smem[t1_off + bfrag3_index<C>(rw, n, 2)] = 0.5 * (xr[u].x + xi[u].x);
+        smem[t1_off + bfrag3_index<C>(rw + 8, n, 0)] = 0.5 * xr[u].y;
+        smem[t1_off + bfrag3_index<C>(rw + 8, n, 1)] = 0.5 * xi[u].y;
+        smem[t1_off + bfrag3_index<C>(rw + 8, n, 2)] = 0.5 * (xr[u].y + xi[u].y);
+      }
     }
   };
   // stage own elements in chunk order (smem at off), then coalesced copy
@@ -248,12 +312,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
   };
 
+  PH_INIT
+  int tb = 0;  // buffer holding this slice's T_1 (written by assemble)
   if (s0 < s1) {
-    assemble(s0);
+    assemble(s0, bo(tb));
     gsync();
-    fill_t1();
     first_frags(gx);
-    __syncthreads();
   }
   for (int64_t sl = s0; sl < s1; ++sl) {
     const bool more = sl + 1 < s1;
@@ -262,12 +326,13 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int rr = row_of(e), n = col_of(e);
-      accR[e] = smem[bofs0 + bfrag3_index<C>(rr, n, 0)];
-      accI[e] = smem[bofs0 + bfrag3_index<C>(rr, n, 1)];
+      accR[e] = smem[bo(tb) + bfrag3_index<C>(rr, n, 0)];
+      accI[e] = smem[bo(tb) + bfrag3_index<C>(rr, n, 1)];
     }
     tmem_store_block<NE>(tm(1), accR, accI);
+    PH(0);
     // ---- powers T_k = 2X T_{k-1} - T_{k-2}
-    int pb = 0;
+    int pb = tb;
     for (int k = 2; k <= s; ++k) {
       if (k == 2) {
 #pragma unroll
@@ -293,9 +358,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
     // 2y = 2 T_s: stage in the free buffer bo(pb^1) (T_{s-2}, already in
     // TMEM; nobody reads it in the last power step)
+    PH(1);
     publish(gy, bo(pb ^ 1), accR, accI, 2.0, 0.0);
+    PH(2);
     gsync();  // 2y published (and everybody is done reading 2X)
     first_frags(gy);
+    PH(3);
     // ---- Clenshaw in y
     int pc = 0;
     {
@@ -325,12 +393,17 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         __syncthreads();
       }
     }
+    PH(4);
     // U (times the plan phase): stage in bo(pc^1) (b_2, consumed) and publish
     __syncthreads();
     publish(gu, bo(pc ^ 1), accR, accI, phase_one ? 1.0 : job.phase[0],
             phase_one ? 0.0 : job.phase[1]);
-    // next slice's 2X: its buffer is dead since the powers phase
-    if (more) assemble(sl + 1);
+    // next slice's 2X (its buffer is dead since the powers phase) and T_1,
+    // into the U staging buffer once the copy-out has finished
+    PH(5);
+    if (more) assemble(sl + 1, bo(pc ^ 1));
+    tb = pc ^ 1;
+    PH(6);
     // P (running product) into bo(pc) as the B operand of the product GEMM
     {
       double pr[NE], pi[NE];
@@ -339,6 +412,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
     gsync();  // U and the next 2X published; P staged
     first_frags(gu);
+    PH(7);
     // ---- V <- U V  (prefetches the next slice's first 2X fragments)
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
@@ -353,11 +427,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         store_prefix(prefix_out, D, sl, row_of(e), col0 + col_of(e), accR[e], accI[e]);
     }
     __syncthreads();  // product GEMM done reading bo(pc)
-    if (more) {
-      fill_t1();
-      __syncthreads();
-    }
+    PH(8);
   }
+  PH_DONE
   if (active) {
     double pr[NE], pi[NE];
     tmem_load_block<NE>(tm(0), pr, pi);

@@ -1,0 +1,50 @@
+"""Per-phase SM-clock breakdown of the group PS3 lane kernel (lane_ps3g_kernel).
+
+    python tools/phase_prof.py [d] [n_ctrl] [slices]
+
+Builds an instrumented copy of the library (-DSP_PHASE_PROF, clock64 stamps
+by thread 0 of every CTA) into tools/libsliceprop_prof.so, runs one equiprop
+and prints the share of CTA time in each phase of the slice loop.
+"""
+import ctypes
+import importlib.util
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "tools", "libsliceprop_prof.so")
+spec = importlib.util.spec_from_file_location(
+    "_sp_build", os.path.join(ROOT, "paper_2108_07126_b200", "build.py"))
+bmod = importlib.util.module_from_spec(spec)
+spec.loader.exec_module(bmod)
+bmod.build(out=OUT, defines=("SP_PHASE_PROF",))
+os.environ["SLICEPROP_B200_LIB"] = OUT
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+import paper_2108_07126_b200 as sp  # noqa: E402
+from cases import random_inputs  # noqa: E402
+
+NAMES = ["T1 extract", "power GEMMs", "publish 2y", "gsync1+frags", "Clenshaw GEMMs",
+         "sync+publish U", "assemble next X+T1", "write P+gsync2", "product GEMM", "(unused)"]
+d = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+nc = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 20000
+h0, hs, v, dt = random_inputs(d, nc, n, 1)
+ctx = sp.create()
+ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+ctx.set_profiling(True)
+amps = sp.ControlAmplitudes(v, dt)
+ctx.equiprop(amps)
+lib = sp._native.lib
+buf = (ctypes.c_ulonglong * 16)()
+lib.sp_phase_prof(buf)
+ctx.equiprop(amps)
+lib.sp_phase_prof(buf)
+t = ctx.last_timing()
+tot = sum(buf[:10])
+if not tot:
+    sys.exit(f"d={d}: no phase data (kernel {ctx.last_timing()['kernel']} is not instrumented)")
+print(f"d={d} N={nc} n={n}: kernel {t['main_kernel_ms']:.3f} ms ({t['kernel']})")
+for k, name in enumerate(NAMES):
+    print(f"  {name:18s} {100.0 * buf[k] / tot:6.2f} %")
+ctx.close()
