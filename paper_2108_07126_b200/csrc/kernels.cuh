@@ -34,6 +34,19 @@
 
 namespace sp {
 
+#ifdef SP_PHASE_PROF
+// per-phase SM clock totals of thread 0 of every CTA (tools/phase_prof.py;
+// instrumented builds only)
+__device__ unsigned long long g_phase[16];
+#define PH_INIT long long ph_t = clock64(); unsigned long long ph_acc[10] = {0};
+#define PH(k) do { const long long t_ = clock64(); ph_acc[k] += t_ - ph_t; ph_t = t_; } while (0)
+#define PH_DONE if (threadIdx.x == 0) for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]);
+#else
+#define PH_INIT
+#define PH(k) do {} while (0)
+#define PH_DONE
+#endif
+
 // ---------------------------------------------------------------------------
 // small helpers
 // ---------------------------------------------------------------------------

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
   };
 
+  PH_INIT
   for (int64_t sl = s0; sl < s1; ++sl) {
     // ---- 1. weights, 2X assembly (A layout)
     for (int tt = tid_l; tt < T; tt += LT)
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
     }
     sync_all();
+    PH(0);
     // ---- 2. T_1 = X column block (own positions), to B layout + private
     double accR[NE], accI[NE];
     {
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       write_B(bofs0, t1r, t1i, 1.0);
     }
     lane_sync<C>();
+    PH(1);
     // ---- 3. powers T_k = 2X T_{k-1} - T_{k-2}, k = 2..s
     int pb = 0;
     for (int k = 2; k <= s; ++k) {
@@ -218,7 +221,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         write_A(gy, ay_off, accR, accI, 2.0, 0.0);  // 2y = 2 T_s
       }
     }
+    PH(2);
     sync_all();
+    PH(3);
     // ---- 4. Clenshaw in y = T_s with matrix coefficients Q_j
     if (r == 1) {
       load_Q(0, accR, accI);
@@ -247,14 +252,17 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
       }
     }
+    PH(4);
     // U (times the plan phase, 1 for equiprop's symmetric plans) to A layout;
     // in smem it overwrites 2X, dead since the powers were formed
     write_A(gu, ax_off, accR, accI, phase_one ? 1.0 : job.phase[0],
             phase_one ? 0.0 : job.phase[1]);
     sync_all();
+    PH(5);
     // ---- 5. V <- U V
     write_B(bofs0, Pr, Pi, 1.0);
     lane_sync<C>();
+    PH(6);
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       accR[e] = 0.0;
@@ -266,6 +274,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       Pr[e] = accR[e];
       Pi[e] = accI[e];
     }
+    PH(7);
     if (prefix_out) {
 #pragma unroll
       for (int e = 0; e < NE; ++e)
@@ -273,7 +282,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
     // smem A buffers (XS) and B buffers are rewritten by the next slice
     lane_sync<C>();
+    PH(8);
   }
+  PH_DONE
   if (active) {
     double2* o = lane_out + (size_t)lane * D * D;
 #pragma unroll

@@ -23,17 +23,6 @@
 
 namespace sp {
 
-#ifdef SP_PHASE_PROF
-// per-phase SM clock totals of thread 0 of every CTA (tools/phase_prof.py)
-__device__ unsigned long long g_phase[16];
-#define PH_INIT long long ph_t = clock64(); unsigned long long ph_acc[10] = {0};
-#define PH(k) do { const long long t_ = clock64(); ph_acc[k] += t_ - ph_t; ph_t = t_; } while (0)
-#define PH_DONE if (threadIdx.x == 0) for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]);
-#else
-#define PH_INIT
-#define PH(k) do {} while (0)
-#define PH_DONE
-#endif
 
 // tile_mma3 with cross-step prefetch: a holds the kb = 0 fragments on entry;
 // on exit it holds the kb = 0 fragments of An (if An != nullptr)

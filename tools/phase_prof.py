@@ -24,6 +24,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 import paper_2108_07126_b200 as sp  # noqa: E402
 from cases import random_inputs  # noqa: E402
 
+NAMES_PS = ["weights+assembly+sync", "T1 extract", "power GEMMs+2y", "sync", "Clenshaw GEMMs",
+            "U write+sync", "P write+sync", "product GEMM", "prefix+sync", "-"]
 NAMES = ["T1 extract", "power GEMMs", "publish 2y", "gsync1+frags", "Clenshaw GEMMs",
          "sync+publish U", "assemble next X+T1", "write P+gsync2", "product GEMM", "(unused)"]
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 128
@@ -45,6 +47,6 @@ tot = sum(buf[:10])
 if not tot:
     sys.exit(f"d={d}: no phase data (kernel {ctx.last_timing()['kernel']} is not instrumented)")
 print(f"d={d} N={nc} n={n}: kernel {t['main_kernel_ms']:.3f} ms ({t['kernel']})")
-for k, name in enumerate(NAMES):
+for k, name in enumerate(NAMES if "ps3g" in t["kernel"] else NAMES_PS):
     print(f"  {name:18s} {100.0 * buf[k] / tot:6.2f} %")
 ctx.close()

@@ -1,0 +1,140 @@
+"""C5 sweep (BASELINE.json configs[4]): dim 2..512 x slices 1e3..1e7, complex64
+and complex128, one B200, with the CPU reference algorithm timed beside it.
+
+    python tools/sweep.py [--out gpurun_out/sweep.jsonl] [--cap-s 6] [--cpu-s 2]
+
+Each GPU point is the device-resident path (``equiprop_device_ptr``: the
+amplitude table already in HBM, CUDA events on the launching stream, median
+of up to 3 steps after one warm-up).  Systems are the random unit-1-norm
+drift + 2 controls of C3(i) (seed 20240911, beta = 0.5 -> m = 13 fp64 / 7
+fp32), midpoint.  Points whose estimated GPU time exceeds --cap-s are skipped
+(d = 512 x 1e6 would take ~10 min).  The CPU column is the oracle (the
+reference algorithm, numpy/OpenBLAS on all host threads) on a bounded prefix
+of the same system, one rate per (dim, precision): its runtime is linear in
+the slice count (reference property, test_acceptance.py:229-245).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+DIMS = [2, 4, 8, 16, 32, 64, 128, 256, 512]
+SLICES = [1_000, 10_000, 100_000, 1_000_000, 10_000_000]
+N_CTRL = 2
+SEED = 20240911
+
+
+def canonical_flops(d, m, n_terms):
+    return 8.0 * d ** 3 * (m + 1) + 4.0 * d * d * n_terms
+
+
+def cpu_rate(h0, hs, values, dt, bits, target_s):
+    import oracle
+    n0 = 2 if h0.shape[0] >= 256 else 16 if h0.shape[0] >= 64 else 512
+    oracle.equiprop(h0, hs, values[:max(1, n0 // 4)], dt, bits=bits)
+    t0 = time.perf_counter()
+    oracle.equiprop(h0, hs, values[:n0], dt, bits=bits)
+    per = (time.perf_counter() - t0) / n0
+    n = int(max(n0, min(values.shape[0], target_s / max(per, 1e-9))))
+    t0 = time.perf_counter()
+    oracle.equiprop(h0, hs, values[:n], dt, bits=bits)
+    return n / (time.perf_counter() - t0), n
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
+    ap.add_argument("--cap-s", type=float, default=6.0)
+    ap.add_argument("--cpu-s", type=float, default=2.0)
+    ap.add_argument("--dims", default=",".join(map(str, DIMS)))
+    ap.add_argument("--precisions", default="fp64,fp32")
+    args = ap.parse_args()
+    import torch
+
+    import paper_2108_07126_b200 as sp
+    from cases import unit_hermitian
+
+    with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+        peak = json.load(fh)["fp64_dmma_tflops"] * 1e12
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    fh = open(args.out, "w")
+    nmax = max(SLICES)
+    for prec in args.precisions.split(","):
+        bits = 64 if prec == "fp64" else 32
+        for d in map(int, args.dims.split(",")):
+            rng = np.random.default_rng(SEED)
+            h0 = unit_hermitian(rng, d)
+            hs = [unit_hermitian(rng, d) for _ in range(N_CTRL)]
+            dt = 0.5 / (N_CTRL + 1.0)
+            values = rng.uniform(-1.0, 1.0, (nmax, N_CTRL))
+            ctx = sp.create(prec)
+            ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+            ctx.set_profiling(True)
+            plan = ctx.plan_for(dt)
+            F = canonical_flops(d, plan.m_max, N_CTRL + 1)
+            d_amps = torch.from_numpy(values).to(dev)
+            out = torch.empty((d, d), dtype=torch.complex128 if bits == 64 else torch.complex64,
+                              device=dev)
+            rate_est = None
+            cpu, cpu_n = cpu_rate(h0, hs, values, dt, bits, args.cpu_s)
+            for n in SLICES:
+                if rate_est is not None and n / rate_est > args.cap_s:
+                    rec = {"precision": prec, "dim": d, "slices": n, "skipped":
+                           f"estimated {n / rate_est:.0f} s > cap {args.cap_s} s"}
+                    print(json.dumps(rec), flush=True)
+                    fh.write(json.dumps(rec) + "\n")
+                    continue
+
+                def step():
+                    ctx.equiprop_device_ptr(d_amps.data_ptr(), n, N_CTRL, dt, out.data_ptr(),
+                                            stream=stream.cuda_stream, plan=plan)
+                step()
+                torch.cuda.synchronize(dev)
+                ms, kern = [], []
+                for _ in range(3):
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    step()
+                    e1.record(stream)
+                    torch.cuda.synchronize(dev)
+                    ms.append(e0.elapsed_time(e1))
+                    t = ctx.last_timing()
+                    kern.append(t["main_kernel_ms"])
+                    if ms[-1] > 1500:
+                        break
+                step_ms = statistics.median(ms)
+                rate = n / (step_ms / 1e3)
+                rate_est = rate
+                kms = statistics.median(kern)
+                rec = {"precision": prec, "dim": d, "slices": n, "m": plan.m_max,
+                       "slices_per_s": rate, "ms_per_step": step_ms,
+                       "kernel": t["kernel"], "kernel_ms": kms, "launches": t["launches"],
+                       "canonical_tflops": n * F / (step_ms / 1e3) / 1e12,
+                       "fp64_roofline_frac": n * F / (step_ms / 1e3) / peak,
+                       "executed_frac": t["executed_flops"] / (kms / 1e3) / peak,
+                       "series": ctx.last_algorithm(),
+                       "cpu_slices_per_s": cpu, "cpu_sample_slices": cpu_n,
+                       "gpu_over_cpu": rate / cpu}
+                print(json.dumps(rec), flush=True)
+                fh.write(json.dumps(rec) + "\n")
+                fh.flush()
+            ctx.close()
+            del d_amps
+    fh.close()
+
+
+if __name__ == "__main__":
+    main()
