@@ -76,6 +76,20 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+// Ampere-style asynchronous 16-byte global -> shared copies (LDGSTS): many
+// loads in flight per thread without holding registers
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    smem_u32(slot)),
@@ -195,6 +209,68 @@ __device__ __forceinline__ double slice_weight(const SliceJob& j, int64_t s, int
   }
   const int kp = k + 1 + e;
   return (j.dt / 6.0) * (r1[k] * r3[kp] - r3[k] * r1[kp]);
+}
+
+// slice_weight split in two so that the amplitude loads of the next slice can
+// be issued a slice ahead: weight_gather() reads the raw samples term t of
+// slice s needs (at most 4), weight_combine() validates them and forms the
+// weight with exactly slice_weight's arithmetic.
+struct WRaw {
+  double v[4];
+};
+__device__ __forceinline__ WRaw weight_gather(const SliceJob& j, int64_t s, int t) {
+  WRaw w;
+  const int N = j.n_ctrl;
+  if (j.mode == SP_MODE_MIDPOINT) {
+    w.v[0] = j.amps[s * N + (t - 1)];
+    return w;
+  }
+  const double* r1 = j.amps + (2 * s) * N;
+  const double* r2 = r1 + N;
+  const double* r3 = r2 + N;
+  int e = t - 1;
+  if (e < N) {
+    w.v[0] = r1[e];
+    w.v[1] = r2[e];
+    w.v[2] = r3[e];
+    return w;
+  }
+  e -= N;
+  if (e < N) {
+    w.v[0] = r1[e];
+    w.v[1] = r3[e];
+    return w;
+  }
+  e -= N;
+  int k = 0;
+  while (e >= N - 1 - k) {
+    e -= N - 1 - k;
+    ++k;
+  }
+  const int kp = k + 1 + e;
+  w.v[0] = r1[k];
+  w.v[1] = r3[kp];
+  w.v[2] = r3[k];
+  w.v[3] = r1[kp];
+  return w;
+}
+__device__ __forceinline__ double weight_combine(const SliceJob& j, int64_t s, int t,
+                                                 const WRaw& w) {
+  const int N = j.n_ctrl;
+  if (j.mode == SP_MODE_MIDPOINT) {
+    check_amp(j, s, t - 1, w.v[0]);
+    return w.v[0];
+  }
+  int e = t - 1;
+  if (e < N) {
+    check_amp(j, 2 * s, e, w.v[0]);
+    check_amp(j, 2 * s + 1, e, w.v[1]);
+    check_amp(j, 2 * s + 2, e, w.v[2]);
+    return (w.v[0] + 4.0 * w.v[1] + w.v[2]) / 6.0;
+  }
+  e -= N;
+  if (e < N) return (j.dt / 6.0) * (w.v[1] - w.v[0]);
+  return (j.dt / 6.0) * (w.v[0] * w.v[1] - w.v[2] * w.v[3]);
 }
 
 // The one complex dot product every ordered-product kernel uses (pair

@@ -26,12 +26,26 @@
 namespace sp {
 
 constexpr int PS_MAXC = 40;  // max r*s coefficients
+#ifndef SP_PS_GROUP_TCAP
+#define SP_PS_GROUP_TCAP 0
+#endif
 
-// PS needs two A-operand buffers (2X / U, and 2y) when they live in smem
+// PS needs two A-operand buffers (2X / U, and 2y) when they live in smem,
+// plus the private power blocks T_1..T_{s-1} (per thread, accumulator order):
+// the first TSB of them in shared memory, as many as fit without lowering the
+// CTA residency the registers allow (2 per SM for the smem-resident families,
+// 1 for the group families); the rest in global memory (L2)
 template <int D_, int WC_, int MT_, int NT_, int WPL_, int LPC_, int GPL_, bool XS_>
 struct PSCfg : TCCfg<D_, WC_, MT_, NT_, WPL_, LPC_, GPL_, XS_> {
   using B = TCCfg<D_, WC_, MT_, NT_, WPL_, LPC_, GPL_, XS_>;
-  static constexpr int LANE_DBL = 2 * B::BDBL + (XS_ ? 2 * B::XDBL : 0) + B::WMAX;
+  static constexpr int NE = MT_ * NT_ * 4;
+  static constexpr int TBLK = 2 * NE * WPL_ * 32;  // doubles of one power block (lane)
+  static constexpr int BASE_DBL = 2 * B::BDBL + (XS_ ? 2 * B::XDBL : 0) + B::WMAX;
+  static constexpr int CAP = XS_ ? 233472 / 2 - 1024 : SP_PS_GROUP_TCAP;  // bytes per CTA
+  static constexpr int TSB = (BASE_DBL + 2 * TBLK) * LPC_ * 8 <= CAP   ? 2
+                             : (BASE_DBL + TBLK) * LPC_ * 8 <= CAP ? 1
+                                                                   : 0;
+  static constexpr int LANE_DBL = BASE_DBL + TSB * TBLK;
   static constexpr size_t SMEM = (size_t)LANE_DBL * LPC_ * sizeof(double);
 };
 
@@ -67,6 +81,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int ax_off = lbase + 2 * C::BDBL;           // XS: 2X, later U
   const int ay_off = ax_off + C::XDBL;              // XS: 2y
   const int w_off = lbase + 2 * C::BDBL + (C::XS ? 2 * C::XDBL : 0);
+  const int t_off = w_off + C::WMAX;               // smem power blocks (TSB of them)
   // global A buffers (group families): 2X, 2y, U
   double* gx = AG ? gA + (size_t)group * 3 * C::XDBL : nullptr;
   double* gy = AG ? gx + C::XDBL : nullptr;
@@ -78,9 +93,19 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int nt0 = (wil / (C::S / MT)) * NT;
   const int col0 = cb * WC;
   const int s = pj.s, r = pj.r;
-  // private column blocks of T_1..T_{s-1}, acc-native, coalesced per thread
-  auto tp = [&](int kk, int e) -> double2& {
-    return tpriv[(((size_t)blockIdx.x * (s - 1) + kk) * NE + e) * C::THREADS + threadIdx.x];
+  // private column blocks of T_1..T_{s-1}, acc-native, coalesced per thread:
+  // blocks < TSB in shared memory, the rest in global memory
+  auto tp_load = [&](int kk, int e) -> double2 {
+    if (kk < C::TSB)
+      return *reinterpret_cast<const double2*>(&smem[t_off + kk * C::TBLK + 2 * (e * LT + tid_l)]);
+    return __ldcg(&tpriv[(((size_t)blockIdx.x * (s - 1) + kk) * NE + e) * C::THREADS +
+                         threadIdx.x]);
+  };
+  auto tp_store = [&](int kk, int e, double2 v) {
+    if (kk < C::TSB)
+      *reinterpret_cast<double2*>(&smem[t_off + kk * C::TBLK + 2 * (e * LT + tid_l)]) = v;
+    else
+      tpriv[(((size_t)blockIdx.x * (s - 1) + kk) * NE + e) * C::THREADS + threadIdx.x] = v;
   };
   auto row_of = [&](int idx) { return 16 * (ms0 + idx / (NT * 4)) + g + 8 * ((idx & 3) >> 1); };
   auto col_of = [&](int idx) { return 8 * (nt0 + (idx / 4) % NT) + 2 * t4 + (idx & 1); };
@@ -140,39 +165,80 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const double ar = pj.alpha[2 * (j * s + i)], ai = pj.alpha[2 * (j * s + i) + 1];
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
-        const double2 tv = __ldcg(&tp(i - 1, e));
+        const double2 tv = tp_load(i - 1, e);
         qr[e] = fma(ar, tv.x, fma(-ai, tv.y, qr[e]));
         qi[e] = fma(ar, tv.y, fma(ai, tv.x, qi[e]));
       }
     }
   };
 
+  // raw samples of weight tid_l (>= 1) of the next slice, loaded a slice ahead
+  // (smem-resident families; the group families are at the register limit)
+  constexpr bool PFW = C::XS;
+  WRaw wr{};
+  if (PFW && s0 < s1 && tid_l >= 1 && tid_l < T) wr = weight_gather(job, s0, tid_l);
   PH_INIT
   for (int64_t sl = s0; sl < s1; ++sl) {
     // ---- 1. weights, 2X assembly (A layout)
-    for (int tt = tid_l; tt < T; tt += LT)
-      smem[w_off + tt] = (tt == 0) ? job.xs : job.xs * slice_weight(job, sl, tt);
+    if (tid_l < T)
+      smem[w_off + tid_l] = (tid_l == 0) ? job.xs
+                            : job.xs * (PFW ? weight_combine(job, sl, tid_l, wr)
+                                            : slice_weight(job, sl, tid_l));
+    for (int tt = tid_l + LT; tt < T; tt += LT)
+      smem[w_off + tt] = job.xs * slice_weight(job, sl, tt);
+    if (PFW && sl + 1 < s1 && tid_l >= 1 && tid_l < T) wr = weight_gather(job, sl + 1, tid_l);
     lane_sync<C>();
     {
-      int lo, hi, first, stride;
-      if constexpr (C::XS) {
-        lo = 0; hi = C::XDBL; first = tid_l; stride = LT;
-      } else {
-        lo = cb * (C::XDBL / C::GPL); hi = lo + C::XDBL / C::GPL;
-        first = threadIdx.x; stride = C::THREADS;
-      }
-      for (int i = lo + 2 * first; i < hi; i += 2 * stride) {
-        double2 h = __ldg(reinterpret_cast<const double2*>(terms + i));
-        double xr = smem[w_off] * h.x, xi = smem[w_off] * h.y;
-        for (int tt = 1; tt < T; ++tt) {
-          h = __ldg(reinterpret_cast<const double2*>(terms + (size_t)tt * C::XDBL + i));
-          xr = fma(smem[w_off + tt], h.x, xr);
-          xi = fma(smem[w_off + tt], h.y, xi);
+      // QB pairs x 2 terms of loads in flight per thread (L2-latency bound
+      // otherwise); summation order as before: term 0, then 1..T-1
+      constexpr int CH = C::XS ? C::XDBL : C::XDBL / C::GPL;  // doubles per lane / CTA
+      constexpr int STR = C::XS ? LT : C::THREADS;
+      constexpr int UPT = CH / (2 * STR);
+      constexpr int QB = UPT < 4 ? UPT : 4;
+      static_assert(CH % (2 * STR) == 0 && UPT % QB == 0, "assembly tiling");
+      const int lo = C::XS ? 0 : cb * CH;
+      const int first = C::XS ? tid_l : (int)threadIdx.x;
+#pragma unroll 1
+      for (int b = 0; b < UPT; b += QB) {
+        int idx[QB];
+        double2 x[QB];
+        const double w0 = smem[w_off];
+        auto term = [&](int t, int i) -> double2 {
+          return __ldg(reinterpret_cast<const double2*>(terms + (size_t)t * C::XDBL + i));
+        };
+#pragma unroll
+        for (int u = 0; u < QB; ++u) {
+          idx[u] = lo + 2 * (first + (b + u) * STR);
+          const double2 h = term(0, idx[u]);
+          x[u] = make_double2(w0 * h.x, w0 * h.y);
         }
-        if constexpr (AG)
-          *reinterpret_cast<double2*>(gx + i) = make_double2(xr, xi);
-        else
-          *reinterpret_cast<double2*>(&smem[ax_off + i]) = make_double2(xr, xi);
+#pragma unroll 1
+        for (int tt = 1; tt < T; tt += 2) {
+          const bool two = tt + 1 < T;
+          double2 h[2][QB];
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int u = 0; u < QB; ++u)
+              if (k == 0 || two) h[k][u] = term(tt + k, idx[u]);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            if (k == 1 && !two) break;
+            const double w = smem[w_off + tt + k];
+#pragma unroll
+            for (int u = 0; u < QB; ++u) {
+              x[u].x = fma(w, h[k][u].x, x[u].x);
+              x[u].y = fma(w, h[k][u].y, x[u].y);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < QB; ++u) {
+          if constexpr (AG)
+            *reinterpret_cast<double2*>(gx + idx[u]) = x[u];
+          else
+            *reinterpret_cast<double2*>(&smem[ax_off + idx[u]]) = x[u];
+        }
       }
     }
     sync_all();
@@ -187,7 +253,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         const int i0 = xfrag_index(D, rr, c, 0), i1 = xfrag_index(D, rr, c, 1);
         t1r[e] = 0.5 * (AG ? __ldcg(gx + i0) : smem[ax_off + i0]);
         t1i[e] = 0.5 * (AG ? __ldcg(gx + i1) : smem[ax_off + i1]);
-        tp(0, e) = make_double2(t1r[e], t1i[e]);
+        tp_store(0, e, make_double2(t1r[e], t1i[e]));
       }
       write_B(bofs0, t1r, t1i, 1.0);
     }
@@ -205,23 +271,25 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       } else {
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
-          const double2 tv = __ldcg(&tp(k - 3, e));
+          const double2 tv = tp_load(k - 3, e);
           accR[e] = -tv.x;
           accI[e] = -tv.y;
         }
       }
+      PH(8);
       tile_mma<C, AG>(gx, ax_off, bo(pb), accR, accI, ms0, nt0, ln);
+      PH(2);
       if (k < s) {
         write_B(bo(pb ^ 1), accR, accI, 1.0);
 #pragma unroll
-        for (int e = 0; e < NE; ++e) tp(k - 1, e) = make_double2(accR[e], accI[e]);
+        for (int e = 0; e < NE; ++e) tp_store(k - 1, e, make_double2(accR[e], accI[e]));
         pb ^= 1;
         lane_sync<C>();
       } else {
         write_A(gy, ay_off, accR, accI, 2.0, 0.0);  // 2y = 2 T_s
       }
     }
-    PH(2);
+    PH(8);
     sync_all();
     PH(3);
     // ---- 4. Clenshaw in y = T_s with matrix coefficients Q_j
@@ -244,7 +312,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
             accI[e] -= smem[o + bfrag_index<C>(rr, n, 1)];
           }
         }
+        PH(9);
         tile_mma<C, AG>(gy, ay_off, bo(pc), accR, accI, ms0, nt0, ln);
+        PH(4);
         if (j >= 1) {
           write_B(bo(pc ^ 1), accR, accI, (j == 1) ? 0.5 : 1.0);
           pc ^= 1;
@@ -252,7 +322,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
       }
     }
-    PH(4);
+    PH(9);
     // U (times the plan phase, 1 for equiprop's symmetric plans) to A layout;
     // in smem it overwrites 2X, dead since the powers were formed
     write_A(gu, ax_off, accR, accI, phase_one ? 1.0 : job.phase[0],
@@ -282,7 +352,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
     // smem A buffers (XS) and B buffers are rewritten by the next slice
     lane_sync<C>();
-    PH(8);
+    PH(5);
   }
   PH_DONE
   if (active) {

@@ -24,8 +24,9 @@ sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 import paper_2108_07126_b200 as sp  # noqa: E402
 from cases import random_inputs  # noqa: E402
 
-NAMES_PS = ["weights+assembly+sync", "T1 extract", "power GEMMs+2y", "sync", "Clenshaw GEMMs",
-            "U write+sync", "P write+sync", "product GEMM", "prefix+sync", "-"]
+NAMES_PS = ["weights+assembly+sync", "T1 extract", "power GEMMs", "sync", "Clenshaw GEMMs",
+            "U write+sync, tail", "P write+sync", "product GEMM", "power non-GEMM",
+            "Clenshaw non-GEMM"]
 NAMES = ["T1 extract", "power GEMMs", "publish 2y", "gsync1+frags", "Clenshaw GEMMs",
          "sync+publish U", "assemble next X+T1", "write P+gsync2", "product GEMM", "(unused)"]
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 128
