@@ -21,6 +21,7 @@
 #include "kernels_ps3.cuh"
 #include "kernels_ps3g.cuh"
 #include "kernels_apply.cuh"
+#include "kernels_d8.cuh"
 
 using namespace sp;
 
@@ -30,8 +31,13 @@ const char* kVersion = "sliceprop_b200 0.1.0 (sm_100a)";
 thread_local char g_err[512] = "";
 
 enum Family {
-  FAM_NONE = 0, FAM_S2, FAM_S4, FAM_T16, FAM_T32, FAM_T64, FAM_T128, FAM_T256, FAM_T512
+  FAM_NONE = 0, FAM_S2, FAM_S4, FAM_T16, FAM_T32, FAM_T64, FAM_T128, FAM_T256, FAM_T512,
+  FAM_T8
 };
+
+// families whose lane products / prefixes use the plain row-major layout
+// (ordered tree, fold and prefix application shared with the small families)
+bool plain_family(int fam) { return fam == FAM_S2 || fam == FAM_S4 || fam == FAM_T8; }
 
 // tensor-core configurations (see TCCfg): D, WC, MT, NT, WPL, LPC, GPL, X-in-smem
 using Cfg16 = TCCfg<16, 16, 1, 2, 1, 4, 1, true>;
@@ -125,6 +131,7 @@ void ps_coefficients(const double* coef, int m, int s, double* alpha, int* r_out
 int family_for(int d, int* D) {
   if (d <= 2) { *D = 2; return FAM_S2; }
   if (d <= 4) { *D = 4; return FAM_S4; }
+  if (d <= 8) { *D = 8; return FAM_T8; }
   if (d <= 16) { *D = 16; return FAM_T16; }
   if (d <= 32) { *D = 32; return FAM_T32; }
   if (d <= 64) { *D = 64; return FAM_T64; }
@@ -136,6 +143,9 @@ int family_for(int d, int* D) {
 }
 
 const char* family_kernel_name(int fam, int algo) {
+  if (fam == FAM_T8)
+    return algo == 3 ? "lane_d8_kernel<ps3m>" : algo == 2 ? "lane_d8_kernel<ps>"
+                                                          : "lane_d8_kernel<clenshaw>";
   if (algo == 3) {
     switch (fam) {
       case FAM_T16: return "lane_ps3_kernel<D16>";
@@ -277,11 +287,24 @@ int ps_prepare(sp_ctx* ctx);
 template <class C>
 int ps3_prepare(sp_ctx* ctx);
 
+int d8_prepare(sp_ctx* ctx);
+
 // permute + pad the host terms into the family's device layout
 int upload_terms(sp_ctx* ctx) {
   const int d = ctx->dim, D = ctx->D, T = ctx->n_terms;
   std::vector<double> h;
-  if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
+  if (ctx->fam == FAM_T8) {
+    // m8n8k4 A-fragment order (kernels_d8.cuh d8_apos), complex interleaved
+    h.assign((size_t)T * 64 * 2, 0.0);
+    for (int t = 0; t < T; ++t)
+      for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+          const double* src = &ctx->terms_host[(((size_t)t * d + r) * d + c) * 2];
+          const int pos = (c >> 2) * 32 + ((r << 2) | (c & 3));
+          h[((size_t)t * 64 + pos) * 2] = src[0];
+          h[((size_t)t * 64 + pos) * 2 + 1] = src[1];
+        }
+  } else if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
     h.assign((size_t)T * D * D * 2, 0.0);
     for (int t = 0; t < T; ++t)
       for (int r = 0; r < d; ++r)
@@ -306,7 +329,7 @@ int upload_terms(sp_ctx* ctx) {
   if (rc) return rc;
   CUDA_TRY(ctx, cudaMemcpy(ctx->terms.p, h.data(), h.size() * sizeof(double),
                            cudaMemcpyHostToDevice));
-  if (!(ctx->fam == FAM_S2 || ctx->fam == FAM_S4)) {
+  if (!plain_family(ctx->fam)) {
     // 3-plane (re, im, re+im) copy for the 3-multiplication kernels
     const size_t xd3 = (size_t)3 * D * D;
     std::vector<double> h3((size_t)T * xd3, 0.0);
@@ -322,6 +345,10 @@ int upload_terms(sp_ctx* ctx) {
     if (rc) return rc;
     CUDA_TRY(ctx, cudaMemcpy(ctx->terms3.p, h3.data(), h3.size() * sizeof(double),
                              cudaMemcpyHostToDevice));
+  }
+  if (ctx->fam == FAM_T8) {
+    rc = d8_prepare(ctx);
+    if (rc) return rc;
   }
   switch (ctx->fam) {
     case FAM_T16: rc = ps3_prepare<P3_16>(ctx); break;
@@ -603,6 +630,76 @@ int reduce_pairwise_dev(sp_ctx* ctx, const double2* in, int cnt, int D, cudaStre
   return SP_OK;
 }
 
+// ---- family D8: one warp per lane, m8n8k4 DMMA (kernels_d8.cuh)
+constexpr int D8_WPC = 8;  // lanes (warps) per CTA
+constexpr size_t D8_SMEM = ((size_t)D8_WPC * D8_SLOT + 2 * 64 * D8_TSM) * sizeof(double);
+
+template <int ALG>
+int d8_prepare_one(sp_ctx* ctx) {
+  CUDA_TRY(ctx, cudaFuncSetAttribute(lane_d8_kernel<D8_WPC, ALG>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D8_SMEM));
+  return SP_OK;
+}
+
+int d8_prepare(sp_ctx* ctx) {
+  int rc = d8_prepare_one<D8_CLENSHAW>(ctx);
+  if (!rc) rc = d8_prepare_one<D8_PS>(ctx);
+  if (!rc) rc = d8_prepare_one<D8_PS3>(ctx);
+  return rc;
+}
+
+template <int ALG>
+int d8_lanes(sp_ctx* ctx, int64_t n) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_d8_kernel<D8_WPC, ALG>, 32 * D8_WPC,
+                                                D8_SMEM);
+  if (occ < 1) occ = 1;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * occ * D8_WPC, n));
+}
+
+int d8_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_t st,
+              const double2** prods, int* count) {
+  const int ps_s = (ctx->algo == ALGO_CLENSHAW) ? 0
+                   : (ctx->algo == ALGO_PS || ctx->algo == ALGO_PS3)
+                         ? std::max(2, ps_choose(job.m) ? ps_choose(job.m) : 2)
+                         : ps_choose(job.m);
+  const int alg = ps_s == 0 ? D8_CLENSHAW : (ctx->algo == ALGO_PS3 ? D8_PS3 : D8_PS);
+  PSJob pj;
+  std::memset(&pj, 0, sizeof(pj));
+  pj.base = job;
+  if (ps_s > 0) {
+    pj.s = ps_s;
+    ps_coefficients(job.coef, job.m, ps_s, pj.alpha, &pj.r);
+  }
+  const int64_t n = job.n_slices;
+  const int lanes = alg == D8_CLENSHAW ? d8_lanes<D8_CLENSHAW>(ctx, n)
+                    : alg == D8_PS     ? d8_lanes<D8_PS>(ctx, n)
+                                       : d8_lanes<D8_PS3>(ctx, n);
+  int rc = ensure(ctx, ctx->lanes, (size_t)lanes * 64 * sizeof(double2));
+  if (rc) return rc;
+  double2* lane_out = (double2*)ctx->lanes.p;
+  const double2* terms = (const double2*)ctx->terms.p;
+  const int grid = (lanes + D8_WPC - 1) / D8_WPC;
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+  if (alg == D8_CLENSHAW)
+    lane_d8_kernel<D8_WPC, D8_CLENSHAW><<<grid, 32 * D8_WPC, D8_SMEM, st>>>(pj, terms, lanes,
+                                                                          lane_out, prefix_out);
+  else if (alg == D8_PS)
+    lane_d8_kernel<D8_WPC, D8_PS><<<grid, 32 * D8_WPC, D8_SMEM, st>>>(pj, terms, lanes,
+                                                                    lane_out, prefix_out);
+  else
+    lane_d8_kernel<D8_WPC, D8_PS3><<<grid, 32 * D8_WPC, D8_SMEM, st>>>(pj, terms, lanes,
+                                                                     lane_out, prefix_out);
+  CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+  ++ctx->launches;
+  ctx->last_algo = alg == D8_CLENSHAW ? ALGO_CLENSHAW : alg == D8_PS ? ALGO_PS : ALGO_PS3;
+  ctx->last_gemms = ps_s == 0 ? job.m : ps_cost(job.m, ps_s);
+  *prods = lane_out;
+  *count = lanes;
+  return SP_OK;
+}
+
 // Run the lane pass.  Returns the lane products (lane_count of them) on the
 // device, or (small families, pairwise) the per-CTA products.
 int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix_out,
@@ -611,6 +708,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   const int D = ctx->D;
   const size_t dd = (size_t)D * D;
   int lanes = 1;
+  if (ctx->fam == FAM_T8) return d8_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
     const int tpl = (ctx->fam == FAM_S2) ? 1 : 4;
     int64_t cap = (int64_t)ctx->sms * 2048 / tpl;
@@ -865,8 +963,9 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
     ++ctx->launches;
     total = (const double2*)ctx->result.p;
   } else {
-    const bool small = ctx->fam == FAM_S2 || ctx->fam == FAM_S4;
-    const bool cta_reduce = small && reduction == SP_REDUCE_PAIRWISE;
+    const bool small = plain_family(ctx->fam);
+    const bool cta_reduce =
+        (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) && reduction == SP_REDUCE_PAIRWISE;
     const double2* prods = nullptr;
     int cnt = 0;
     // small families + pairwise: one launch does everything (fused tail)
@@ -1159,7 +1258,7 @@ int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, do
   rc = ensure(ctx, ctx->out, obytes);
   if (rc) return rc;
   ctx->launches += 1;
-  if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
+  if (plain_family(ctx->fam)) {
     rc = ensure(ctx, ctx->cumO, (size_t)n * dd * sizeof(double2));
     if (rc) return rc;
     apply_prefix_kernel<<<grid_for((int64_t)n * dd, 256), 256, 0, st>>>(

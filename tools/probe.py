@@ -55,3 +55,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "cum":
         print(f"cum d{d} n={n}: wall {wall*1e3:.2f} ms (lane kernel {lane_ms:.2f} ms), output "
               f"{out_gb:.3f} GB, final==seq {np.array_equal(cum.final, seq)}", flush=True)
         ctx.close()
+if len(sys.argv) > 1 and sys.argv[1] == "d8":
+    for d in (5, 8):
+        for a in ("auto", "clenshaw", "ps", "ps3m"):
+            run(f"d{d} rand 1e6 {a}", *random_inputs(d, 2, 1000000, 1), algo=a)
