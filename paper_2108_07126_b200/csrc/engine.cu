@@ -711,9 +711,16 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   if (ctx->fam == FAM_T8) return d8_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
     const int tpl = (ctx->fam == FAM_S2) ? 1 : 4;
-    int64_t cap = (int64_t)ctx->sms * 2048 / tpl;
-    int64_t want = cta_reduce ? std::max<int64_t>((int64_t)ctx->sms * 256 / tpl, (n + 7) / 8)
-                              : 1024;
+    // pairwise: one full wave of resident threads (every thread busy, no
+    // second partial wave); sequential / cumulative: 1024 lanes for the fold
+    int occ = 0;
+    if (ctx->fam == FAM_S2)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_small_kernel<2, 1>, 256, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_small_kernel<4, 4>, 256, 0);
+    occ = std::max(occ, 1);
+    int64_t cap = (int64_t)ctx->sms * occ * 256 / tpl;
+    int64_t want = cta_reduce ? cap : 1024;
     lanes = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(cap, want), n));
     const int blocks = (int)(((int64_t)lanes * tpl + 255) / 256);
     int rc = ensure(ctx, ctx->lanes, (size_t)(cta_reduce ? blocks : lanes) * dd * sizeof(double2));

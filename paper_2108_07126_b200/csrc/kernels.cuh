@@ -311,7 +311,9 @@ struct SmallTail {
 };
 
 template <int D, int TPL>
-__global__ void __launch_bounds__(256) lane_small_kernel(SliceJob job,
+// (register budget for 3 CTAs/SM at D = 2 and 2 at D = 4: the lane loop is
+// latency bound and needs the resident warps)
+__global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJob job,
                                                          const double2* __restrict__ terms,
                                                          int lanes, double2* __restrict__ lane_out,
                                                          double2* cta_out,
@@ -333,7 +335,14 @@ __global__ void __launch_bounds__(256) lane_small_kernel(SliceJob job,
   const int m = job.m;
   const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
 
+  // the amplitude rows a few slices ahead are prefetched into L1 (no
+  // registers held): the loop is otherwise bound by one memory round trip
+  // per slice; a thread's slices are contiguous rows of the table
+  const int64_t rows_per_slice = job.mode == SP_MODE_MIDPOINT ? 1 : 2;
   for (int64_t s = s0; s < s1; ++s) {
+    if (s + 4 < s1)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(job.amps + (s + 4) * rows_per_slice *
+                                                                   job.n_ctrl));
     // ---- assemble 2X in registers
     double2 X[D][D];
 #pragma unroll
