@@ -194,6 +194,7 @@ struct sp_ctx {
   bool loaded = false;
   int dim = 0, n_ctrl = 0, n_terms = 0, mode = 0;
   std::vector<double> terms_host;  // T x d x d complex128 interleaved
+  bool herm_exact = false;         // every term bitwise Hermitian
   // device-side
   bool dev_ready = false;
   bool terms_uploaded = false;
@@ -711,7 +712,8 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   if (ctx->fam == FAM_T8) return d8_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
     const int tpl = (ctx->fam == FAM_S2) ? 1 : 4;
-    // pairwise: one full wave of resident threads (every thread busy, no
+    // pairwise: at least 4 slices per lane (short CTA tree and tail for the
+    // latency-bound small n), at most one full wave of resident threads (no
     // second partial wave); sequential / cumulative: 1024 lanes for the fold
     int occ = 0;
     if (ctx->fam == FAM_S2)
@@ -720,7 +722,8 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_small_kernel<4, 4>, 256, 0);
     occ = std::max(occ, 1);
     int64_t cap = (int64_t)ctx->sms * occ * 256 / tpl;
-    int64_t want = cta_reduce ? cap : 1024;
+    int64_t want = cta_reduce ? std::max<int64_t>((int64_t)ctx->sms * 256 / tpl, (n + 3) / 4)
+                              : 1024;
     lanes = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(cap, want), n));
     const int blocks = (int)(((int64_t)lanes * tpl + 255) / 256);
     int rc = ensure(ctx, ctx->lanes, (size_t)(cta_reduce ? blocks : lanes) * dd * sizeof(double2));
@@ -892,6 +895,7 @@ int build_job(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double
   job->phase[0] = plan->phase[0];
   job->phase[1] = plan->phase[1];
   job->n_slices = n;
+  job->herm_exact = ctx->herm_exact ? 1 : 0;
   return SP_OK;
 }
 
@@ -939,7 +943,9 @@ int prepare_device(sp_ctx* ctx) {
 
 double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
   const double D = ctx->D;
-  (void)m;
+  // D = 2: Clenshaw on (a, b) coefficient pairs (~32 flop/step) + forming U
+  // and V <- U V (~120 flop) (lane_small_kernel<2,1>)
+  if (ctx->fam == FAM_S2) return (double)n * (32.0 * m + 120.0 + 16.0 * ctx->n_terms);
   // 3-multiplication products execute 3/4 of the real FP64 MMA work
   const double f = (ctx->last_algo == ALGO_PS3) ? 6.0 : 8.0;
   return (double)n * (f * D * D * D * ctx->last_gemms + 4.0 * D * D * ctx->n_terms);
@@ -1166,6 +1172,17 @@ int sp_set_hamiltonian(sp_ctx* ctx, int dim, int n_ctrl, int n_terms, int mode,
   ctx->n_terms = n_terms;
   ctx->mode = mode;
   ctx->terms_host.assign(terms, terms + (size_t)n_terms * dim * dim * 2);
+  ctx->herm_exact = true;
+  for (int t = 0; t < n_terms && ctx->herm_exact; ++t)
+    for (int r = 0; r < dim && ctx->herm_exact; ++r)
+      for (int c = r; c < dim; ++c) {
+        const double* a = &ctx->terms_host[(((size_t)t * dim + r) * dim + c) * 2];
+        const double* b = &ctx->terms_host[(((size_t)t * dim + c) * dim + r) * 2];
+        if (!(a[0] == b[0] && a[1] == -b[1])) {
+          ctx->herm_exact = false;
+          break;
+        }
+      }
   ctx->fam = fam;
   ctx->D = D;
   ctx->terms_uploaded = false;

@@ -31,6 +31,9 @@ struct SliceJob {
   // first out-of-range amplitude (row-major index), ULLONG_MAX if none:
   // validation fused into the weight computation (hamiltonian.py:145-153)
   unsigned long long* viol;
+  // every expansion term is exactly (bitwise) Hermitian: the d <= 2 kernel
+  // may then use real Cayley-Hamilton coefficients (lane_small_kernel<2,1>)
+  int herm_exact;
 };
 
 }  // namespace sp

@@ -40,7 +40,7 @@ namespace sp {
 __device__ unsigned long long g_phase[16];
 #define PH_INIT long long ph_t = clock64(); unsigned long long ph_acc[10] = {0};
 #define PH(k) do { const long long t_ = clock64(); ph_acc[k] += t_ - ph_t; ph_t = t_; } while (0)
-#define PH_DONE if (threadIdx.x == 0) for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]);
+#define PH_DONE if (threadIdx.x == 0) { for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]); atomicAdd(&g_phase[15], 1ull); }
 #else
 #define PH_INIT
 #define PH(k) do {} while (0)
@@ -310,6 +310,46 @@ struct SmallTail {
   int to_fp32;
 };
 
+// C = A B for D x D complex matrices in registers
+template <int D>
+__device__ __forceinline__ void mat_mul(const double2 (&A)[D][D], const double2 (&B)[D][D],
+                                        double2 (&C)[D][D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        re = fma(A[r][k].x, B[k][c].x, re);
+        re = fma(-A[r][k].y, B[k][c].y, re);
+        im = fma(A[r][k].x, B[k][c].y, im);
+        im = fma(A[r][k].y, B[k][c].x, im);
+      }
+      C[r][c] = make_double2(re, im);
+    }
+}
+
+// ordered product over the first `width` lanes of a warp: lane 0 ends with
+// M_{width-1} ... M_1 M_0 (later lanes on the left)
+template <int D>
+__device__ __forceinline__ void warp_ordered_product(double2 (&M)[D][D], int width = 32) {
+  for (int k = 1; k < width; k <<= 1) {
+    double2 W[D][D], N[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+        W[r][c] = make_double2(__shfl_down_sync(0xffffffffu, M[r][c].x, k),
+                               __shfl_down_sync(0xffffffffu, M[r][c].y, k));
+    mat_mul<D>(W, M, N);
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) M[r][c] = N[r][c];
+  }
+}
+
 template <int D, int TPL>
 // (register budget for 3 CTAs/SM at D = 2 and 2 at D = 4: the lane loop is
 // latency bound and needs the resident warps)
@@ -338,19 +378,123 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
   // the amplitude rows a few slices ahead are prefetched into L1 (no
   // registers held): the loop is otherwise bound by one memory round trip
   // per slice; a thread's slices are contiguous rows of the table
+  // midpoint with <= RP controls (the driven qubit): the next slice's row is
+  // loaded into registers a slice ahead instead
   const int64_t rows_per_slice = job.mode == SP_MODE_MIDPOINT ? 1 : 2;
+  constexpr int RP = 4;
+  const bool rowpf = job.mode == SP_MODE_MIDPOINT && job.n_ctrl <= RP;
+  double nrow[RP];
+  auto load_row = [&](int64_t sl) {
+    const double* a = job.amps + sl * job.n_ctrl;
+#pragma unroll
+    for (int q = 0; q < RP; ++q)
+      if (q < job.n_ctrl) nrow[q] = a[q];
+  };
+  if (rowpf && s0 < s1) load_row(s0);
+  // D = 2, exactly Hermitian terms, <= 3 terms, midpoint (the driven qubit):
+  // Z = 2X = z0 I + Z' with real z0, Z'00 = -Z'11 = dz real, Z'01 = conj(Z'10)
+  // = zc, Z'^2 = zeta2 I with zeta2 = dz^2 + |zc|^2 real, so the Clenshaw
+  // pairs below need real-by-complex products only; the per-term (z0, dz, zc)
+  // contributions, with the 2X factor folded in, are formed once per thread
+  const bool fast2 = D == 2 && job.herm_exact && rowpf && T <= 3;
+  double tA[3] = {0.0, 0.0, 0.0}, tB[3] = {0.0, 0.0, 0.0};
+  double2 tC[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  if (fast2) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      if (q < T) {
+        const double2* H = terms + (size_t)q * D * D;
+        tA[q] = job.xs * (0.5 * (H[0].x + H[D * D - 1].x));
+        tB[q] = job.xs * (0.5 * (H[0].x - H[D * D - 1].x));
+        tC[q] = make_double2(job.xs * H[1].x, job.xs * H[1].y);
+      }
+  }
+  PH_INIT
   for (int64_t s = s0; s < s1; ++s) {
-    if (s + 4 < s1)
+    double crow[RP];
+#pragma unroll
+    for (int q = 0; q < RP; ++q) crow[q] = nrow[q];
+    if (rowpf) {
+      if (s + 1 < s1) load_row(s + 1);
+    } else if (s + 4 < s1) {
       asm volatile("prefetch.global.L1 [%0];" ::"l"(job.amps + (s + 4) * rows_per_slice *
                                                                    job.n_ctrl));
+    }
+    if constexpr (D == 2) {
+      if (fast2) {
+        double z0 = tA[0], dz = tB[0];
+        double2 zc = tC[0];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q + 1 >= T) break;
+          const double w = crow[q];
+          check_amp(job, s, q, w);
+          z0 = fma(w, tA[q + 1], z0);
+          dz = fma(w, tB[q + 1], dz);
+          zc.x = fma(w, tC[q + 1].x, zc.x);
+          zc.y = fma(w, tC[q + 1].y, zc.y);
+        }
+        const double zeta2 = fma(dz, dz, fma(zc.x, zc.x, zc.y * zc.y));
+        double2 ca = make_double2(job.coef[2 * m], job.coef[2 * m + 1]);
+        double2 cb = make_double2(0.0, 0.0), oa = cb, ob = cb;
+        for (int jj = m - 1; jj >= 0; --jj) {
+          const double beta = (jj == 0) ? 2.0 : 1.0;
+          const double2 na =
+              make_double2(job.coef[2 * jj] + fma(z0, ca.x, fma(zeta2, cb.x, -beta * oa.x)),
+                           job.coef[2 * jj + 1] + fma(z0, ca.y, fma(zeta2, cb.y, -beta * oa.y)));
+          const double2 nb = make_double2(ca.x + fma(z0, cb.x, -beta * ob.x),
+                                          ca.y + fma(z0, cb.y, -beta * ob.y));
+          oa = ca;
+          ob = cb;
+          ca = na;
+          cb = nb;
+        }
+        if (!phase_one) {
+          const double pr = job.phase[0], pi = job.phase[1];
+          ca = make_double2(pr * ca.x - pi * ca.y, pr * ca.y + pi * ca.x);
+          cb = make_double2(pr * cb.x - pi * cb.y, pr * cb.y + pi * cb.x);
+        }
+        double2 U[2][2];
+        U[0][0] = make_double2(fma(cb.x, dz, ca.x), fma(cb.y, dz, ca.y));
+        U[1][1] = make_double2(fma(-cb.x, dz, ca.x), fma(-cb.y, dz, ca.y));
+        U[0][1] = make_double2(cb.x * zc.x - cb.y * zc.y, cb.x * zc.y + cb.y * zc.x);
+        U[1][0] = make_double2(cb.x * zc.x + cb.y * zc.y, cb.y * zc.x - cb.x * zc.y);
+        double2 nv[2][CPT];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int cc = 0; cc < CPT; ++cc) {
+            double re = U[r][0].x * V[0][cc].x;
+            re = fma(-U[r][0].y, V[0][cc].y, re);
+            re = fma(U[r][1].x, V[1][cc].x, re);
+            re = fma(-U[r][1].y, V[1][cc].y, re);
+            double im = U[r][0].x * V[0][cc].y;
+            im = fma(U[r][0].y, V[0][cc].x, im);
+            im = fma(U[r][1].x, V[1][cc].y, im);
+            im = fma(U[r][1].y, V[1][cc].x, im);
+            nv[r][cc] = make_double2(re, im);
+          }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int cc = 0; cc < CPT; ++cc) V[r][cc] = nv[r][cc];
+        if (prefix_out) {
+          double2* o = prefix_out + (size_t)s * D * D;
+#pragma unroll
+          for (int r = 0; r < D; ++r)
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) o[r * D + c0 + cc] = V[r][cc];
+        }
+        continue;
+      }
+    }
     // ---- assemble 2X in registers
     double2 X[D][D];
 #pragma unroll
     for (int r = 0; r < D; ++r)
 #pragma unroll
       for (int c = 0; c < D; ++c) X[r][c] = __ldg(&terms[r * D + c]);
-    for (int t = 1; t < T; ++t) {
-      const double w = slice_weight(job, s, t);
+    auto add_term = [&](int t, double w) {
       const double2* tt = terms + (size_t)t * D * D;
 #pragma unroll
       for (int r = 0; r < D; ++r)
@@ -360,6 +504,16 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
           X[r][c].x = fma(w, h.x, X[r][c].x);
           X[r][c].y = fma(w, h.y, X[r][c].y);
         }
+    };
+    if (rowpf) {
+#pragma unroll
+      for (int q = 0; q < RP; ++q) {
+        if (q >= job.n_ctrl) break;
+        check_amp(job, s, q, crow[q]);
+        add_term(q + 1, crow[q]);
+      }
+    } else {
+      for (int t = 1; t < T; ++t) add_term(t, slice_weight(job, s, t));
     }
 #pragma unroll
     for (int r = 0; r < D; ++r)
@@ -368,57 +522,118 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
         X[r][c].x *= job.xs;
         X[r][c].y *= job.xs;
       }
-    // ---- Clenshaw applied to V (chebyshev.py:298-303 with I -> V)
-    double2 cur[D][CPT], old[D][CPT];
-    {
-      const double ar = job.coef[2 * m], ai = job.coef[2 * m + 1];
-#pragma unroll
-      for (int r = 0; r < D; ++r)
-#pragma unroll
-        for (int cc = 0; cc < CPT; ++cc) {
-          cur[r][cc] = make_double2(ar * V[r][cc].x - ai * V[r][cc].y,
-                                    ar * V[r][cc].y + ai * V[r][cc].x);
-          old[r][cc] = make_double2(0.0, 0.0);
-        }
-    }
-    for (int jj = m - 1; jj >= 0; --jj) {
-      const double ar = job.coef[2 * jj], ai = job.coef[2 * jj + 1];
-      const double beta = (jj == 0) ? 2.0 : 1.0;
-      double2 nw[D][CPT];
-#pragma unroll
-      for (int r = 0; r < D; ++r)
-#pragma unroll
-        for (int cc = 0; cc < CPT; ++cc) {
-          double re = fma(ar, V[r][cc].x, fma(-ai, V[r][cc].y, -beta * old[r][cc].x));
-          double im = fma(ar, V[r][cc].y, fma(ai, V[r][cc].x, -beta * old[r][cc].y));
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            re = fma(X[r][k].x, cur[k][cc].x, re);
-            re = fma(-X[r][k].y, cur[k][cc].y, re);
-            im = fma(X[r][k].x, cur[k][cc].y, im);
-            im = fma(X[r][k].y, cur[k][cc].x, im);
-          }
-          nw[r][cc] = make_double2(re, im);
-        }
-#pragma unroll
-      for (int r = 0; r < D; ++r)
-#pragma unroll
-        for (int cc = 0; cc < CPT; ++cc) {
-          old[r][cc] = cur[r][cc];
-          cur[r][cc] = nw[r][cc];
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < D; ++r)
-#pragma unroll
-      for (int cc = 0; cc < CPT; ++cc) {
-        if (phase_one) {
-          V[r][cc] = cur[r][cc];
-        } else {
-          V[r][cc] = make_double2(job.phase[0] * cur[r][cc].x - job.phase[1] * cur[r][cc].y,
-                                  job.phase[0] * cur[r][cc].y + job.phase[1] * cur[r][cc].x);
-        }
+    if constexpr (D == 2) {
+      // 2 x 2: every polynomial in Z = 2X lies in span{I, Z'}, Z' = Z - z0 I,
+      // z0 = tr(Z)/2, Z'^2 = zeta2 I (Cayley-Hamilton, exact for any complex
+      // 2 x 2), so the reference's matrix Clenshaw recurrence
+      // (chebyshev.py:298-303) runs on coefficient pairs (a, b) = a I + b Z':
+      // Z (a, b) = (z0 a + zeta2 b, a + z0 b).  Same polynomial, a quarter of
+      // the work; U = a I + b Z' is formed once and applied to V.
+      auto cmul = [](double2 x, double2 y) {
+        return make_double2(fma(x.x, y.x, -x.y * y.y), fma(x.x, y.y, x.y * y.x));
+      };
+      const double2 z0 = make_double2(0.5 * (X[0][0].x + X[1][1].x),
+                                      0.5 * (X[0][0].y + X[1][1].y));
+      const double2 dz = make_double2(0.5 * (X[0][0].x - X[1][1].x),
+                                      0.5 * (X[0][0].y - X[1][1].y));
+      const double2 dd = cmul(dz, dz), od = cmul(X[0][1], X[1][0]);
+      const double2 zeta2 = make_double2(dd.x + od.x, dd.y + od.y);
+      double2 ca = make_double2(job.coef[2 * m], job.coef[2 * m + 1]);
+      double2 cb = make_double2(0.0, 0.0), oa = cb, ob = cb;
+      for (int jj = m - 1; jj >= 0; --jj) {
+        const double beta = (jj == 0) ? 2.0 : 1.0;
+        const double2 t1 = cmul(z0, ca), t2 = cmul(zeta2, cb), t3 = cmul(z0, cb);
+        const double2 na = make_double2(job.coef[2 * jj] + t1.x + t2.x - beta * oa.x,
+                                        job.coef[2 * jj + 1] + t1.y + t2.y - beta * oa.y);
+        const double2 nb = make_double2(ca.x + t3.x - beta * ob.x, ca.y + t3.y - beta * ob.y);
+        oa = ca;
+        ob = cb;
+        ca = na;
+        cb = nb;
       }
+      if (!phase_one) {
+        const double2 ph = make_double2(job.phase[0], job.phase[1]);
+        ca = cmul(ph, ca);
+        cb = cmul(ph, cb);
+      }
+      const double2 bd = cmul(cb, dz);
+      double2 U[2][2];
+      U[0][0] = make_double2(ca.x + bd.x, ca.y + bd.y);
+      U[1][1] = make_double2(ca.x - bd.x, ca.y - bd.y);
+      U[0][1] = cmul(cb, X[0][1]);
+      U[1][0] = cmul(cb, X[1][0]);
+      double2 nv[2][CPT];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            re = fma(U[r][k].x, V[k][cc].x, re);
+            re = fma(-U[r][k].y, V[k][cc].y, re);
+            im = fma(U[r][k].x, V[k][cc].y, im);
+            im = fma(U[r][k].y, V[k][cc].x, im);
+          }
+          nv[r][cc] = make_double2(re, im);
+        }
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) V[r][cc] = nv[r][cc];
+    } else {
+      // ---- Clenshaw applied to V (chebyshev.py:298-303 with I -> V)
+      double2 cur[D][CPT], old[D][CPT];
+      {
+        const double ar = job.coef[2 * m], ai = job.coef[2 * m + 1];
+  #pragma unroll
+        for (int r = 0; r < D; ++r)
+  #pragma unroll
+          for (int cc = 0; cc < CPT; ++cc) {
+            cur[r][cc] = make_double2(ar * V[r][cc].x - ai * V[r][cc].y,
+                                      ar * V[r][cc].y + ai * V[r][cc].x);
+            old[r][cc] = make_double2(0.0, 0.0);
+          }
+      }
+      for (int jj = m - 1; jj >= 0; --jj) {
+        const double ar = job.coef[2 * jj], ai = job.coef[2 * jj + 1];
+        const double beta = (jj == 0) ? 2.0 : 1.0;
+        double2 nw[D][CPT];
+  #pragma unroll
+        for (int r = 0; r < D; ++r)
+  #pragma unroll
+          for (int cc = 0; cc < CPT; ++cc) {
+            double re = fma(ar, V[r][cc].x, fma(-ai, V[r][cc].y, -beta * old[r][cc].x));
+            double im = fma(ar, V[r][cc].y, fma(ai, V[r][cc].x, -beta * old[r][cc].y));
+  #pragma unroll
+            for (int k = 0; k < D; ++k) {
+              re = fma(X[r][k].x, cur[k][cc].x, re);
+              re = fma(-X[r][k].y, cur[k][cc].y, re);
+              im = fma(X[r][k].x, cur[k][cc].y, im);
+              im = fma(X[r][k].y, cur[k][cc].x, im);
+            }
+            nw[r][cc] = make_double2(re, im);
+          }
+  #pragma unroll
+        for (int r = 0; r < D; ++r)
+  #pragma unroll
+          for (int cc = 0; cc < CPT; ++cc) {
+            old[r][cc] = cur[r][cc];
+            cur[r][cc] = nw[r][cc];
+          }
+      }
+  #pragma unroll
+      for (int r = 0; r < D; ++r)
+  #pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+          if (phase_one) {
+            V[r][cc] = cur[r][cc];
+          } else {
+            V[r][cc] = make_double2(job.phase[0] * cur[r][cc].x - job.phase[1] * cur[r][cc].y,
+                                    job.phase[0] * cur[r][cc].y + job.phase[1] * cur[r][cc].x);
+          }
+        }
+    }
     if (prefix_out) {
       double2* o = prefix_out + (size_t)s * D * D;
 #pragma unroll
@@ -438,6 +653,105 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
     }
     return;
   }
+  PH(0);
+  if constexpr (TPL == 1) {
+    // ---- one thread per lane (D = 2): ordered products by warp shuffles
+    // (lane i takes V_{i+k} V_i, k = 1, 2, 4, ...; lanes without slices
+    // hold I), then the CTA's 8 warp products by warp 0; the fused tail
+    // reduces the CTA products the same way, 256 at a time
+    __shared__ double2 wbuf[8][D * D];
+    __shared__ bool last2;
+    const int ln = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    auto load_id = [&](double2 (&M)[D][D]) {
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) M[r][c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    };
+    auto cta_product = [&](double2 (&M)[D][D]) {  // result in thread 0
+      warp_ordered_product<D>(M);
+      if (ln == 0)
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+          for (int c = 0; c < D; ++c) wbuf[wp][r * D + c] = M[r][c];
+      __syncthreads();
+      if (wp == 0) {
+        if (ln < 8) {
+#pragma unroll
+          for (int r = 0; r < D; ++r)
+#pragma unroll
+            for (int c = 0; c < D; ++c) M[r][c] = wbuf[ln][r * D + c];
+        } else {
+          load_id(M);
+        }
+        warp_ordered_product<D>(M, 8);
+      }
+      __syncthreads();  // wbuf reusable
+    };
+    double2 M[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) M[r][c] = V[r][c];
+    cta_product(M);
+    PH(1);
+    if (threadIdx.x == 0) {
+      double2* o = cta_out + (size_t)blockIdx.x * D * D;
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) o[r * D + c] = M[r][c];
+      if (tail.ctr != nullptr) {
+        __threadfence();
+        last2 = (atomicAdd(tail.ctr, 1u) == gridDim.x - 1);
+        if (last2) __threadfence();  // acquire side, ordered for the CTA by the barrier
+      }
+    }
+    if (tail.ctr == nullptr) {
+      PH_DONE
+      return;
+    }
+    __syncthreads();
+    PH(2);
+    if (!last2) {
+      PH_DONE
+      return;
+    }
+    // every thread folds a contiguous run of CTA products (later on the
+    // left), then one CTA-wide ordered product: a single pass for any grid
+    {
+      const int G = (int)gridDim.x, per = (G + 255) / 256;
+      const int i0 = min(G, (int)threadIdx.x * per), i1 = min(G, i0 + per);
+      load_id(M);
+      for (int i = i0; i < i1; ++i) {
+        double2 P[D][D], N[D][D];
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+          for (int c = 0; c < D; ++c) P[r][c] = __ldcg(&cta_out[(size_t)i * D * D + r * D + c]);
+        mat_mul<D>(P, M, N);
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+          for (int c = 0; c < D; ++c) M[r][c] = N[r][c];
+      }
+      cta_product(M);
+    }
+    if (threadIdx.x == 0) {
+      for (int e = 0; e < tail.d * tail.d; ++e) {
+        const double2 v = M[e / tail.d][e % tail.d];
+        if (tail.to_fp32)
+          reinterpret_cast<float2*>(tail.out)[e] = make_float2((float)v.x, (float)v.y);
+        else
+          reinterpret_cast<double2*>(tail.out)[e] = v;
+      }
+      *tail.ctr = 0;  // ready for the next launch
+    }
+    PH(3);
+    PH_DONE
+    return;
+  } else {
   // ---- in-CTA ordered pairwise tree over the CTA's consecutive lanes
   constexpr int LPB = 256 / TPL;  // lanes per block (blockDim = 256)
   __shared__ double2 buf[2][LPB * D * D];
@@ -463,20 +777,31 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
     cnt = pairs + (cnt & 1);
     src ^= 1;
   }
-  for (int e = threadIdx.x; e < D * D; e += blockDim.x)
-    cta_out[(size_t)blockIdx.x * D * D + e] = buf[src][e];
-  if (tail.ctr == nullptr) return;
+  PH(1);
+  if (tail.ctr == nullptr) {
+    for (int e = threadIdx.x; e < D * D; e += blockDim.x)
+      cta_out[(size_t)blockIdx.x * D * D + e] = buf[src][e];
+    PH_DONE
+    return;
+  }
 
   // ---- fused tail: the last CTA to finish multiplies the CTA products in
   // time order (chunks of LPB by the same smem tree, later chunks on the
-  // left) and writes the d x d result — the whole equiprop in one launch
+  // left) and writes the d x d result — the whole equiprop in one launch.
+  // One thread publishes the CTA product, fences and takes the ticket.
   __shared__ bool is_last;
   __shared__ double2 carry[D * D];
-  __threadfence();
+  if (threadIdx.x == 0) {
+    for (int e = 0; e < D * D; ++e) cta_out[(size_t)blockIdx.x * D * D + e] = buf[src][e];
+    __threadfence();
+    is_last = (atomicAdd(tail.ctr, 1u) == gridDim.x - 1);
+  }
   __syncthreads();
-  if (threadIdx.x == 0) is_last = (atomicAdd(tail.ctr, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!is_last) return;
+  PH(2);
+  if (!is_last) {
+    PH_DONE
+    return;
+  }
   __threadfence();
   for (int e = threadIdx.x; e < D * D; e += blockDim.x)
     carry[e] = make_double2((e / D) == (e % D) ? 1.0 : 0.0, 0.0);
@@ -515,6 +840,9 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
       reinterpret_cast<double2*>(tail.out)[e] = v;
   }
   if (threadIdx.x == 0) *tail.ctr = 0;  // ready for the next launch
+  PH(3);
+  PH_DONE
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -32,7 +32,13 @@ NAMES = ["T1 extract", "power GEMMs", "publish 2y", "gsync1+frags", "Clenshaw GE
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 nc = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 20000
-h0, hs, v, dt = random_inputs(d, nc, n, 1)
+if d == 0:  # the driven qubit (C1)
+    q = sp.DrivenQubit(1.0, 0.1, 1.0, 6.0)
+    sysm = q.system()
+    amp = q.amplitudes(n)
+    h0, hs, v, dt = sysm.drift, list(sysm.controls), amp.values, amp.dt
+else:
+    h0, hs, v, dt = random_inputs(d, nc, n, 1)
 ctx = sp.create()
 ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
 ctx.set_profiling(True)
@@ -48,6 +54,8 @@ tot = sum(buf[:10])
 if not tot:
     sys.exit(f"d={d}: no phase data (kernel {ctx.last_timing()['kernel']} is not instrumented)")
 print(f"d={d} N={nc} n={n}: kernel {t['main_kernel_ms']:.3f} ms ({t['kernel']})")
-for k, name in enumerate(NAMES if "ps3g" in t["kernel"] else NAMES_PS):
-    print(f"  {name:18s} {100.0 * buf[k] / tot:6.2f} %")
+NAMES_SMALL = ["lane loop", "CTA tree", "publish+ticket", "tail (last CTA)"] + ["-"] * 6
+names = NAMES if "ps3g" in t["kernel"] else NAMES_SMALL if "small" in t["kernel"] else NAMES_PS
+for k, name in enumerate(names):
+    print(f"  {name:18s} {100.0 * buf[k] / tot:6.2f} %  ({buf[k] / 1.965e3 / max(1, buf[15]):.2f} us per CTA of {buf[15]})")
 ctx.close()
