@@ -8,9 +8,9 @@ Headline workload (BASELINE.json configs[3], the largest single-GPU config):
 C4 = dim-128 random unit-1-norm system, 4 controls, 1e6 slices, midpoint,
 complex128, beta = 0.5 (m = 13), time-sharded over the N GPUs (strong
 scaling: 1e6 slices in total).  Secondary lines (same JSON, "per_dim"): C3
-(dim 32, 2 controls, 1e6 slices) and C1 (the paper's driven qubit, dim 2,
-1e5 slices).  A step is one full propagation U = U_{n-1} ... U_0 of the
-workload; value = slices / device time (CUDA events, max over ranks), with
+(dim 32, 2 controls, 1e6 slices), C1 (the paper's driven qubit, dim 2,
+1e5 slices) and c1m (the same qubit at the north star's 1e6 slices).
+A step is one full propagation U = U_{n-1} ... U_0 of the workload; value = slices / device time (CUDA events, max over ranks), with
 the amplitude table resident in HBM and L2 flushed between timed steps.
 e2e = the same through the public API with the table in page-locked host
 memory (H2D + kernels + gather + D2H inside the timed region, wall clock,
@@ -52,6 +52,9 @@ WORKLOADS = {
     "c1": dict(d=2, n_ctrl=2, slices=100_000, kind="qubit",
                label="C1: paper's driven qubit (w0=1, w1=0.1, wrf=1, T=6), dim 2, 2 controls, "
                      "1e5 slices, midpoint, complex128 (m=3)"),
+    "c1m": dict(d=2, n_ctrl=2, slices=1_000_000, kind="qubit",
+                label="north-star d=2 target: the driven qubit at 1e6 slices, midpoint, "
+                      "complex128 (m=3)"),
 }
 
 
@@ -373,7 +376,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
-    ap.add_argument("--secondary", default="c3,c1",
+    ap.add_argument("--secondary", default="c3,c1,c1m",
                     help="extra workloads reported under per_dim ('' for none)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")

@@ -144,3 +144,28 @@ def test_large_dims_against_oracle(d, n_ctrl, pts, mode, algo):
     assert res.slice_count == n
     assert rel_fro(res.u, ref) <= tol
     ctx.close()
+
+
+@pytest.mark.parametrize("pts", [1, 37, 5000, 200_000])
+@pytest.mark.parametrize("hermitian_exact", [True, False])
+def test_d2_paths_against_oracle(pts, hermitian_exact):
+    """d = 2 runs the reference's Clenshaw recurrence on Cayley-Hamilton
+    coefficient pairs: with real coefficients when every term is bitwise
+    Hermitian, complex ones otherwise (an asymmetry far inside the
+    reference's 1e-12 ingest tolerance).  Both against the oracle, from one
+    slice up to several slices per lane and the multi-CTA fused tail."""
+    import oracle
+    from cases import random_inputs
+    h0, hs, values, dt = random_inputs(2, 2, pts, 99 + pts)
+    if not hermitian_exact:
+        hs[0] = hs[0].copy()
+        hs[0][0, 1] += 1e-15
+    ref, _, _ = oracle.equiprop(h0, hs, values, dt, mode="midpoint")
+    ref_seq, _, _ = oracle.equiprop(h0, hs, values, dt, mode="midpoint", reduction="sequential")
+    tol, _ = parity_tolerance(ref, ref_seq, "fp64")
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+    amps = sp.ControlAmplitudes(values, dt)
+    assert rel_fro(ctx.equiprop(amps).u, ref) <= tol
+    assert rel_fro(ctx.equiprop(amps, reduction="sequential").u, ref) <= tol
+    ctx.close()
