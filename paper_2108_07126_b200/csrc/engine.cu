@@ -633,29 +633,63 @@ int reduce_pairwise_dev(sp_ctx* ctx, const double2* in, int cnt, int D, cudaStre
 
 // ---- family D8: one warp per lane, m8n8k4 DMMA (kernels_d8.cuh)
 constexpr int D8_WPC = 8;  // lanes (warps) per CTA
-constexpr size_t D8_SMEM = ((size_t)D8_WPC * D8_SLOT + 2 * 64 * D8_TSM) * sizeof(double);
+// 3 planes for the 3-multiplication form, 2 otherwise (3 CTAs/SM for the latter)
+constexpr size_t d8_smem(int alg) {
+  return ((size_t)D8_WPC * d8_slot(alg == D8_PS3 ? 3 : 2) + 2 * 64 * D8_TSM) * sizeof(double);
+}
+
+template <int ALG, int SC = 0, int RC = 0>
+int d8_prepare_one(sp_ctx* ctx) {
+  CUDA_TRY(ctx, cudaFuncSetAttribute(lane_d8_kernel<D8_WPC, ALG, SC, RC>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d8_smem(ALG)));
+  return SP_OK;
+}
 
 template <int ALG>
-int d8_prepare_one(sp_ctx* ctx) {
-  CUDA_TRY(ctx, cudaFuncSetAttribute(lane_d8_kernel<D8_WPC, ALG>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D8_SMEM));
-  return SP_OK;
+int d8_prepare_ps(sp_ctx* ctx) {
+  int rc = d8_prepare_one<ALG>(ctx);
+  if (!rc) rc = d8_prepare_one<ALG, 3, 5>(ctx);
+  if (!rc) rc = d8_prepare_one<ALG, 4, 4>(ctx);
+  if (!rc) rc = d8_prepare_one<ALG, 2, 4>(ctx);
+  return rc;
 }
 
 int d8_prepare(sp_ctx* ctx) {
   int rc = d8_prepare_one<D8_CLENSHAW>(ctx);
-  if (!rc) rc = d8_prepare_one<D8_PS>(ctx);
-  if (!rc) rc = d8_prepare_one<D8_PS3>(ctx);
+  if (!rc) rc = d8_prepare_ps<D8_PS>(ctx);
+  if (!rc) rc = d8_prepare_ps<D8_PS3>(ctx);
   return rc;
 }
 
-template <int ALG>
-int d8_lanes(sp_ctx* ctx, int64_t n) {
+// one launch of a D8 kernel variant: lanes = its resident capacity (one wave)
+template <int ALG, int SC = 0, int RC = 0>
+int d8_run(sp_ctx* ctx, const PSJob& pj, double2* prefix_out, cudaStream_t st, int* lanes_out) {
+  auto kern = lane_d8_kernel<D8_WPC, ALG, SC, RC>;
+  const size_t sm = d8_smem(ALG);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_d8_kernel<D8_WPC, ALG>, 32 * D8_WPC,
-                                                D8_SMEM);
-  if (occ < 1) occ = 1;
-  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->sms * occ * D8_WPC, n));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * D8_WPC, sm);
+  occ = std::max(occ, 1);
+  const int lanes = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)ctx->sms * occ * D8_WPC, pj.base.n_slices));
+  int rc = ensure(ctx, ctx->lanes, (size_t)lanes * 64 * sizeof(double2));
+  if (rc) return rc;
+  const int grid = (lanes + D8_WPC - 1) / D8_WPC;
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+  kern<<<grid, 32 * D8_WPC, sm, st>>>(pj, (const double2*)ctx->terms.p, lanes,
+                                      (double2*)ctx->lanes.p, prefix_out);
+  CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+  *lanes_out = lanes;
+  return SP_OK;
+}
+
+// PS forms: the (s, r) split compiled in where it is one of the common ones
+template <int ALG>
+int d8_run_ps(sp_ctx* ctx, const PSJob& pj, double2* prefix_out, cudaStream_t st, int* lanes) {
+  if (pj.s == 3 && pj.r == 5) return d8_run<ALG, 3, 5>(ctx, pj, prefix_out, st, lanes);
+  if (pj.s == 4 && pj.r == 4) return d8_run<ALG, 4, 4>(ctx, pj, prefix_out, st, lanes);
+  if (pj.s == 2 && pj.r == 4) return d8_run<ALG, 2, 4>(ctx, pj, prefix_out, st, lanes);
+  return d8_run<ALG>(ctx, pj, prefix_out, st, lanes);
 }
 
 int d8_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_t st,
@@ -672,31 +706,15 @@ int d8_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_
     pj.s = ps_s;
     ps_coefficients(job.coef, job.m, ps_s, pj.alpha, &pj.r);
   }
-  const int64_t n = job.n_slices;
-  const int lanes = alg == D8_CLENSHAW ? d8_lanes<D8_CLENSHAW>(ctx, n)
-                    : alg == D8_PS     ? d8_lanes<D8_PS>(ctx, n)
-                                       : d8_lanes<D8_PS3>(ctx, n);
-  int rc = ensure(ctx, ctx->lanes, (size_t)lanes * 64 * sizeof(double2));
+  int lanes = 0;
+  const int rc = alg == D8_CLENSHAW ? d8_run<D8_CLENSHAW>(ctx, pj, prefix_out, st, &lanes)
+                 : alg == D8_PS     ? d8_run_ps<D8_PS>(ctx, pj, prefix_out, st, &lanes)
+                                    : d8_run_ps<D8_PS3>(ctx, pj, prefix_out, st, &lanes);
   if (rc) return rc;
-  double2* lane_out = (double2*)ctx->lanes.p;
-  const double2* terms = (const double2*)ctx->terms.p;
-  const int grid = (lanes + D8_WPC - 1) / D8_WPC;
-  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-  if (alg == D8_CLENSHAW)
-    lane_d8_kernel<D8_WPC, D8_CLENSHAW><<<grid, 32 * D8_WPC, D8_SMEM, st>>>(pj, terms, lanes,
-                                                                          lane_out, prefix_out);
-  else if (alg == D8_PS)
-    lane_d8_kernel<D8_WPC, D8_PS><<<grid, 32 * D8_WPC, D8_SMEM, st>>>(pj, terms, lanes,
-                                                                    lane_out, prefix_out);
-  else
-    lane_d8_kernel<D8_WPC, D8_PS3><<<grid, 32 * D8_WPC, D8_SMEM, st>>>(pj, terms, lanes,
-                                                                     lane_out, prefix_out);
-  CUDA_TRY(ctx, cudaGetLastError());
-  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
   ++ctx->launches;
   ctx->last_algo = alg == D8_CLENSHAW ? ALGO_CLENSHAW : alg == D8_PS ? ALGO_PS : ALGO_PS3;
   ctx->last_gemms = ps_s == 0 ? job.m : ps_cost(job.m, ps_s);
-  *prods = lane_out;
+  *prods = (const double2*)ctx->lanes.p;
   *count = lanes;
   return SP_OK;
 }

@@ -21,7 +21,8 @@ namespace sp {
 
 enum D8Alg { D8_CLENSHAW = 0, D8_PS = 1, D8_PS3 = 2 };
 
-constexpr int D8_SLOT = 4 * 192 + 256;  // doubles per warp: XA, YA, B0, B1 (3 planes) + weights
+// doubles per warp: XA, YA, B0, B1 (np planes of 64) + 256 weights
+__host__ __device__ constexpr int d8_slot(int np) { return 4 * 64 * np + 256; }
 constexpr int D8_TSM = 16;              // expansion terms kept in shared memory (per CTA)
 
 // m8n8k4 fragment-native positions (0..63) of element (r, c)
@@ -68,7 +69,11 @@ __device__ __forceinline__ void d8_mma(const double* A, const double* B, double 
   }
 }
 
-template <int WPC, int ALG>
+// SC, RC > 0: the Paterson-Stockmeyer split (s, r) fixed at compile time
+// (m = 13 -> (3, 5), m = 15 -> (4, 4), m = 7 -> (2, 4)): every loop over the
+// powers and the Clenshaw steps unrolls, so coefficient loads, buffer
+// toggles and loop control become immediates; 0 = runtime (other orders)
+template <int WPC, int ALG, int SC = 0, int RC = 0>
 __global__ void __launch_bounds__(32 * WPC) lane_d8_kernel(PSJob pj,
                                                           const double2* __restrict__ terms,
                                                           int lanes,
@@ -80,11 +85,12 @@ __global__ void __launch_bounds__(32 * WPC) lane_d8_kernel(PSJob pj,
   const SliceJob& job = pj.base;
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
   const int lane = blockIdx.x * WPC + warp;
-  double* XA = smem + warp * D8_SLOT;  // 2X, later U (A-native)
-  double* YA = XA + 192;               // 2y (A-native)
-  auto Bb = [&](int i) { return XA + 384 + 192 * i; };  // B-native ping-pong
-  double* W = XA + 768;                // weights
-  double2* TS = reinterpret_cast<double2*>(smem + WPC * D8_SLOT);  // terms (T <= D8_TSM)
+  constexpr int PL = 64 * NP, SLOT = d8_slot(NP);
+  double* XA = smem + warp * SLOT;  // 2X, later U (A-native)
+  double* YA = XA + PL;             // 2y (A-native)
+  auto Bb = [&](int i) { return XA + 2 * PL + PL * i; };  // B-native ping-pong
+  double* W = XA + 4 * PL;          // weights
+  double2* TS = reinterpret_cast<double2*>(smem + WPC * SLOT);  // terms (T <= D8_TSM)
   const int g = ln >> 2, c0 = 2 * (ln & 3);
   const int bp[2] = {d8_bpos(g, c0), d8_bpos(g, c0 + 1)};
   const int ap[2] = {d8_apos(g, c0), d8_apos(g, c0 + 1)};
@@ -120,7 +126,7 @@ __global__ void __launch_bounds__(32 * WPC) lane_d8_kernel(PSJob pj,
   if (lane < lanes) lane_range(job.n_slices, lanes, lane, s0, s1);
   const int T = job.n_terms;
   const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
-  const int s = pj.s, r = pj.r, m = job.m;
+  const int s = SC > 0 ? SC : pj.s, r = RC > 0 ? RC : pj.r, m = job.m;
   // the CTA's warps share one shared-memory copy of the expansion terms
   const bool tsm = T <= D8_TSM;
   if (tsm)
@@ -261,6 +267,7 @@ __global__ void __launch_bounds__(32 * WPC) lane_d8_kernel(PSJob pj,
         int pc = 0;
         writeB(Bb(pc), b1r, b1i, (r - 1 == 1) ? 0.5 : 1.0);
         __syncwarp();
+#pragma unroll
         for (int j = r - 2; j >= 0; --j) {
           loadQ(j, accR, accI);
           if (j + 2 <= r - 1) {
