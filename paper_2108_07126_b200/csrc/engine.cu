@@ -459,6 +459,12 @@ int ps_prepare(sp_ctx* ctx) {
   CUDA_TRY(ctx, cudaFuncSetAttribute(ps_kernel<C, M3>(),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)C::SMEM));
+  if constexpr (!M3 && C::GPL == 1) {
+    CUDA_TRY(ctx, cudaFuncSetAttribute(lane_ps_kernel<C, 3, 5>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    CUDA_TRY(ctx, cudaFuncSetAttribute(lane_ps_kernel<C, 4, 4>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  }
   return SP_OK;
 }
 
@@ -508,8 +514,15 @@ int ps_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double
                                               dim3(C::THREADS), args, C::SMEM, st));
   } else {
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-    ps_kernel<C, M3>()<<<grid, C::THREADS, C::SMEM, st>>>(pj, terms, lanes, ga, ctr, tpriv,
-                                                          lane_out, prefix_out);
+    // smem-resident 4-product families: the (s, r) split of the common
+    // orders (m = 13 -> (3, 5), m = 15 -> (4, 4)) compiled in
+    auto kern = ps_kernel<C, M3>();
+    if constexpr (!M3 && C::GPL == 1) {
+      if (pj.s == 3 && pj.r == 5) kern = lane_ps_kernel<C, 3, 5>;
+      if (pj.s == 4 && pj.r == 4) kern = lane_ps_kernel<C, 4, 4>;
+    }
+    kern<<<grid, C::THREADS, C::SMEM, st>>>(pj, terms, lanes, ga, ctr, tpriv, lane_out,
+                                            prefix_out);
   }
   CUDA_TRY(ctx, cudaGetLastError());
   if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));

@@ -55,7 +55,9 @@ struct PSJob {
   double alpha[2 * PS_MAXC];  // alpha_{j,i} at (j*s + i), complex
 };
 
-template <class C>
+// SC, RC > 0: the (s, r) split fixed at compile time (as lane_d8_kernel):
+// the power / Clenshaw loops unroll and the power-block locations resolve
+template <class C, int SC = 0, int RC = 0>
 __global__ void __launch_bounds__(C::THREADS, 1)
     lane_ps_kernel(PSJob pj, const double* __restrict__ terms, int lanes,
                    double* __restrict__ gA, unsigned* __restrict__ gctr,
@@ -92,7 +94,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int ms0 = (wil % (C::S / MT)) * MT;
   const int nt0 = (wil / (C::S / MT)) * NT;
   const int col0 = cb * WC;
-  const int s = pj.s, r = pj.r;
+  const int s = SC > 0 ? SC : pj.s, r = RC > 0 ? RC : pj.r;
+  constexpr int UNR = SC > 0 ? 8 : 1;
   // private column blocks of T_1..T_{s-1}, acc-native, coalesced per thread:
   // blocks < TSB in shared memory, the rest in global memory
   auto tp_load = [&](int kk, int e) -> double2 {
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       qr[e] = diag ? a0r : 0.0;
       qi[e] = diag ? a0i : 0.0;
     }
+#pragma unroll UNR
     for (int i = 1; i < s; ++i) {
       const double ar = pj.alpha[2 * (j * s + i)], ai = pj.alpha[2 * (j * s + i) + 1];
 #pragma unroll
@@ -261,6 +265,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     PH(1);
     // ---- 3. powers T_k = 2X T_{k-1} - T_{k-2}, k = 2..s
     int pb = 0;
+#pragma unroll UNR
     for (int k = 2; k <= s; ++k) {
       if (k == 2) {
 #pragma unroll
@@ -301,6 +306,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       int pc = 0;
       write_B(bo(pc), qr, qi, (r - 1 == 1) ? 0.5 : 1.0);
       lane_sync<C>();
+#pragma unroll UNR
       for (int j = r - 2; j >= 0; --j) {
         load_Q(j, accR, accI);
         if (j + 2 <= r - 1) {

@@ -59,3 +59,6 @@ if len(sys.argv) > 1 and sys.argv[1] == "d8":
     for d in (5, 8):
         for a in ("auto", "clenshaw", "ps", "ps3m"):
             run(f"d{d} rand 1e6 {a}", *random_inputs(d, 2, 1000000, 1), algo=a)
+if len(sys.argv) > 1 and sys.argv[1] == "magnus":
+    run("d128 magnus 2e3", *random_inputs(128, 4, 4001, 1), mode="magnus")
+    run("d32 magnus 2e4", *random_inputs(32, 2, 40001, 1), mode="magnus")
