@@ -32,7 +32,6 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
     "-Xptxas", "-v",
-    "--split-compile", "0",  # parallel optimizer/ptxas over the kernel instantiations
 ]
 
 

@@ -464,6 +464,8 @@ int ps_prepare(sp_ctx* ctx) {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     CUDA_TRY(ctx, cudaFuncSetAttribute(lane_ps_kernel<C, 4, 4>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    CUDA_TRY(ctx, cudaFuncSetAttribute(lane_ps_kernel<C, 2, 4>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   }
   return SP_OK;
 }
@@ -515,11 +517,13 @@ int ps_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double
   } else {
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
     // smem-resident 4-product families: the (s, r) split of the common
-    // orders (m = 13 -> (3, 5), m = 15 -> (4, 4)) compiled in
+    // orders (m = 13 -> (3, 5), m = 15 -> (4, 4), fp32 m = 7 -> (2, 4))
+    // compiled in
     auto kern = ps_kernel<C, M3>();
     if constexpr (!M3 && C::GPL == 1) {
       if (pj.s == 3 && pj.r == 5) kern = lane_ps_kernel<C, 3, 5>;
       if (pj.s == 4 && pj.r == 4) kern = lane_ps_kernel<C, 4, 4>;
+      if (pj.s == 2 && pj.r == 4) kern = lane_ps_kernel<C, 2, 4>;
     }
     kern<<<grid, C::THREADS, C::SMEM, st>>>(pj, terms, lanes, ga, ctr, tpriv, lane_out,
                                             prefix_out);

@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
   // loaded into registers a slice ahead instead
   const int64_t rows_per_slice = job.mode == SP_MODE_MIDPOINT ? 1 : 2;
   constexpr int RP = 4;
-  const bool rowpf = job.mode == SP_MODE_MIDPOINT && job.n_ctrl <= RP;
+  const bool rowpf = D == 2 && job.mode == SP_MODE_MIDPOINT && job.n_ctrl <= RP;
   double nrow[RP];
   auto load_row = [&](int64_t sl) {
     const double* a = job.amps + sl * job.n_ctrl;
