@@ -777,12 +777,26 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
       tail.out = fused_out;
     }
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-    if (ctx->fam == FAM_S2)
-      lane_small_kernel<2, 1><<<blocks, 256, 0, st>>>(job, (const double2*)ctx->terms.p, lanes,
-                                                      lane_out, cta_out, prefix_out, tail);
+    const double2* tp = (const double2*)ctx->terms.p;
+    if (ctx->fam == FAM_S2) {
+      // the common series orders compiled in (qubit fine steps 3, fp32 7,
+      // beta = 0.5 fp64 13, magnus 15)
+      switch (job.m) {
+        case 3: lane_small_kernel<2, 1, 3><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
+                                                                   cta_out, prefix_out, tail); break;
+        case 7: lane_small_kernel<2, 1, 7><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
+                                                                   cta_out, prefix_out, tail); break;
+        case 13: lane_small_kernel<2, 1, 13><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
+                                                                     cta_out, prefix_out, tail); break;
+        case 15: lane_small_kernel<2, 1, 15><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
+                                                                     cta_out, prefix_out, tail); break;
+        default: lane_small_kernel<2, 1><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
+                                                                 cta_out, prefix_out, tail);
+      }
+    }
     else
-      lane_small_kernel<4, 4><<<blocks, 256, 0, st>>>(job, (const double2*)ctx->terms.p, lanes,
-                                                      lane_out, cta_out, prefix_out, tail);
+      lane_small_kernel<4, 4><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out, cta_out,
+                                                      prefix_out, tail);
     CUDA_TRY(ctx, cudaGetLastError());
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
     ++ctx->launches;
@@ -1123,6 +1137,12 @@ int sp_phase_prof(unsigned long long* out) {
     return 1;
   unsigned long long z[16] = {0};
   return cudaMemcpyToSymbol(sp::g_phase, z, sizeof(z)) != cudaSuccess;
+}
+int sp_timeline(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, sp::g_tl, 4096 * sizeof(unsigned long long)) != cudaSuccess)
+    return 1;
+  static unsigned long long z[4096];
+  return cudaMemcpyToSymbol(sp::g_tl, z, sizeof(z)) != cudaSuccess;
 }
 #endif
 

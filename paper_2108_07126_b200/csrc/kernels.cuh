@@ -350,7 +350,10 @@ __device__ __forceinline__ void warp_ordered_product(double2 (&M)[D][D], int wid
   }
 }
 
-template <int D, int TPL>
+// MC > 0: the series order m compiled in (the common orders 3, 7, 13, 15):
+// the Clenshaw loop unrolls and the plan coefficients become constant-bank
+// operands; 0 = runtime m
+template <int D, int TPL, int MC = 0>
 // (register budget for 3 CTAs/SM at D = 2 and 2 at D = 4: the lane loop is
 // latency bound and needs the resident warps)
 __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJob job,
@@ -372,7 +375,8 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
   int64_t s0 = 0, s1 = 0;
   if (lane < lanes) lane_range(job.n_slices, lanes, lane, s0, s1);
   const int T = job.n_terms;
-  const int m = job.m;
+  const int m = MC > 0 ? MC : job.m;
+  constexpr int MUNR = MC > 0 ? MC : 1;
   const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
 
   // the amplitude rows a few slices ahead are prefetched into L1 (no
@@ -437,7 +441,9 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
         const double zeta2 = fma(dz, dz, fma(zc.x, zc.x, zc.y * zc.y));
         double2 ca = make_double2(job.coef[2 * m], job.coef[2 * m + 1]);
         double2 cb = make_double2(0.0, 0.0), oa = cb, ob = cb;
-        for (int jj = m - 1; jj >= 0; --jj) {
+#pragma unroll MUNR
+  #pragma unroll MUNR
+      for (int jj = m - 1; jj >= 0; --jj) {
           const double beta = (jj == 0) ? 2.0 : 1.0;
           const double2 na =
               make_double2(job.coef[2 * jj] + fma(z0, ca.x, fma(zeta2, cb.x, -beta * oa.x)),
@@ -540,6 +546,7 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
       const double2 zeta2 = make_double2(dd.x + od.x, dd.y + od.y);
       double2 ca = make_double2(job.coef[2 * m], job.coef[2 * m + 1]);
       double2 cb = make_double2(0.0, 0.0), oa = cb, ob = cb;
+#pragma unroll MUNR
       for (int jj = m - 1; jj >= 0; --jj) {
         const double beta = (jj == 0) ? 2.0 : 1.0;
         const double2 t1 = cmul(z0, ca), t2 = cmul(zeta2, cb), t3 = cmul(z0, cb);
@@ -595,6 +602,7 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
             old[r][cc] = make_double2(0.0, 0.0);
           }
       }
+#pragma unroll MUNR
       for (int jj = m - 1; jj >= 0; --jj) {
         const double ar = job.coef[2 * jj], ai = job.coef[2 * jj + 1];
         const double beta = (jj == 0) ? 2.0 : 1.0;

@@ -46,9 +46,12 @@ amps = sp.ControlAmplitudes(v, dt)
 ctx.equiprop(amps)
 lib = sp._native.lib
 buf = (ctypes.c_ulonglong * 16)()
+tl = (ctypes.c_ulonglong * 4096)()
 lib.sp_phase_prof(buf)
+lib.sp_timeline(tl)
 ctx.equiprop(amps)
 lib.sp_phase_prof(buf)
+lib.sp_timeline(tl)
 t = ctx.last_timing()
 tot = sum(buf[:10])
 if not tot:
@@ -59,3 +62,13 @@ names = NAMES if "ps3g" in t["kernel"] else NAMES_SMALL if "small" in t["kernel"
 for k, name in enumerate(names):
     print(f"  {name:18s} {100.0 * buf[k] / tot:6.2f} %  ({buf[k] / 1.965e3 / max(1, buf[15]):.2f} us per CTA of {buf[15]})")
 ctx.close()
+
+st = [tl[2 * i] for i in range(2048) if tl[2 * i]]
+en = [tl[2 * i + 1] for i in range(2048) if tl[2 * i]]
+if st:
+    t0 = min(st)
+    ss, ee = sorted(x - t0 for x in st), sorted(x - t0 for x in en)
+    q = lambda v, f: v[min(len(v) - 1, int(f * len(v)))] / 1e3
+    print(f"  CTA timeline over {len(st)} CTAs (us from the first start): start p50 {q(ss, .5):.2f} "
+          f"p90 {q(ss, .9):.2f} max {ss[-1] / 1e3:.2f}; end min {ee[0] / 1e3:.2f} p50 {q(ee, .5):.2f} "
+          f"p90 {q(ee, .9):.2f} max {ee[-1] / 1e3:.2f}")
