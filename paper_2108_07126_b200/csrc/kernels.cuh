@@ -442,8 +442,7 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
         double2 ca = make_double2(job.coef[2 * m], job.coef[2 * m + 1]);
         double2 cb = make_double2(0.0, 0.0), oa = cb, ob = cb;
 #pragma unroll MUNR
-  #pragma unroll MUNR
-      for (int jj = m - 1; jj >= 0; --jj) {
+        for (int jj = m - 1; jj >= 0; --jj) {
           const double beta = (jj == 0) ? 2.0 : 1.0;
           const double2 na =
               make_double2(job.coef[2 * jj] + fma(z0, ca.x, fma(zeta2, cb.x, -beta * oa.x)),
