@@ -169,3 +169,28 @@ def test_d2_paths_against_oracle(pts, hermitian_exact):
     assert rel_fro(ctx.equiprop(amps).u, ref) <= tol
     assert rel_fro(ctx.equiprop(amps, reduction="sequential").u, ref) <= tol
     ctx.close()
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 6, 8, 12, 24, 40, 96])
+@pytest.mark.parametrize("mode", ["midpoint", "magnus"])
+def test_cumulative_every_family_against_oracle(d, mode):
+    """equiprop_all for every kernel family (plain-layout d <= 8, DMMA
+    prefix application above) against the oracle's cumulative stack, and the
+    reference property u_all[-1] == sequential total, bit for bit
+    (propagator.py:304-306, 310-316)."""
+    import oracle
+    from cases import random_inputs
+    h0, hs, values, dt = random_inputs(d, 2, 41, 7000 + d)
+    ref_all, _, _ = oracle.equiprop_all(h0, hs, values, dt, mode=mode)
+    ref, _, _ = oracle.equiprop(h0, hs, values, dt, mode=mode)
+    ref_seq, _, _ = oracle.equiprop(h0, hs, values, dt, mode=mode, reduction="sequential")
+    tol, _ = parity_tolerance(ref, ref_seq, "fp64")
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus")
+    amps = sp.ControlAmplitudes(values, dt)
+    cum = ctx.equiprop_all(amps)
+    assert cum.u_all.shape == ref_all.shape
+    for k in range(ref_all.shape[0]):
+        assert rel_fro(cum.u_all[k], ref_all[k]) <= tol, k
+    assert np.array_equal(cum.final, ctx.equiprop(amps, reduction="sequential").u)
+    ctx.close()
