@@ -111,6 +111,11 @@ int sp_equiprop_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctr
  * propagator.py:310-331).  u_all_out holds slices x d x d (host). */
 int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
                     const sp_plan* plan, void* u_all_out);
+/* same, device-resident (d_u_all_out: slices x d x d on the device, output
+ * dtype), stream-ordered and asynchronous; the caller owns amplitude
+ * validation (sp_amplitude_violation).  HBM-write-bound path. */
+int sp_equiprop_all_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
+                           double dt, const sp_plan* plan, void* d_u_all_out, void* stream);
 /* ordered product mats[count-1] ... mats[0] of device-resident complex128
  * d x d matrices (the multi-GPU gather step; pairwise =
  * reduce_pairwise propagator.py:68-102, sequential = left fold) */

@@ -61,6 +61,8 @@ HEADER_SYMBOLS = {
                                       _c.POINTER(SpPlan), _c.c_int, _P, _P]),
     "sp_equiprop_all": (_c.c_int, [_P, _P, _c.c_int64, _c.c_int, _c.c_double,
                                    _c.POINTER(SpPlan), _P]),
+    "sp_equiprop_all_device": (_c.c_int, [_P, _P, _c.c_int64, _c.c_int, _c.c_double,
+                                          _c.POINTER(SpPlan), _P, _P]),
     "sp_product_device": (_c.c_int, [_P, _c.c_int, _P, _c.c_int, _P, _P]),
     "sp_slice_count": (_c.c_int, [_P, _c.c_int64, _c.POINTER(_c.c_int64)]),
     "sp_amplitude_violation": (_c.c_int, [_P, _c.POINTER(_c.c_int64)]),

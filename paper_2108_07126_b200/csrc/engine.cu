@@ -202,7 +202,7 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   int fam = FAM_NONE, D = 0;
   DevBuf terms, amps, lanes, ctab, tree0, tree1, xglob, gctr, result, out, cumP, cumE, cumO,
-      fold_scratch, psA, tpriv, viol, terms3, tailctr, seqA;
+      fold_scratch, psA, tpriv, viol, terms3, tailctr, seqA, scanEin, scanG, scanEG, lstarts;
   cudaStream_t viol_stream = nullptr;
   int64_t viol_pts = 0;
   int algo = 0;          // Algo
@@ -749,7 +749,8 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     const int tpl = (ctx->fam == FAM_S2) ? 1 : 4;
     // pairwise: at least 4 slices per lane (short CTA tree and tail for the
     // latency-bound small n), at most one full wave of resident threads (no
-    // second partial wave); sequential / cumulative: 1024 lanes for the fold
+    // second partial wave); sequential / cumulative: at least 16 slices per
+    // lane (the two-level scan of the lane products)
     int occ = 0;
     if (ctx->fam == FAM_S2)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_small_kernel<2, 1>, 256, 0);
@@ -758,7 +759,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     occ = std::max(occ, 1);
     int64_t cap = (int64_t)ctx->sms * occ * 256 / tpl;
     int64_t want = cta_reduce ? std::max<int64_t>((int64_t)ctx->sms * 256 / tpl, (n + 3) / 4)
-                              : 1024;
+                              : std::max<int64_t>(1024, (n + 15) / 16);
     lanes = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(cap, want), n));
     const int blocks = (int)(((int64_t)lanes * tpl + 255) / 256);
     int rc = ensure(ctx, ctx->lanes, (size_t)(cta_reduce ? blocks : lanes) * dd * sizeof(double2));
@@ -1000,6 +1001,42 @@ double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
   return (double)n * (f * D * D * D * ctx->last_gemms + 4.0 * D * D * ctx->n_terms);
 }
 
+// exclusive prefixes E[l] of cnt plain-layout lane products (into cumE) and
+// the total M[cnt-1] E[cnt-1] (into result) by the two-level scan of
+// kernels.cuh (group_fold_kernel / fold_kernel / combine_prefix_kernel)
+int plain_scan(sp_ctx* ctx, const double2* prods, int cnt, cudaStream_t st) {
+  const int D = ctx->D;
+  const size_t dd = (size_t)D * D;
+  int GS = (int)std::ceil(std::sqrt((double)cnt));
+  GS = std::max(1, GS);
+  const int G = (cnt + GS - 1) / GS;
+  int rc = ensure(ctx, ctx->cumE, (size_t)cnt * dd * sizeof(double2));
+  if (!rc) rc = ensure(ctx, ctx->scanEin, (size_t)cnt * dd * sizeof(double2));
+  if (!rc) rc = ensure(ctx, ctx->scanG, (size_t)G * dd * sizeof(double2));
+  if (!rc) rc = ensure(ctx, ctx->scanEG, (size_t)G * dd * sizeof(double2));
+  if (!rc) rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
+  if (!rc) rc = ensure(ctx, ctx->result, dd * sizeof(double2));
+  if (rc) return rc;
+  group_fold_kernel<<<G, 64, 0, st>>>(prods, cnt, D, GS, (double2*)ctx->scanEin.p,
+                                      (double2*)ctx->scanG.p);
+  CUDA_TRY(ctx, cudaGetLastError());
+  // group totals: exclusive prefixes EG (the total of all groups is unused)
+  fold_kernel<<<1, 1024, 0, st>>>((const double2*)ctx->scanG.p, G, D,
+                                   (double2*)ctx->fold_scratch.p, (double2*)ctx->scanEG.p,
+                                   (double2*)ctx->result.p);
+  CUDA_TRY(ctx, cudaGetLastError());
+  combine_prefix_kernel<<<grid_for((int64_t)cnt * dd, 256), 256, 0, st>>>(
+      (const double2*)ctx->scanEin.p, (const double2*)ctx->scanEG.p, cnt, D, GS,
+      (double2*)ctx->cumE.p);
+  CUDA_TRY(ctx, cudaGetLastError());
+  lane_total_kernel<<<1, 64, 0, st>>>(prods + (size_t)(cnt - 1) * dd,
+                                      (const double2*)ctx->cumE.p + (size_t)(cnt - 1) * dd, D,
+                                      (double2*)ctx->result.p);
+  CUDA_TRY(ctx, cudaGetLastError());
+  ctx->launches += 4;
+  return SP_OK;
+}
+
 // total propagator on the device -> d x d in d_out (output dtype)
 int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double dt,
                  const sp_plan* plan, int reduction, void* d_out, cudaStream_t st) {
@@ -1060,12 +1097,9 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
       rc = reduce_pairwise_dev(ctx, prods, cnt, D, st, &total);
       if (rc) return rc;
     } else {
-      rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
+      // plain-layout families: the scan equiprop_all uses (bitwise-equal last entry)
+      rc = plain_scan(ctx, prods, cnt, st);
       if (rc) return rc;
-      fold_kernel<<<1, 1024, 0, st>>>(prods, cnt, D, (double2*)ctx->fold_scratch.p, nullptr,
-                                       (double2*)ctx->result.p);
-      CUDA_TRY(ctx, cudaGetLastError());
-      ++ctx->launches;
       total = (const double2*)ctx->result.p;
     }
   }
@@ -1117,6 +1151,63 @@ int product_dev(sp_ctx* ctx, int count, const double2* d_mats, int reduction, vo
                                                                 ctx->bits == 32, d_out);
   CUDA_TRY(ctx, cudaGetLastError());
   ++ctx->launches;
+  return SP_OK;
+}
+
+// cumulative propagators on the device: slices x d x d (output dtype) in d_out
+int equiprop_all_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double dt,
+                     const sp_plan* plan, void* d_out, cudaStream_t st) {
+  ctx->launches = 0;
+  ctx->ev_pending = false;
+  SliceJob job;
+  int rc = build_job(ctx, d_amps, pts, n_ctrl, dt, plan, &job);
+  if (rc) return rc;
+  rc = arm_validation(ctx, &job, st);
+  if (rc) return rc;
+  const int64_t n = job.n_slices;
+  if (n == 0) return SP_OK;
+  const int D = ctx->D, d = ctx->dim;
+  const size_t dd = (size_t)D * D;
+  rc = ensure(ctx, ctx->cumP, (size_t)n * dd * sizeof(double2));
+  if (rc) return rc;
+  const double2* prods = nullptr;
+  int cnt = 0;
+  rc = run_lanes(ctx, job, false, (double2*)ctx->cumP.p, st, &prods, &cnt);
+  if (rc) return rc;
+  ctx->ev_pending = ctx->prof;
+  ctx->kname = family_kernel_name(ctx->fam, ctx->last_algo);
+  ctx->flops = executed_flops(ctx, n, job.m);
+  if (plain_family(ctx->fam)) {
+    rc = plain_scan(ctx, prods, cnt, st);
+    if (rc) return rc;
+  } else {
+    rc = ensure(ctx, ctx->cumE, (size_t)cnt * dd * sizeof(double2));
+    if (rc) return rc;
+    rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
+    if (rc) return rc;
+    rc = ensure(ctx, ctx->result, dd * sizeof(double2));
+    if (rc) return rc;
+    fold_kernel<<<1, 1024, 0, st>>>(prods, cnt, D, (double2*)ctx->fold_scratch.p,
+                                     (double2*)ctx->cumE.p, (double2*)ctx->result.p);
+    CUDA_TRY(ctx, cudaGetLastError());
+    ctx->launches += 1;
+  }
+  if (plain_family(ctx->fam)) {
+    rc = ensure(ctx, ctx->lstarts, (size_t)(cnt + 1) * sizeof(int64_t));
+    if (rc) return rc;
+    lane_starts_kernel<<<grid_for(cnt + 1, 256), 256, 0, st>>>(n, cnt, (int64_t*)ctx->lstarts.p);
+    CUDA_TRY(ctx, cudaGetLastError());
+    apply_prefix_kernel<<<grid_for(n * d * d, 256), 256, 0, st>>>(
+        (const double2*)ctx->cumP.p, (const double2*)ctx->cumE.p,
+        (const int64_t*)ctx->lstarts.p, n, cnt, D, d, ctx->bits == 32, d_out);
+    CUDA_TRY(ctx, cudaGetLastError());
+    ctx->launches += 2;
+  } else {
+    // tensor-core prefix application straight into the output dtype
+    rc = tc_apply(ctx, (const double*)ctx->cumP.p, (const double2*)ctx->cumE.p, n, cnt, d_out,
+                  st);
+    if (rc) return rc;
+  }
   return SP_OK;
 }
 
@@ -1192,7 +1283,7 @@ int sp_free(sp_ctx* ctx) {
                       &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
                       &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch,
                       &ctx->psA,   &ctx->tpriv, &ctx->viol, &ctx->terms3, &ctx->tailctr,
-                      &ctx->seqA};
+                      &ctx->seqA, &ctx->scanEin, &ctx->scanG, &ctx->scanEG, &ctx->lstarts};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1299,64 +1390,38 @@ int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, do
   rc = prepare_device(ctx);
   if (rc) return rc;
   cudaStream_t st = ctx->stream;
-  ctx->launches = 0;
-  ctx->ev_pending = false;
   const size_t abytes = (size_t)pts * n_ctrl * sizeof(double);
   rc = ensure(ctx, ctx->amps, abytes);
   if (rc) return rc;
   if (abytes)
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->amps.p, amps, abytes, cudaMemcpyHostToDevice, st));
-  SliceJob job;
-  rc = build_job(ctx, (const double*)ctx->amps.p, pts, n_ctrl, dt, plan, &job);
-  if (rc) return rc;
-  rc = arm_validation(ctx, &job, st);
-  if (rc) return rc;
-  const int64_t n = job.n_slices;
-  if (n == 0) return SP_OK;
-  const int D = ctx->D, d = ctx->dim;
-  const size_t dd = (size_t)D * D;
-  rc = ensure(ctx, ctx->cumP, (size_t)n * dd * sizeof(double2));
-  if (rc) return rc;
-  const double2* prods = nullptr;
-  int cnt = 0;
-  rc = run_lanes(ctx, job, false, (double2*)ctx->cumP.p, st, &prods, &cnt);
-  if (rc) return rc;
-  ctx->ev_pending = ctx->prof;
-  ctx->kname = family_kernel_name(ctx->fam, ctx->last_algo);
-  ctx->flops = executed_flops(ctx, n, job.m);
-  rc = ensure(ctx, ctx->cumE, (size_t)cnt * dd * sizeof(double2));
-  if (rc) return rc;
-  rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
-  if (rc) return rc;
-  rc = ensure(ctx, ctx->result, dd * sizeof(double2));
-  if (rc) return rc;
-  fold_kernel<<<1, 1024, 0, st>>>(prods, cnt, D, (double2*)ctx->fold_scratch.p,
-                                   (double2*)ctx->cumE.p, (double2*)ctx->result.p);
-  CUDA_TRY(ctx, cudaGetLastError());
-  const size_t obytes = (size_t)n * d * d * (ctx->bits == 32 ? 8 : 16);
-  rc = ensure(ctx, ctx->out, obytes);
-  if (rc) return rc;
-  ctx->launches += 1;
-  if (plain_family(ctx->fam)) {
-    rc = ensure(ctx, ctx->cumO, (size_t)n * dd * sizeof(double2));
-    if (rc) return rc;
-    apply_prefix_kernel<<<grid_for((int64_t)n * dd, 256), 256, 0, st>>>(
-        (const double2*)ctx->cumP.p, (const double2*)ctx->cumE.p, n, cnt, D,
-        (double2*)ctx->cumO.p);
-    CUDA_TRY(ctx, cudaGetLastError());
-    extract_kernel<<<grid_for((int64_t)n * d * d, 256), 256, 0, st>>>(
-        (const double2*)ctx->cumO.p, n, D, d, ctx->bits == 32, ctx->out.p);
-    CUDA_TRY(ctx, cudaGetLastError());
-    ctx->launches += 2;
-  } else {
-    // tensor-core prefix application straight into the output dtype
-    rc = tc_apply(ctx, (const double*)ctx->cumP.p, (const double2*)ctx->cumE.p, n, cnt,
-                  ctx->out.p, st);
+  int64_t n = 0;
+  int code = 0;
+  n = slice_count_for(ctx->mode, pts, &code);
+  if (code == 0 && n > 0) {
+    const size_t obytes = (size_t)n * ctx->dim * ctx->dim * (ctx->bits == 32 ? 8 : 16);
+    rc = ensure(ctx, ctx->out, obytes);
     if (rc) return rc;
   }
-  CUDA_TRY(ctx, cudaMemcpyAsync(u_all_out, ctx->out.p, obytes, cudaMemcpyDeviceToHost, st));
+  rc = equiprop_all_dev(ctx, (const double*)ctx->amps.p, pts, n_ctrl, dt, plan, ctx->out.p, st);
+  if (rc) return rc;
+  if (n > 0) {
+    const size_t obytes = (size_t)n * ctx->dim * ctx->dim * (ctx->bits == 32 ? 8 : 16);
+    CUDA_TRY(ctx, cudaMemcpyAsync(u_all_out, ctx->out.p, obytes, cudaMemcpyDeviceToHost, st));
+  }
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   return read_violation(ctx, amps, nullptr);
+}
+
+int sp_equiprop_all_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
+                           double dt, const sp_plan* plan, void* d_u_all_out, void* stream) {
+  int rc = check_loaded(ctx);
+  if (rc) return rc;
+  if (pts < 0) return fail(ctx, SP_E_SHAPE, "negative sample count");
+  rc = prepare_device(ctx);
+  if (rc) return rc;
+  return equiprop_all_dev(ctx, d_amps, pts, n_ctrl, dt, plan, d_u_all_out,
+                          (cudaStream_t)stream);
 }
 
 int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction, void* d_out,

@@ -976,20 +976,87 @@ __global__ void fold_kernel(const double2* __restrict__ mats, int cnt, int D,
   }
 }
 
-// cumulative products: out[s] = P[s] E[lane(s)] with P[s] the in-lane prefix
-__global__ void apply_prefix_kernel(const double2* __restrict__ P, const double2* __restrict__ E,
-                                    int64_t n, int lanes, int D, double2* __restrict__ out) {
-  const int64_t dd = (int64_t)D * D;
-  const int64_t total = n * dd;
+// Two-level exclusive scan of many lane products (plain-layout families,
+// d <= 8, where thousands of lanes keep the lane pass busy):
+//  group_fold_kernel: block b folds lanes [b GS, (b+1) GS) in order, writing
+//    the in-group exclusive prefixes Ein[l] and the group total Gt[b];
+//  fold_kernel over Gt gives the exclusive group prefixes EG[b];
+//  combine_prefix_kernel: E[l] = Ein[l] EG[l / GS];
+//  lane_total_kernel: total = M[L-1] E[L-1].
+// The sequential reduction and equiprop_all share these steps, so the last
+// cumulative entry P_last E[L-1] equals the sequential total bit for bit.
+__global__ void group_fold_kernel(const double2* __restrict__ mats, int cnt, int D, int GS,
+                                  double2* __restrict__ Ein, double2* __restrict__ Gt) {
+  __shared__ double2 acc[2][64];
+  const int dd = D * D, b = blockIdx.x;
+  const int l0 = b * GS, l1 = min(cnt, l0 + GS);
+  for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+    acc[0][e] = make_double2((e / D) == (e % D) ? 1.0 : 0.0, 0.0);
+    Ein[(size_t)l0 * dd + e] = acc[0][e];
+  }
+  __syncthreads();
+  int cur = 0;
+  for (int l = l0; l < l1; ++l) {
+    const double2* Ml = mats + (size_t)l * dd;
+    for (int e = threadIdx.x; e < dd; e += blockDim.x)
+      acc[cur ^ 1][e] = cdot(Ml + (size_t)(e / D) * D, acc[cur], D, e % D, D);
+    __syncthreads();
+    cur ^= 1;
+    for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+      if (l + 1 < l1) Ein[(size_t)(l + 1) * dd + e] = acc[cur][e];
+      else Gt[(size_t)b * dd + e] = acc[cur][e];
+    }
+  }
+}
+
+__global__ void combine_prefix_kernel(const double2* __restrict__ Ein,
+                                      const double2* __restrict__ EG, int cnt, int D, int GS,
+                                      double2* __restrict__ E) {
+  const int64_t dd = (int64_t)D * D, total = (int64_t)cnt * dd;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = e / dd;
-    const int rc = (int)(e % dd), r = rc / D, c = rc % D;
-    // lane of slice s under lane_range(): largest l with l*n/lanes <= s
-    int64_t l = ((s + 1) * lanes - 1) / n;
-    while (l > 0 && l * n / lanes > s) --l;
-    while (l + 1 < lanes && (l + 1) * n / lanes <= s) ++l;
-    out[e] = cdot(P + s * dd + (int64_t)r * D, E + l * dd, D, c, D);
+    const int64_t l = e / dd;
+    const int rc = (int)(e % dd);
+    E[e] = cdot(Ein + l * dd + (int64_t)(rc / D) * D, EG + (l / GS) * dd, D, rc % D, D);
+  }
+}
+
+__global__ void lane_total_kernel(const double2* __restrict__ M, const double2* __restrict__ E,
+                                  int D, double2* __restrict__ out) {
+  const int dd = D * D;
+  for (int e = threadIdx.x; e < dd; e += blockDim.x)
+    out[e] = cdot(M + (e / D) * D, E, D, e % D, D);
+}
+
+// first slice of every lane under lane_range() (lanes + 1 entries)
+__global__ void lane_starts_kernel(int64_t n, int lanes, int64_t* __restrict__ starts) {
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l <= lanes; l += gridDim.x * blockDim.x)
+    starts[l] = (int64_t)l * n / lanes;
+}
+
+// cumulative products: out[s] = P[s] E[lane(s)] with P[s] the in-lane prefix,
+// written straight into the (n, d, d) output in the output dtype, one element
+// per thread (plain-layout families, D <= 8); the lane of slice s comes from a
+// floating-point estimate checked against the lane start table (no 64-bit
+// division per element)
+__global__ void apply_prefix_kernel(const double2* __restrict__ P, const double2* __restrict__ E,
+                                    const int64_t* __restrict__ starts, int64_t n, int lanes,
+                                    int D, int d, int to_fp32, void* __restrict__ out) {
+  const int64_t dd = (int64_t)D * D, od = (int64_t)d * d;
+  const double ratio = (double)lanes / (double)n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * od;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = e / od;
+    const int rc = (int)(e - s * od), r = rc / d, c = rc - r * d;
+    int64_t l = (int64_t)((double)s * ratio);
+    if (l >= lanes) l = lanes - 1;
+    while (l > 0 && starts[l] > s) --l;
+    while (l + 1 < lanes && starts[l + 1] <= s) ++l;
+    const double2 v = cdot(P + s * dd + (int64_t)r * D, E + l * dd, D, c, D);
+    if (to_fp32)
+      reinterpret_cast<float2*>(out)[e] = make_float2((float)v.x, (float)v.y);
+    else
+      reinterpret_cast<double2*>(out)[e] = v;
   }
 }
 

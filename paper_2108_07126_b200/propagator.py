@@ -352,6 +352,25 @@ class IntegratorContext:
                                      ctypes.c_void_p(stream)), self._handle)
         return {"slice_count": count, "plan": plan.summary()}
 
+    def equiprop_all_device_ptr(self, amps_ptr: int, pts: int, n_ctrl: int, dt: float,
+                                out_ptr: int, stream: int = 0,
+                                plan: ChebyshevPlan | None = None) -> dict:
+        """Asynchronous cumulative propagators of a device-resident (pts,
+        n_ctrl) float64 table into a device (slices, d, d) array (working
+        dtype).  The caller owns amplitude validation."""
+        self._require_loaded()
+        if n_ctrl != self._system.n_controls:
+            raise ShapeError(f"amplitude table has {n_ctrl} controls, "
+                             f"system has {self._system.n_controls}")
+        count = self.slice_count(pts) if pts else 0
+        plan = plan or self.plan_for(dt)
+        native = plan.to_native()
+        check(lib.sp_equiprop_all_device(self._handle, ctypes.c_void_p(amps_ptr), int(pts),
+                                         int(n_ctrl), float(dt), ctypes.byref(native),
+                                         ctypes.c_void_p(out_ptr), ctypes.c_void_p(stream)),
+              self._handle)
+        return {"slice_count": count, "plan": plan.summary()}
+
     def product_device_ptr(self, count: int, mats_ptr: int, out_ptr: int, stream: int = 0,
                            reduction: str = "pairwise") -> None:
         """Ordered product mats[count-1] ... mats[0] of device complex128 d x d

@@ -215,3 +215,26 @@ def test_binding_session_and_errors():
         assert ei.value.code == "amplitude-bound"
         cum = s.equiprop(np.zeros((4, 1)), 0.1, cumulative=True)
         assert cum.shape == (4, 2, 2)
+
+
+@pytest.mark.parametrize("d", [2, 8, 32])
+def test_equiprop_all_device_matches_host(d, rng):
+    """sp_equiprop_all_device (device-resident table and output, caller's
+    stream) returns exactly the host entry's cumulative stack."""
+    import torch
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(random_hermitian(rng, d, 1.0),
+                                         [random_hermitian(rng, d, 1.0)] * 2))
+    values = rng.uniform(-1.0, 1.0, (300, 2))
+    amps = sp.ControlAmplitudes(values, 0.05)
+    host = ctx.equiprop_all(amps).u_all
+    dev = torch.device("cuda", 0)
+    d_amps = torch.from_numpy(np.ascontiguousarray(values)).to(dev)
+    out = torch.empty((300, d, d), dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    info = ctx.equiprop_all_device_ptr(d_amps.data_ptr(), 300, 2, 0.05, out.data_ptr(),
+                                       stream=stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    assert info["slice_count"] == 300
+    assert np.array_equal(out.cpu().numpy(), host)
+    ctx.close()
