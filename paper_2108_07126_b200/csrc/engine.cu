@@ -202,7 +202,7 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   int fam = FAM_NONE, D = 0;
   DevBuf terms, amps, lanes, ctab, tree0, tree1, xglob, gctr, result, out, cumP, cumE, cumO,
-      fold_scratch, psA, tpriv, viol, terms3, tailctr, seqA, scanEin, scanG, scanEG, lstarts;
+      fold_scratch, psA, tpriv, viol, terms3, tailctr, seqA, scanEin, lstarts;
   cudaStream_t viol_stream = nullptr;
   int64_t viol_pts = 0;
   int algo = 0;          // Algo
@@ -1004,36 +1004,73 @@ double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
 // exclusive prefixes E[l] of cnt plain-layout lane products (into cumE) and
 // the total M[cnt-1] E[cnt-1] (into result) by the two-level scan of
 // kernels.cuh (group_fold_kernel / fold_kernel / combine_prefix_kernel)
+// recursive exclusive scan: E[l] = M[l-1] ... M[0] for cnt lane products,
+// groups of SCAN_GS folded in order (one thread per group for D = 2, one CTA
+// per group otherwise), the group totals scanned recursively, then
+// E[l] = Ein[l] EG[l / SCAN_GS].  Scratch: the arena in ctx->scanEin.
+constexpr int SCAN_GS = 32;
+
+size_t scan_arena_elems(int cnt, size_t dd) {
+  size_t total = 0;
+  while (cnt > SCAN_GS) {
+    const int G = (cnt + SCAN_GS - 1) / SCAN_GS;
+    total += ((size_t)cnt + 2 * (size_t)G) * dd;  // Ein, group totals, their prefixes
+    cnt = G;
+  }
+  return total + dd;
+}
+
+int scan_rec(sp_ctx* ctx, const double2* M, int cnt, double2* E, double2* arena,
+             cudaStream_t st) {
+  const int D = ctx->D;
+  const size_t dd = (size_t)D * D;
+  if (cnt <= SCAN_GS) {  // one group
+    if (D == 2) {
+      group_fold_reg_kernel<2><<<1, 32, 0, st>>>(M, cnt, cnt, E, nullptr);
+    } else {
+      group_fold_kernel<<<1, 64, 0, st>>>(M, cnt, D, cnt, E, arena);
+    }
+    CUDA_TRY(ctx, cudaGetLastError());
+    ++ctx->launches;
+    return SP_OK;
+  }
+  const int G = (cnt + SCAN_GS - 1) / SCAN_GS;
+  double2* Ein = arena;
+  double2* Gt = Ein + (size_t)cnt * dd;
+  double2* EG = Gt + (size_t)G * dd;
+  double2* rest = EG + (size_t)G * dd;
+  if (D == 2)
+    group_fold_reg_kernel<2><<<(G + 127) / 128, 128, 0, st>>>(M, cnt, SCAN_GS, Ein, Gt);
+  else
+    group_fold_kernel<<<G, 64, 0, st>>>(M, cnt, D, SCAN_GS, Ein, Gt);
+  CUDA_TRY(ctx, cudaGetLastError());
+  int rc = scan_rec(ctx, Gt, G, EG, rest, st);
+  if (rc) return rc;
+  combine_prefix_kernel<<<grid_for((int64_t)cnt * dd, 256), 256, 0, st>>>(Ein, EG, cnt, D,
+                                                                          SCAN_GS, E);
+  CUDA_TRY(ctx, cudaGetLastError());
+  ctx->launches += 2;
+  return SP_OK;
+}
+
+// exclusive prefixes E[l] of cnt plain-layout lane products (into cumE) and
+// the total M[cnt-1] E[cnt-1] (into result); equiprop(sequential) and
+// equiprop_all share it, so the last cumulative entry equals the sequential
+// total bit for bit
 int plain_scan(sp_ctx* ctx, const double2* prods, int cnt, cudaStream_t st) {
   const int D = ctx->D;
   const size_t dd = (size_t)D * D;
-  int GS = (int)std::ceil(std::sqrt((double)cnt));
-  GS = std::max(1, GS);
-  const int G = (cnt + GS - 1) / GS;
   int rc = ensure(ctx, ctx->cumE, (size_t)cnt * dd * sizeof(double2));
-  if (!rc) rc = ensure(ctx, ctx->scanEin, (size_t)cnt * dd * sizeof(double2));
-  if (!rc) rc = ensure(ctx, ctx->scanG, (size_t)G * dd * sizeof(double2));
-  if (!rc) rc = ensure(ctx, ctx->scanEG, (size_t)G * dd * sizeof(double2));
-  if (!rc) rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
+  if (!rc) rc = ensure(ctx, ctx->scanEin, scan_arena_elems(cnt, dd) * sizeof(double2));
   if (!rc) rc = ensure(ctx, ctx->result, dd * sizeof(double2));
   if (rc) return rc;
-  group_fold_kernel<<<G, 64, 0, st>>>(prods, cnt, D, GS, (double2*)ctx->scanEin.p,
-                                      (double2*)ctx->scanG.p);
-  CUDA_TRY(ctx, cudaGetLastError());
-  // group totals: exclusive prefixes EG (the total of all groups is unused)
-  fold_kernel<<<1, 1024, 0, st>>>((const double2*)ctx->scanG.p, G, D,
-                                   (double2*)ctx->fold_scratch.p, (double2*)ctx->scanEG.p,
-                                   (double2*)ctx->result.p);
-  CUDA_TRY(ctx, cudaGetLastError());
-  combine_prefix_kernel<<<grid_for((int64_t)cnt * dd, 256), 256, 0, st>>>(
-      (const double2*)ctx->scanEin.p, (const double2*)ctx->scanEG.p, cnt, D, GS,
-      (double2*)ctx->cumE.p);
-  CUDA_TRY(ctx, cudaGetLastError());
+  rc = scan_rec(ctx, prods, cnt, (double2*)ctx->cumE.p, (double2*)ctx->scanEin.p, st);
+  if (rc) return rc;
   lane_total_kernel<<<1, 64, 0, st>>>(prods + (size_t)(cnt - 1) * dd,
                                       (const double2*)ctx->cumE.p + (size_t)(cnt - 1) * dd, D,
                                       (double2*)ctx->result.p);
   CUDA_TRY(ctx, cudaGetLastError());
-  ctx->launches += 4;
+  ++ctx->launches;
   return SP_OK;
 }
 
@@ -1283,7 +1320,7 @@ int sp_free(sp_ctx* ctx) {
                       &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
                       &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch,
                       &ctx->psA,   &ctx->tpriv, &ctx->viol, &ctx->terms3, &ctx->tailctr,
-                      &ctx->seqA, &ctx->scanEin, &ctx->scanG, &ctx->scanEG, &ctx->lstarts};
+                      &ctx->seqA, &ctx->scanEin, &ctx->lstarts};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);

@@ -1009,6 +1009,72 @@ __global__ void group_fold_kernel(const double2* __restrict__ mats, int cnt, int
   }
 }
 
+// the same group fold with one thread per group and the running product in
+// registers (D <= 4: a short dependent chain per step, no barriers); the
+// exclusive group prefixes use it too (one group spanning all totals)
+template <int D>
+__global__ void group_fold_reg_kernel(const double2* __restrict__ mats, int cnt, int GS,
+                                      double2* __restrict__ Ein, double2* __restrict__ Gt) {
+  constexpr int dd = D * D;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l0 = b * GS, l1 = min(cnt, l0 + GS);
+  if (l0 >= cnt) return;
+  double2 acc[D][D];
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[r][c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  // chunks of 8 lane products: all 8 loads in flight, then 8 dependent steps
+  constexpr int CH = 8;
+  for (int lb = l0; lb < l1; lb += CH) {
+    double2 M[CH][D][D];
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      if (lb + j < l1) {
+        const double2* Ml = mats + (size_t)(lb + j) * dd;
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+          for (int c = 0; c < D; ++c) M[j][r][c] = __ldcg(&Ml[r * D + c]);
+      }
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      if (lb + j >= l1) break;
+      double2* o = Ein + (size_t)(lb + j) * dd;
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) o[r * D + c] = acc[r][c];
+      // acc <- M acc, each entry with the cdot summation order
+      double2 N[D][D];
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            re = fma(M[j][r][k].x, acc[k][c].x, re);
+            re = fma(-M[j][r][k].y, acc[k][c].y, re);
+            im = fma(M[j][r][k].x, acc[k][c].y, im);
+            im = fma(M[j][r][k].y, acc[k][c].x, im);
+          }
+          N[r][c] = make_double2(re, im);
+        }
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc[r][c] = N[r][c];
+    }
+  }
+  if (Gt != nullptr) {
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) Gt[(size_t)b * dd + r * D + c] = acc[r][c];
+  }
+}
+
 __global__ void combine_prefix_kernel(const double2* __restrict__ Ein,
                                       const double2* __restrict__ EG, int cnt, int D, int GS,
                                       double2* __restrict__ E) {
