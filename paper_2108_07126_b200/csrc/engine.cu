@@ -782,18 +782,22 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     if (ctx->fam == FAM_S2) {
       // the common series orders compiled in (qubit fine steps 3, fp32 7,
       // beta = 0.5 fp64 13, magnus 15)
+      // and, for two controls in midpoint mode (the driven qubit), the
+      // control count of the fast path
+      const bool two = job.n_ctrl == 2 && job.mode == SP_MODE_MIDPOINT;
+#define SP_S2(MCV)                                                                          \
+  (two ? lane_small_kernel<2, 1, MCV, 2><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,  \
+                                                                 cta_out, prefix_out, tail) \
+       : lane_small_kernel<2, 1, MCV><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,     \
+                                                              cta_out, prefix_out, tail))
       switch (job.m) {
-        case 3: lane_small_kernel<2, 1, 3><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
-                                                                   cta_out, prefix_out, tail); break;
-        case 7: lane_small_kernel<2, 1, 7><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
-                                                                   cta_out, prefix_out, tail); break;
-        case 13: lane_small_kernel<2, 1, 13><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
-                                                                     cta_out, prefix_out, tail); break;
-        case 15: lane_small_kernel<2, 1, 15><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
-                                                                     cta_out, prefix_out, tail); break;
-        default: lane_small_kernel<2, 1><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,
-                                                                 cta_out, prefix_out, tail);
+        case 3: SP_S2(3); break;
+        case 7: SP_S2(7); break;
+        case 13: SP_S2(13); break;
+        case 15: SP_S2(15); break;
+        default: SP_S2(0);
       }
+#undef SP_S2
     }
     else
       lane_small_kernel<4, 4><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out, cta_out,

@@ -38,9 +38,19 @@ namespace sp {
 // per-phase SM clock totals of thread 0 of every CTA (tools/phase_prof.py;
 // instrumented builds only)
 __device__ unsigned long long g_phase[16];
-#define PH_INIT long long ph_t = clock64(); unsigned long long ph_acc[10] = {0};
+// and per-CTA (start, end << 8 | smid) %globaltimer stamps of the first 2048 CTAs
+__device__ unsigned long long g_tl[4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PH_INIT long long ph_t = clock64(); unsigned long long ph_acc[10] = {0}; \
+  const unsigned long long ph_g0 = gtimer();
 #define PH(k) do { const long long t_ = clock64(); ph_acc[k] += t_ - ph_t; ph_t = t_; } while (0)
-#define PH_DONE if (threadIdx.x == 0) { for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]); atomicAdd(&g_phase[15], 1ull); }
+#define PH_DONE if (threadIdx.x == 0) { for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]); atomicAdd(&g_phase[15], 1ull); \
+  if (blockIdx.x < 2048) { unsigned sm_; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_)); \
+    g_tl[2 * blockIdx.x] = ph_g0; g_tl[2 * blockIdx.x + 1] = ((gtimer() - ph_g0) << 8) | (sm_ & 0xff); } }
 #else
 #define PH_INIT
 #define PH(k) do {} while (0)
@@ -353,7 +363,7 @@ __device__ __forceinline__ void warp_ordered_product(double2 (&M)[D][D], int wid
 // MC > 0: the series order m compiled in (the common orders 3, 7, 13, 15):
 // the Clenshaw loop unrolls and the plan coefficients become constant-bank
 // operands; 0 = runtime m
-template <int D, int TPL, int MC = 0>
+template <int D, int TPL, int MC = 0, int NCC = 0>
 // (register budget for 3 CTAs/SM at D = 2 and 2 at D = 4: the lane loop is
 // latency bound and needs the resident warps)
 __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJob job,
@@ -414,6 +424,98 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
       }
   }
   PH_INIT
+  if constexpr (D == 2 && NCC > 0) {
+    // the driven-qubit fast path with the control count compiled in: one
+    // vector load per row (prefetched a slice ahead through a running
+    // pointer), a 32-bit slice counter
+    if (fast2 && job.n_ctrl == NCC) {
+      const int cnt = (int)(s1 - s0);
+      const double* arow = job.amps + s0 * NCC;
+      double rn[NCC], rc[NCC];
+      auto ldrow = [&](const double* a) {
+        if constexpr (NCC == 2) {
+          const double2 v = *reinterpret_cast<const double2*>(a);
+          rn[0] = v.x;
+          rn[1] = v.y;
+        } else {
+#pragma unroll
+          for (int q = 0; q < NCC; ++q) rn[q] = a[q];
+        }
+      };
+      if (cnt > 0) ldrow(arow);
+      for (int k = 0; k < cnt; ++k) {
+#pragma unroll
+        for (int q = 0; q < NCC; ++q) rc[q] = rn[q];
+        arow += NCC;
+        if (k + 1 < cnt) ldrow(arow);
+        const int64_t s = s0 + k;
+        double z0 = tA[0], dz = tB[0];
+        double2 zc = tC[0];
+#pragma unroll
+        for (int q = 0; q < NCC; ++q) {
+          const double w = rc[q];
+          check_amp(job, s, q, w);
+          z0 = fma(w, tA[q + 1], z0);
+          dz = fma(w, tB[q + 1], dz);
+          zc.x = fma(w, tC[q + 1].x, zc.x);
+          zc.y = fma(w, tC[q + 1].y, zc.y);
+        }
+        const double zeta2 = fma(dz, dz, fma(zc.x, zc.x, zc.y * zc.y));
+        double2 ca = make_double2(job.coef[2 * m], job.coef[2 * m + 1]);
+        double2 cb = make_double2(0.0, 0.0), oa = cb, ob = cb;
+#pragma unroll MUNR
+        for (int jj = m - 1; jj >= 0; --jj) {
+          const double beta = (jj == 0) ? 2.0 : 1.0;
+          const double2 na =
+              make_double2(job.coef[2 * jj] + fma(z0, ca.x, fma(zeta2, cb.x, -beta * oa.x)),
+                           job.coef[2 * jj + 1] + fma(z0, ca.y, fma(zeta2, cb.y, -beta * oa.y)));
+          const double2 nb = make_double2(ca.x + fma(z0, cb.x, -beta * ob.x),
+                                          ca.y + fma(z0, cb.y, -beta * ob.y));
+          oa = ca;
+          ob = cb;
+          ca = na;
+          cb = nb;
+        }
+        if (!phase_one) {
+          const double pr = job.phase[0], pi = job.phase[1];
+          ca = make_double2(pr * ca.x - pi * ca.y, pr * ca.y + pi * ca.x);
+          cb = make_double2(pr * cb.x - pi * cb.y, pr * cb.y + pi * cb.x);
+        }
+        double2 U[2][2];
+        U[0][0] = make_double2(fma(cb.x, dz, ca.x), fma(cb.y, dz, ca.y));
+        U[1][1] = make_double2(fma(-cb.x, dz, ca.x), fma(-cb.y, dz, ca.y));
+        U[0][1] = make_double2(cb.x * zc.x - cb.y * zc.y, cb.x * zc.y + cb.y * zc.x);
+        U[1][0] = make_double2(cb.x * zc.x + cb.y * zc.y, cb.y * zc.x - cb.x * zc.y);
+        double2 nv[2][CPT];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int cc = 0; cc < CPT; ++cc) {
+            double re = U[r][0].x * V[0][cc].x;
+            re = fma(-U[r][0].y, V[0][cc].y, re);
+            re = fma(U[r][1].x, V[1][cc].x, re);
+            re = fma(-U[r][1].y, V[1][cc].y, re);
+            double im = U[r][0].x * V[0][cc].y;
+            im = fma(U[r][0].y, V[0][cc].x, im);
+            im = fma(U[r][1].x, V[1][cc].y, im);
+            im = fma(U[r][1].y, V[1][cc].x, im);
+            nv[r][cc] = make_double2(re, im);
+          }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int cc = 0; cc < CPT; ++cc) V[r][cc] = nv[r][cc];
+        if (prefix_out) {
+          double2* o = prefix_out + (size_t)s * D * D;
+#pragma unroll
+          for (int r = 0; r < D; ++r)
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) o[r * D + c0 + cc] = V[r][cc];
+        }
+      }
+      s0 = s1;  // done: the general loop below has nothing left
+    }
+  }
   for (int64_t s = s0; s < s1; ++s) {
     double crow[RP];
 #pragma unroll

@@ -64,7 +64,8 @@ for k, name in enumerate(names):
 ctx.close()
 
 st = [tl[2 * i] for i in range(2048) if tl[2 * i]]
-en = [tl[2 * i + 1] for i in range(2048) if tl[2 * i]]
+en = [tl[2 * i] + (tl[2 * i + 1] >> 8) for i in range(2048) if tl[2 * i]]
+sm = [tl[2 * i + 1] & 0xff for i in range(2048) if tl[2 * i]]
 if st:
     t0 = min(st)
     ss, ee = sorted(x - t0 for x in st), sorted(x - t0 for x in en)
@@ -72,3 +73,8 @@ if st:
     print(f"  CTA timeline over {len(st)} CTAs (us from the first start): start p50 {q(ss, .5):.2f} "
           f"p90 {q(ss, .9):.2f} max {ss[-1] / 1e3:.2f}; end min {ee[0] / 1e3:.2f} p50 {q(ee, .5):.2f} "
           f"p90 {q(ee, .9):.2f} max {ee[-1] / 1e3:.2f}")
+    if len(sys.argv) > 4:
+        per = {}
+        for x, e in zip(sm, en):
+            per[x] = max(per.get(x, 0), e - t0)
+        print("  last CTA end per SM (us): " + " ".join(f"{k}:{per[k] / 1e3:.1f}" for k in sorted(per)))
