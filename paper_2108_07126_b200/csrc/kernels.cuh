@@ -812,9 +812,14 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
 #pragma unroll
         for (int c = 0; c < D; ++c) o[r * D + c] = M[r][c];
       if (tail.ctr != nullptr) {
-        __threadfence();
-        last2 = (atomicAdd(tail.ctr, 1u) == gridDim.x - 1);
-        if (last2) __threadfence();  // acquire side, ordered for the CTA by the barrier
+        // one acq_rel RMW: releases this thread's CTA product, acquires the
+        // others' for the last arriver (the CTA barrier below extends it)
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                     : "=r"(old)
+                     : "l"(tail.ctr)
+                     : "memory");
+        last2 = (old == gridDim.x - 1);
       }
     }
     if (tail.ctr == nullptr) {
