@@ -99,6 +99,37 @@ def apply(u, state) -> np.ndarray:
         f"nor a density matrix ({d}, {d})")
 
 
+def reduce_pairwise(batch, backend=None, scratch=None) -> np.ndarray:
+    """Time-ordered product U[n-1] ... U[0] of a propagator batch on the
+    device (``propagator.py:68-102``): the reference's level-order fold, later
+    slices on the left, odd leftovers carried forward; an empty batch gives
+    the identity.  ``batch`` is a reference-style batch (anything with a
+    ``matrices()`` view) or an (n, d, d) array; the result keeps its complex
+    dtype.  ``backend`` and ``scratch`` are accepted for signature
+    compatibility (the device owns its scratch)."""
+    import torch
+
+    u = batch.matrices() if hasattr(batch, "matrices") else np.asarray(batch)
+    if u.ndim != 3 or u.shape[1] != u.shape[2]:
+        raise ShapeError(f"expected (n, d, d) matrices, got shape {u.shape}")
+    n, d = u.shape[0], u.shape[1]
+    out_dtype = np.complex64 if u.dtype == np.complex64 else np.complex128
+    if n == 0:
+        return np.eye(d, dtype=out_dtype)
+    ctx = create("fp32" if out_dtype == np.complex64 else "fp64")
+    try:
+        ctx.set_hamiltonian(ControlSystem(np.zeros((d, d), dtype=np.complex128)))
+        dev = torch.device("cuda", ctx.device)
+        mats = torch.from_numpy(np.ascontiguousarray(u, dtype=np.complex128)).to(dev)
+        res = torch.empty((d, d), dtype=torch.complex64 if out_dtype == np.complex64
+                          else torch.complex128, device=dev)
+        stream = torch.cuda.current_stream(dev)
+        ctx.product_device_ptr(n, mats.data_ptr(), res.data_ptr(), stream=stream.cuda_stream)
+        return res.cpu().numpy()
+    finally:
+        ctx.close()
+
+
 class IntegratorContext:
     """Stateful propagation session bound to one B200 (``propagator.py:132-331``).
 

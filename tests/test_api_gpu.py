@@ -238,3 +238,23 @@ def test_equiprop_all_device_matches_host(d, rng):
     assert info["slice_count"] == 300
     assert np.array_equal(out.cpu().numpy(), host)
     ctx.close()
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 5, 33, 64])
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_reduce_pairwise_matches_reference_order(n, dtype, rng):
+    """Module-level reduce_pairwise (propagator.py:68-102) on the device
+    against the reference's level-order fold restated by the oracle; the
+    empty batch is the identity."""
+    import oracle
+    d = 3
+    u = np.stack([haar_unitary(rng, d) for _ in range(n)]).astype(dtype) if n else \
+        np.zeros((0, d, d), dtype=dtype)
+    got = sp.reduce_pairwise(u)
+    assert got.dtype == dtype and got.shape == (d, d)
+    if n == 0:
+        assert np.array_equal(got, np.eye(d, dtype=dtype))
+        return
+    ref = oracle.reduce_pairwise(u.astype(np.complex128))
+    tol = 1e-13 if dtype == np.complex128 else 1e-5
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= tol
