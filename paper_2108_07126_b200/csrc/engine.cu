@@ -577,33 +577,34 @@ int tc_apply(sp_ctx* ctx, const double* P, const double2* E, int64_t n, int lane
   return fail(ctx, SP_E_INTERNAL, "no tensor-core apply for this family");
 }
 
-template <int D>
-__global__ void chunk_reduce_kernel(const double2* __restrict__ in, int cnt,
+// one CTA folds a chunk of CH consecutive products by the level-order smem
+// tree (later on the left, odd leftovers carried): log2(CH) levels per launch
+__global__ void chunk_reduce_kernel(const double2* __restrict__ in, int cnt, int D, int CH,
                                     double2* __restrict__ out) {
-  constexpr int CH = (D == 2) ? 256 : 64;
-  __shared__ double2 buf[2][CH * D * D];
+  extern __shared__ double2 cbuf[];
+  const int dd = D * D;
+  double2* buf[2] = {cbuf, cbuf + (size_t)CH * dd};
   const int base = blockIdx.x * CH;
   const int here = min(CH, cnt - base);
-  for (int e = threadIdx.x; e < here * D * D; e += blockDim.x)
-    buf[0][e] = in[(size_t)base * D * D + e];
+  for (int e = threadIdx.x; e < here * dd; e += blockDim.x)
+    buf[0][e] = in[(size_t)base * dd + e];
   __syncthreads();
   int c = here, src = 0;
   while (c > 1) {
     const int pairs = c >> 1;
-    for (int e = threadIdx.x; e < pairs * D * D; e += blockDim.x) {
-      const int p = e / (D * D), rc = e % (D * D), r = rc / D, cc = rc % D;
-      buf[src ^ 1][p * D * D + rc] =
-          cdot(&buf[src][(2 * p + 1) * D * D + r * D], &buf[src][(2 * p) * D * D], D, cc, D);
+    for (int e = threadIdx.x; e < pairs * dd; e += blockDim.x) {
+      const int p = e / dd, rc = e % dd, r = rc / D, cc = rc % D;
+      buf[src ^ 1][p * dd + rc] =
+          cdot(&buf[src][(2 * p + 1) * dd + r * D], &buf[src][(2 * p) * dd], D, cc, D);
     }
     if (c & 1)
-      for (int e = threadIdx.x; e < D * D; e += blockDim.x)
-        buf[src ^ 1][pairs * D * D + e] = buf[src][(c - 1) * D * D + e];
+      for (int e = threadIdx.x; e < dd; e += blockDim.x)
+        buf[src ^ 1][pairs * dd + e] = buf[src][(c - 1) * dd + e];
     __syncthreads();
     c = pairs + (c & 1);
     src ^= 1;
   }
-  for (int e = threadIdx.x; e < D * D; e += blockDim.x)
-    out[(size_t)blockIdx.x * D * D + e] = buf[src][e];
+  for (int e = threadIdx.x; e < dd; e += blockDim.x) out[(size_t)blockIdx.x * dd + e] = buf[src][e];
 }
 
 // pairwise tree over cnt matrices (in place ping-pong); returns the buffer
@@ -625,13 +626,16 @@ int reduce_pairwise_dev(sp_ctx* ctx, const double2* in, int cnt, int D, cudaStre
   while (cnt > 1) {
     const int nxt = cnt / 2 + (cnt & 1);
     double2* dst = (double2*)bufs[which]->p;
-    if (D <= 4 && cnt > 2) {
-      const int ch = (D == 2) ? 256 : 64;
+    // chunks of CH products per CTA (smem budget 96 KB: D <= 32) cut the
+    // launches of a deep tree to log_CH(cnt); larger D: one level per launch
+    const int ch = std::min(256, 98304 / (int)(dd * 2 * sizeof(double2)));
+    if (ch >= 3 && cnt > 2) {
       const int blocks = (cnt + ch - 1) / ch;
-      if (D == 2)
-        chunk_reduce_kernel<2><<<blocks, 256, 0, st>>>(src, cnt, dst);
-      else
-        chunk_reduce_kernel<4><<<blocks, 256, 0, st>>>(src, cnt, dst);
+      const size_t sm = (size_t)2 * ch * dd * sizeof(double2);
+      if (sm > 48 * 1024)
+        CUDA_TRY(ctx, cudaFuncSetAttribute(chunk_reduce_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      chunk_reduce_kernel<<<blocks, 256, sm, st>>>(src, cnt, D, ch, dst);
       CUDA_TRY(ctx, cudaGetLastError());
       ++ctx->launches;
       cnt = blocks;
