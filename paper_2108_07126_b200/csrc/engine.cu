@@ -58,7 +58,9 @@ using PS512 = PSCfg<512, 8, 4, 1, 8, 1, 64, false>;
 // ... and with 3-multiplication complex products (3-plane operands)
 using P3_16 = PS3Cfg<16, 16, 1, 2, 1, 4, 1, true>;
 using P3_32 = PS3Cfg<32, 32, 1, 2, 4, 1, 1, true>;
-using P3_64 = PS3Cfg<64, 32, 1, 4, 4, 1, 2, false>;
+// D=64: 2 CTAs x 32 columns, 8 warps of 16 x 16 (measured: +2% over 4 warps
+// of 16 x 32; 4 CTAs x 16 columns -38%)
+using P3_64 = PS3Cfg<64, 32, 1, 2, 8, 1, 2, false>;
 // D=128: 4 CTAs x 32 columns per lane, 8 warps, 1 CTA per SM.  (Measured:
 // 8 CTAs x 16 columns with 2 CTAs/SM is 1.4x slower — twice the L2 operand
 // traffic and an 8-way group barrier outweigh the barrier overlap.)
@@ -820,10 +822,14 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
                          ? std::max(2, ps_choose(job.m) ? ps_choose(job.m) : 2)
                          : ps_choose(job.m);
   // auto: the 3-multiplication/TMEM form where it measured faster (the
-  // group families, D >= 128: 165% vs 149% of canonical FP64 peak at D=128);
-  // for D <= 64 its 1.5x smem operands cost occupancy and the 4-product PS wins
+  // group families, D >= 128: 165% vs 149% of canonical FP64 peak at D128;
+  // D64 with 8 warps of 16 x 16: +2% for fp64 plans, -4% for the fp32 m = 7
+  // plan); for the smem-resident D <= 32 its 1.5x operands cost occupancy
+  // and the 4-product PS wins
   const bool three_m =
-      ps_s > 0 && (ctx->algo == ALGO_PS3 || (ctx->algo == ALGO_AUTO && ctx->D >= 128));
+      ps_s > 0 && (ctx->algo == ALGO_PS3 ||
+                   (ctx->algo == ALGO_AUTO &&
+                    (ctx->D >= 128 || (ctx->D == 64 && ctx->bits == 64))));
   if (ps_s > 0 && three_m) {
     PSJob pj;
     std::memset(&pj, 0, sizeof(pj));
