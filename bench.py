@@ -8,7 +8,8 @@ Headline workload (BASELINE.json configs[3], the largest single-GPU config):
 C4 = dim-128 random unit-1-norm system, 4 controls, 1e6 slices, midpoint,
 complex128, beta = 0.5 (m = 13), time-sharded over the N GPUs (strong
 scaling: 1e6 slices in total).  Secondary lines (same JSON, "per_dim"): C3
-(dim 32, 2 controls, 1e6 slices), C1 (the paper's driven qubit, dim 2,
+(dim 32, 2 controls, 1e6 slices; random and the coupled-spin chain of
+configs[2]), C1 (the paper's driven qubit, dim 2,
 1e5 slices) and c1m (the same qubit at the north star's 1e6 slices).
 A step is one full propagation U = U_{n-1} ... U_0 of the workload; value = slices / device time (CUDA events, max over ranks), with
 the amplitude table resident in HBM and L2 flushed between timed steps.
@@ -49,6 +50,9 @@ WORKLOADS = {
     "c3": dict(d=32, n_ctrl=2, slices=1_000_000, kind="random",
                label="C3: dim-32 random unit-norm system, 2 controls, 1e6 slices, midpoint, "
                      "complex128, beta=0.5 (m=13)"),
+    "c3s": dict(d=32, n_ctrl=2, slices=1_000_000, kind="spin",
+                label="C3 physics variant: 5-spin coupled chain (d=32, 2 controls, "
+                      "cos/sin drive over T=6), 1e6 slices, midpoint, complex128"),
     "c1": dict(d=2, n_ctrl=2, slices=100_000, kind="qubit",
                label="C1: paper's driven qubit (w0=1, w1=0.1, wrf=1, T=6), dim 2, 2 controls, "
                      "1e5 slices, midpoint, complex128 (m=3)"),
@@ -70,6 +74,10 @@ def make_problem(wl):
         q = sp.DrivenQubit(1.0, 0.1, 1.0, 6.0)
         amps = q.amplitudes(wl["slices"])
         return q.system(), np.ascontiguousarray(amps.values), amps.dt
+    if wl["kind"] == "spin":
+        c = sp.SpinChain()
+        amps = c.amplitudes(wl["slices"])
+        return c.system(), np.ascontiguousarray(amps.values), amps.dt
     rng = np.random.default_rng(SEED)
     from paper_2108_07126_b200.studies import random_system
     system = random_system(rng, wl["d"], wl["n_ctrl"])
@@ -376,7 +384,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
-    ap.add_argument("--secondary", default="c3,c1,c1m",
+    ap.add_argument("--secondary", default="c3,c3s,c1,c1m",
                     help="extra workloads reported under per_dim ('' for none)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")

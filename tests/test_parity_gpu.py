@@ -194,3 +194,27 @@ def test_cumulative_every_family_against_oracle(d, mode):
         assert rel_fro(cum.u_all[k], ref_all[k]) <= tol, k
     assert np.array_equal(cum.final, ctx.equiprop(amps, reduction="sequential").u)
     ctx.close()
+
+
+@pytest.mark.parametrize("pts,algo", [(200, "auto"), (200, "ps"), (2001, "auto")])
+def test_spin_chain_against_oracle(pts, algo):
+    """BASELINE configs[2]: the 5-spin coupled chain (d = 32, 2 controls)
+    against the oracle, plus unitarity of the propagator."""
+    import oracle
+    chain = sp.SpinChain()
+    system = chain.system()
+    amps = chain.amplitudes(pts)
+    h0, hs = system.drift, list(system.controls)
+    ref, _, _ = oracle.equiprop(h0, hs, amps.values, amps.dt, mode="midpoint")
+    ref_seq, _, _ = oracle.equiprop(h0, hs, amps.values, amps.dt, mode="midpoint",
+                                    reduction="sequential")
+    tol, _ = parity_tolerance(ref, ref_seq, "fp64")
+    ctx = sp.create()
+    ctx.set_algorithm(algo)
+    ctx.set_hamiltonian(system)
+    u = ctx.equiprop(amps).u
+    assert rel_fro(u, ref) <= tol
+    # unitarity no worse than the reference's own (rounding accumulates with n)
+    dev = lambda m: np.linalg.norm(m.conj().T @ m - np.eye(32))
+    assert dev(u) <= max(1e-12, 4.0 * dev(ref))
+    ctx.close()
