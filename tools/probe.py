@@ -62,3 +62,16 @@ if len(sys.argv) > 1 and sys.argv[1] == "d8":
 if len(sys.argv) > 1 and sys.argv[1] == "magnus":
     run("d128 magnus 2e3", *random_inputs(128, 4, 4001, 1), mode="magnus")
     run("d32 magnus 2e4", *random_inputs(32, 2, 40001, 1), mode="magnus")
+if len(sys.argv) > 1 and sys.argv[1] == "c64":
+    for d, n in ((16, 100000), (32, 100000), (12, 100000), (24, 50000)):
+        h0, hs, v, dt = random_inputs(d, 2, n, 1)
+        for prec in ("fp32", "fp64"):
+            ctx = sp.create(prec); ctx.set_hamiltonian(sp.ControlSystem(h0, hs)); ctx.set_profiling(True)
+            amps = sp.ControlAmplitudes(v, dt)
+            u = ctx.equiprop(amps).u
+            best = 1e9
+            for _ in range(3):
+                ctx.equiprop(amps); best = min(best, ctx.last_timing()["main_kernel_ms"])
+            t = ctx.last_timing()
+            print(f"c64 probe d{d} {prec}: n={n} kernel {best:.3f} ms ({t['kernel']}), slices/s {n/(best/1e3):.3e}", flush=True)
+            ctx.close()
