@@ -1219,10 +1219,35 @@ int equiprop_all_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
   if (n == 0) return SP_OK;
   const int D = ctx->D, d = ctx->dim;
   const size_t dd = (size_t)D * D;
-  rc = ensure(ctx, ctx->cumP, (size_t)n * dd * sizeof(double2));
-  if (rc) return rc;
   const double2* prods = nullptr;
   int cnt = 0;
+  if (ctx->fam == FAM_S2 && d == 2 && ctx->bits == 64) {
+    // d = 2 (the HBM-write-bound case): no prefix round trip.  Pass 1 forms
+    // the lane products, the ordered scan their exclusive prefixes E_l, and
+    // pass 2 re-runs every lane from V = E_l writing U(t_k <- 0) straight
+    // into the (n, 2, 2) complex128 output; the last entry is the sequential
+    // total M_{L-1} E_{L-1} of the same scan (bitwise contract with
+    // equiprop(reduction="sequential"), propagator.py:304-306)
+    rc = run_lanes(ctx, job, false, nullptr, st, &prods, &cnt);
+    if (rc) return rc;
+    rc = plain_scan(ctx, prods, cnt, st);
+    if (rc) return rc;
+    SliceJob job2 = job;
+    job2.vinit = ctx->cumE.p;
+    const double2* prods2 = nullptr;
+    int cnt2 = 0;
+    rc = run_lanes(ctx, job2, false, (double2*)d_out, st, &prods2, &cnt2);
+    if (rc) return rc;
+    if (cnt2 != cnt) return fail(ctx, SP_E_INTERNAL, "lane count changed between passes");
+    CUDA_TRY(ctx, cudaMemcpyAsync((double2*)d_out + (size_t)(n - 1) * dd, ctx->result.p,
+                                  dd * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    ctx->ev_pending = ctx->prof;
+    ctx->kname = family_kernel_name(ctx->fam, ctx->last_algo);
+    ctx->flops = 2.0 * executed_flops(ctx, n, job.m);
+    return SP_OK;
+  }
+  rc = ensure(ctx, ctx->cumP, (size_t)n * dd * sizeof(double2));
+  if (rc) return rc;
   rc = run_lanes(ctx, job, false, (double2*)ctx->cumP.p, st, &prods, &cnt);
   if (rc) return rc;
   ctx->ev_pending = ctx->prof;

@@ -377,10 +377,14 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
   const int lane = gtid / TPL;
   const int c0 = (gtid % TPL) * CPT;
   double2 V[D][CPT];
+  const double2* vinit = static_cast<const double2*>(job.vinit);
 #pragma unroll
   for (int r = 0; r < D; ++r)
 #pragma unroll
-    for (int cc = 0; cc < CPT; ++cc) V[r][cc] = make_double2(r == c0 + cc ? 1.0 : 0.0, 0.0);
+    for (int cc = 0; cc < CPT; ++cc)
+      V[r][cc] = (vinit != nullptr && lane < lanes)
+                     ? vinit[(size_t)lane * D * D + r * D + c0 + cc]
+                     : make_double2(r == c0 + cc ? 1.0 : 0.0, 0.0);
 
   int64_t s0 = 0, s1 = 0;
   if (lane < lanes) lane_range(job.n_slices, lanes, lane, s0, s1);
