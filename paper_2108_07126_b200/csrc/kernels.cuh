@@ -433,10 +433,7 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
     // vector load per row (prefetched a slice ahead through a running
     // pointer), a 32-bit slice counter
     if (fast2 && job.n_ctrl == NCC) {
-      const int cnt = (int)(s1 - s0);
-      const double* arow = job.amps + s0 * NCC;
-      double rn[NCC], rc[NCC];
-      auto ldrow = [&](const double* a) {
+      auto ldrow = [&](const double* a, double (&rn)[NCC]) {
         if constexpr (NCC == 2) {
           const double2 v = *reinterpret_cast<const double2*>(a);
           rn[0] = v.x;
@@ -446,13 +443,9 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
           for (int q = 0; q < NCC; ++q) rn[q] = a[q];
         }
       };
-      if (cnt > 0) ldrow(arow);
-      for (int k = 0; k < cnt; ++k) {
-#pragma unroll
-        for (int q = 0; q < NCC; ++q) rc[q] = rn[q];
-        arow += NCC;
-        if (k + 1 < cnt) ldrow(arow);
-        const int64_t s = s0 + k;
+      // U(slice s) from its amplitude row: the Clenshaw pairs (first step
+      // peeled: b_{m+1} = b_{m+2} = 0 there, same values as the full step)
+      auto slice_u = [&](const double (&rc)[NCC], int64_t s, double2 (&U)[2][2]) {
         double z0 = tA[0], dz = tB[0];
         double2 zc = tC[0];
 #pragma unroll
@@ -467,8 +460,14 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
         const double zeta2 = fma(dz, dz, fma(zc.x, zc.x, zc.y * zc.y));
         double2 ca = make_double2(job.coef[2 * m], job.coef[2 * m + 1]);
         double2 cb = make_double2(0.0, 0.0), oa = cb, ob = cb;
+        if (m >= 1) {
+          const int jj = m - 1;
+          oa = ca;
+          cb = ca;
+          ca = make_double2(job.coef[2 * jj] + z0 * oa.x, job.coef[2 * jj + 1] + z0 * oa.y);
+        }
 #pragma unroll MUNR
-        for (int jj = m - 1; jj >= 0; --jj) {
+        for (int jj = m - 2; jj >= 0; --jj) {
           const double beta = (jj == 0) ? 2.0 : 1.0;
           const double2 na =
               make_double2(job.coef[2 * jj] + fma(z0, ca.x, fma(zeta2, cb.x, -beta * oa.x)),
@@ -485,36 +484,55 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
           ca = make_double2(pr * ca.x - pi * ca.y, pr * ca.y + pi * ca.x);
           cb = make_double2(pr * cb.x - pi * cb.y, pr * cb.y + pi * cb.x);
         }
-        double2 U[2][2];
         U[0][0] = make_double2(fma(cb.x, dz, ca.x), fma(cb.y, dz, ca.y));
         U[1][1] = make_double2(fma(-cb.x, dz, ca.x), fma(-cb.y, dz, ca.y));
         U[0][1] = make_double2(cb.x * zc.x - cb.y * zc.y, cb.x * zc.y + cb.y * zc.x);
         U[1][0] = make_double2(cb.x * zc.x + cb.y * zc.y, cb.y * zc.x - cb.x * zc.y);
+      };
+      // W <- U W (2 x 2 complex)
+      auto left_mul = [&](const double2 (&U)[2][2], double2 (&W)[2][CPT]) {
         double2 nv[2][CPT];
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
           for (int cc = 0; cc < CPT; ++cc) {
-            double re = U[r][0].x * V[0][cc].x;
-            re = fma(-U[r][0].y, V[0][cc].y, re);
-            re = fma(U[r][1].x, V[1][cc].x, re);
-            re = fma(-U[r][1].y, V[1][cc].y, re);
-            double im = U[r][0].x * V[0][cc].y;
-            im = fma(U[r][0].y, V[0][cc].x, im);
-            im = fma(U[r][1].x, V[1][cc].y, im);
-            im = fma(U[r][1].y, V[1][cc].x, im);
+            double re = U[r][0].x * W[0][cc].x;
+            re = fma(-U[r][0].y, W[0][cc].y, re);
+            re = fma(U[r][1].x, W[1][cc].x, re);
+            re = fma(-U[r][1].y, W[1][cc].y, re);
+            double im = U[r][0].x * W[0][cc].y;
+            im = fma(U[r][0].y, W[0][cc].x, im);
+            im = fma(U[r][1].x, W[1][cc].y, im);
+            im = fma(U[r][1].y, W[1][cc].x, im);
             nv[r][cc] = make_double2(re, im);
           }
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
-          for (int cc = 0; cc < CPT; ++cc) V[r][cc] = nv[r][cc];
-        if (prefix_out) {
-          double2* o = prefix_out + (size_t)s * D * D;
+          for (int cc = 0; cc < CPT; ++cc) W[r][cc] = nv[r][cc];
+      };
+      const int cnt = (int)(s1 - s0);
+      {
+        const double* arow = job.amps + s0 * NCC;
+        double rn[NCC];
+        if (cnt > 0) ldrow(arow, rn);
+        for (int k = 0; k < cnt; ++k) {
+          double rc[NCC];
 #pragma unroll
-          for (int r = 0; r < D; ++r)
+          for (int q = 0; q < NCC; ++q) rc[q] = rn[q];
+          arow += NCC;
+          if (k + 1 < cnt) ldrow(arow, rn);
+          const int64_t s = s0 + k;
+          double2 U[2][2];
+          slice_u(rc, s, U);
+          left_mul(U, V);
+          if (prefix_out) {
+            double2* o = prefix_out + (size_t)s * D * D;
 #pragma unroll
-            for (int cc = 0; cc < CPT; ++cc) o[r * D + c0 + cc] = V[r][cc];
+            for (int r = 0; r < D; ++r)
+#pragma unroll
+              for (int cc = 0; cc < CPT; ++cc) o[r * D + c0 + cc] = V[r][cc];
+          }
         }
       }
       s0 = s1;  // done: the general loop below has nothing left
