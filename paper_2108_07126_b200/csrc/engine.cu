@@ -964,11 +964,16 @@ int build_job(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double
 }
 
 // amplitude validation fused into the lane kernels: reset the device flag
-int arm_validation(sp_ctx* ctx, SliceJob* job, cudaStream_t st) {
-  int rc = ensure(ctx, ctx->viol, sizeof(unsigned long long));
+// (fused: a single-launch call whose last CTA rotates the slots, no memset)
+int arm_validation(sp_ctx* ctx, SliceJob* job, cudaStream_t st, bool fused = false) {
+  const bool fresh = ctx->viol.p == nullptr;
+  int rc = ensure(ctx, ctx->viol, 4 * sizeof(unsigned long long));
   if (rc) return rc;
-  CUDA_TRY(ctx, cudaMemsetAsync(ctx->viol.p, 0xFF, sizeof(unsigned long long), st));
+  if (fresh || !fused)
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->viol.p, 0xFF,
+                                  (fresh ? 4 : 3) * sizeof(unsigned long long), st));
   job->viol = (unsigned long long*)ctx->viol.p;
+  job->viol_epoch = fused ? 1 : 0;
   ctx->viol_stream = st;
   ctx->viol_pts = job->pts;
   return SP_OK;
@@ -980,7 +985,9 @@ int read_violation(sp_ctx* ctx, const double* host_amps, int64_t* index_out) {
   unsigned long long v = ~0ull;
   if (ctx->viol.p) {
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->viol_stream));
-    CUDA_TRY(ctx, cudaMemcpy(&v, ctx->viol.p, sizeof(v), cudaMemcpyDeviceToHost));
+    unsigned long long slots[3];
+    CUDA_TRY(ctx, cudaMemcpy(slots, ctx->viol.p, sizeof(slots), cudaMemcpyDeviceToHost));
+    v = std::min(slots[0], std::min(slots[1], slots[2]));
   }
   if (index_out) *index_out = (v == ~0ull) ? -1 : (int64_t)v;
   if (v == ~0ull) return SP_OK;
@@ -1097,7 +1104,10 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
   SliceJob job;
   int rc = build_job(ctx, d_amps, pts, n_ctrl, dt, plan, &job);
   if (rc) return rc;
-  rc = arm_validation(ctx, &job, st);
+  // the small families' pairwise product is one launch with a fused tail
+  const bool fused = (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) &&
+                     reduction == SP_REDUCE_PAIRWISE && job.n_slices > 0;
+  rc = arm_validation(ctx, &job, st, fused);
   if (rc) return rc;
   const int D = ctx->D, d = ctx->dim;
   const size_t dd = (size_t)D * D;

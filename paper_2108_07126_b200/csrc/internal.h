@@ -29,8 +29,14 @@ struct SliceJob {
   double phase[2];
   int64_t n_slices;
   // first out-of-range amplitude (row-major index), ULLONG_MAX if none:
-  // validation fused into the weight computation (hamiltonian.py:145-153)
+  // validation fused into the weight computation (hamiltonian.py:145-153).
+  // viol[0..2] are slots, viol[3] an epoch: multi-launch calls reset the
+  // slots with a memset and record into slot 2; the single-launch (fused
+  // tail) calls record into slot (epoch & 1) and their last CTA clears the
+  // two other slots and advances the epoch, so no memset is needed in front
+  // of the launch.  The host reads min(slots).
   unsigned long long* viol;
+  int viol_epoch;
   // every expansion term is exactly (bitwise) Hermitian: the d <= 2 kernel
   // may then use real Cayley-Hamilton coefficients (lane_small_kernel<2,1>)
   int herm_exact;

@@ -186,8 +186,22 @@ __device__ __forceinline__ void tmem_store_block(uint32_t taddr, const double (&
 //   (the reference divides the magnus columns by the 2dt scale; same values)
 __device__ __forceinline__ void check_amp(const SliceJob& j, int64_t row, int col, double v) {
   // |c| <= 1 (false for NaN too); the first offender in row-major order wins
-  if (!(fabs(v) <= 1.0) && j.viol)
-    atomicMin(j.viol, (unsigned long long)(row * j.n_ctrl + col));
+  if (!(fabs(v) <= 1.0) && j.viol) {
+    unsigned long long* slot = j.viol + 2;
+    if (j.viol_epoch) slot = j.viol + (__ldcg(j.viol + 3) & 1ull);
+    atomicMin(slot, (unsigned long long)(row * j.n_ctrl + col));
+  }
+}
+
+// end of a single-launch call (its last CTA, after every other CTA arrived):
+// clear the slots the next call may use and advance the epoch (see SliceJob)
+__device__ __forceinline__ void rotate_violation_slots(const SliceJob& j) {
+  if (j.viol && j.viol_epoch) {
+    const unsigned long long e = __ldcg(j.viol + 3);
+    j.viol[(e + 1) & 1ull] = ~0ull;
+    j.viol[2] = ~0ull;
+    j.viol[3] = e + 1;
+  }
 }
 
 // Every amplitude of the table is read by exactly one weight t in 1..N of
@@ -883,6 +897,7 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
           reinterpret_cast<double2*>(tail.out)[e] = v;
       }
       *tail.ctr = 0;  // ready for the next launch
+      rotate_violation_slots(job);
     }
     PH(3);
     PH_DONE
@@ -975,7 +990,10 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
     else
       reinterpret_cast<double2*>(tail.out)[e] = v;
   }
-  if (threadIdx.x == 0) *tail.ctr = 0;  // ready for the next launch
+  if (threadIdx.x == 0) {
+    *tail.ctr = 0;  // ready for the next launch
+    rotate_violation_slots(job);
+  }
   PH(3);
   PH_DONE
   }

@@ -258,3 +258,57 @@ def test_reduce_pairwise_matches_reference_order(n, dtype, rng):
     ref = oracle.reduce_pairwise(u.astype(np.complex128))
     tol = 1e-13 if dtype == np.complex128 else 1e-5
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= tol
+
+
+@pytest.mark.parametrize("d", [2, 4])
+def test_violation_slots_across_fused_calls_and_graph_replays(d, rng):
+    """Single-launch calls (small families, pairwise) record violations in
+    epoch-rotated slots instead of a memset in front of the launch: every
+    call, fused or not, replayed in a CUDA graph or not, reports exactly its
+    own first offender."""
+    import torch
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(random_hermitian(rng, d, 1.0),
+                                         [random_hermitian(rng, d, 1.0)] * 2))
+    dev = torch.device("cuda", 0)
+    good = rng.uniform(-1.0, 1.0, (500, 2))
+    bad = good.copy()
+    bad[321, 1] = 1.25
+    worse = good.copy()
+    worse[17, 0] = np.nan
+    # host entry points: fused (pairwise) and multi-launch (sequential,
+    # cumulative) interleaved with and without violations
+    seq = [(good, "pairwise", None), (bad, "pairwise", 321 * 2 + 1), (good, "pairwise", None),
+           (bad, "sequential", 321 * 2 + 1), (good, "pairwise", None), (worse, "all", 34),
+           (good, "pairwise", None), (good, "sequential", None), (worse, "pairwise", 34),
+           (bad, "pairwise", 321 * 2 + 1), (good, "all", None), (good, "pairwise", None)]
+    for values, kind, expect in seq:
+        amps = sp.ControlAmplitudes(values, 0.02)
+        call = (lambda: ctx.equiprop_all(amps)) if kind == "all" else \
+            (lambda: ctx.equiprop(amps, reduction=kind))
+        if expect is None:
+            call()
+        else:
+            with pytest.raises(sp.AmplitudeBoundError,
+                               match=f"sample {expect // 2}, control {expect % 2}"):
+                call()
+    # device entry point captured once and replayed with new table contents
+    d_amps = torch.from_numpy(np.ascontiguousarray(good)).to(dev)
+    out = torch.empty((d, d), dtype=torch.complex128, device=dev)
+    plan = ctx.plan_for(0.02)
+    s = torch.cuda.Stream(dev)
+    ctx.set_profiling(False)
+    ctx.equiprop_device_ptr(d_amps.data_ptr(), 500, 2, 0.02, out.data_ptr(),
+                            stream=s.cuda_stream, plan=plan)
+    assert ctx.amplitude_violation() == -1
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ctx.equiprop_device_ptr(d_amps.data_ptr(), 500, 2, 0.02, out.data_ptr(),
+                                stream=s.cuda_stream, plan=plan)
+    for values, expect in ((good, -1), (bad, 321 * 2 + 1), (bad, 321 * 2 + 1), (good, -1),
+                           (worse, 34), (good, -1), (good, -1), (bad, 643)):
+        d_amps.copy_(torch.from_numpy(np.ascontiguousarray(values)))
+        g.replay()
+        torch.cuda.synchronize(dev)
+        assert ctx.amplitude_violation() == expect
+    ctx.close()
