@@ -64,7 +64,18 @@ for n in (100000, 1000000):
             cur.synchronize()
             ts.append(a.elapsed_time(b) * 1e3)
         res[name] = float(np.median(ts))
+    ts = []
+    for k in range(30):  # direct launch (no graph) after the 256 MiB flush
+        big.fill_(float(k))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        ctx.equiprop_device_ptr(d_amps.data_ptr(), n, 2, dt, out.data_ptr(),
+                                stream=cur.cuda_stream, plan=plan)
+        b.record(cur)
+        cur.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    res["direct"] = float(np.median(ts))
     print(f"n={n}: back-to-back {b2b:.2f} us/step; single replay after flush 256 MiB "
-          f"{res['flush256']:.2f}, after 32 MiB {res['flush32']:.2f}, no flush {res['none']:.2f} us",
+          f"{res['flush256']:.2f}, after 32 MiB {res['flush32']:.2f}, no flush {res['none']:.2f} us; direct launch after 256 MiB {res['direct']:.2f} us",
           flush=True)
     ctx.close()
