@@ -130,6 +130,13 @@ void ps_coefficients(const double* coef, int m, int s, double* alpha, int* r_out
   *r_out = r;
 }
 
+// alpha alternates exactly real / imaginary with the parity of j*s + i
+int ps_alpha_alt(const double* alpha, int count) {
+  for (int q = 0; q < count; ++q)
+    if (alpha[2 * q + ((q & 1) ? 0 : 1)] != 0.0) return 0;
+  return 1;
+}
+
 int family_for(int d, int* D) {
   if (d <= 2) { *D = 2; return FAM_S2; }
   if (d <= 4) { *D = 4; return FAM_S4; }
@@ -728,6 +735,7 @@ int d8_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_
   if (ps_s > 0) {
     pj.s = ps_s;
     ps_coefficients(job.coef, job.m, ps_s, pj.alpha, &pj.r);
+    pj.alt = ps_alpha_alt(pj.alpha, pj.r * pj.s);
   }
   int lanes = 0;
   const int rc = alg == D8_CLENSHAW ? d8_run<D8_CLENSHAW>(ctx, pj, prefix_out, st, &lanes)
@@ -805,9 +813,32 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
       }
 #undef SP_S2
     }
-    else
-      lane_small_kernel<4, 4><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out, cta_out,
-                                                      prefix_out, tail);
+    else {
+      // d = 3, 4: the series order compiled in for every order of the plan
+      // grid (odd 3..25; the Clenshaw loop unrolls, no spills) with the
+      // alternating-coefficient products when the plan has them
+#define SP_S4(MCV)                                                                            \
+  lane_small_kernel<4, 4, MCV, 0, true><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,   \
+                                                                cta_out, prefix_out, tail)
+      switch (job.coef_alt ? job.m : 0) {
+        case 3: SP_S4(3); break;
+        case 5: SP_S4(5); break;
+        case 7: SP_S4(7); break;
+        case 9: SP_S4(9); break;
+        case 11: SP_S4(11); break;
+        case 13: SP_S4(13); break;
+        case 15: SP_S4(15); break;
+        case 17: SP_S4(17); break;
+        case 19: SP_S4(19); break;
+        case 21: SP_S4(21); break;
+        case 23: SP_S4(23); break;
+        case 25: SP_S4(25); break;
+        default:
+          lane_small_kernel<4, 4><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out, cta_out,
+                                                          prefix_out, tail);
+      }
+#undef SP_S4
+    }
     CUDA_TRY(ctx, cudaGetLastError());
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
     ++ctx->launches;
@@ -836,6 +867,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     pj.base = job;
     pj.s = ps_s;
     ps_coefficients(job.coef, job.m, ps_s, pj.alpha, &pj.r);
+    pj.alt = ps_alpha_alt(pj.alpha, pj.r * pj.s);
     switch (ctx->fam) {
       case FAM_T16: lanes = ps3_lanes<P3_16>(ctx, n); break;
       case FAM_T32: lanes = ps3_lanes<P3_32>(ctx, n); break;
@@ -868,6 +900,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     pj.base = job;
     pj.s = ps_s;
     ps_coefficients(job.coef, job.m, ps_s, pj.alpha, &pj.r);
+    pj.alt = ps_alpha_alt(pj.alpha, pj.r * pj.s);
     switch (ctx->fam) {
       case FAM_T16: lanes = ps_lanes<PS16>(ctx, n); break;
       case FAM_T32: lanes = ps_lanes<PS32>(ctx, n); break;
@@ -960,6 +993,9 @@ int build_job(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double
   job->phase[1] = plan->phase[1];
   job->n_slices = n;
   job->herm_exact = ctx->herm_exact ? 1 : 0;
+  job->coef_alt = 1;
+  for (int k = 0; k <= job->m; ++k)
+    if (job->coef[2 * k + ((k & 1) ? 0 : 1)] != 0.0) job->coef_alt = 0;
   return SP_OK;
 }
 

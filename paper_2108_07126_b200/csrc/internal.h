@@ -40,6 +40,8 @@ struct SliceJob {
   // every expansion term is exactly (bitwise) Hermitian: the d <= 2 kernel
   // may then use real Cayley-Hamilton coefficients (lane_small_kernel<2,1>)
   int herm_exact;
+  // the plan coefficients alternate exactly real / imaginary (ALT kernels)
+  int coef_alt;
   // plain D x D per-lane initial running products (nullptr = identity): the
   // second pass of the d = 2 cumulative path (lane_small_kernel)
   const void* vinit;

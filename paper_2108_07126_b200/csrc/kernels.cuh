@@ -377,7 +377,12 @@ __device__ __forceinline__ void warp_ordered_product(double2 (&M)[D][D], int wid
 // MC > 0: the series order m compiled in (the common orders 3, 7, 13, 15):
 // the Clenshaw loop unrolls and the plan coefficients become constant-bank
 // operands; 0 = runtime m
-template <int D, int TPL, int MC = 0, int NCC = 0>
+// ALT: the plan coefficients alternate real / imaginary (c_k = (-i)^k |c_k|,
+// every symmetric equiprop plan: exact zeros, checked on the host), so each
+// Clenshaw step of the d <= 4 general path needs one real-by-complex product
+// per entry instead of a complex one (with MC the parity of every step is
+// known at compile time)
+template <int D, int TPL, int MC = 0, int NCC = 0, bool ALT = false>
 // (register budget for 3 CTAs/SM at D = 2 and 2 at D = 4: the lane loop is
 // latency bound and needs the resident warps)
 __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJob job,
@@ -734,8 +739,13 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
         for (int r = 0; r < D; ++r)
   #pragma unroll
           for (int cc = 0; cc < CPT; ++cc) {
-            cur[r][cc] = make_double2(ar * V[r][cc].x - ai * V[r][cc].y,
-                                      ar * V[r][cc].y + ai * V[r][cc].x);
+            if (ALT && (m & 1))
+              cur[r][cc] = make_double2(-ai * V[r][cc].y, ai * V[r][cc].x);
+            else if (ALT)
+              cur[r][cc] = make_double2(ar * V[r][cc].x, ar * V[r][cc].y);
+            else
+              cur[r][cc] = make_double2(ar * V[r][cc].x - ai * V[r][cc].y,
+                                        ar * V[r][cc].y + ai * V[r][cc].x);
             old[r][cc] = make_double2(0.0, 0.0);
           }
       }
@@ -748,8 +758,17 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
         for (int r = 0; r < D; ++r)
   #pragma unroll
           for (int cc = 0; cc < CPT; ++cc) {
-            double re = fma(ar, V[r][cc].x, fma(-ai, V[r][cc].y, -beta * old[r][cc].x));
-            double im = fma(ar, V[r][cc].y, fma(ai, V[r][cc].x, -beta * old[r][cc].y));
+            double re, im;
+            if (ALT && (jj & 1)) {  // c_jj = i ai: same values, one product less
+              re = fma(-ai, V[r][cc].y, -beta * old[r][cc].x);
+              im = fma(ai, V[r][cc].x, -beta * old[r][cc].y);
+            } else if (ALT) {  // c_jj = ar
+              re = fma(ar, V[r][cc].x, -beta * old[r][cc].x);
+              im = fma(ar, V[r][cc].y, -beta * old[r][cc].y);
+            } else {
+              re = fma(ar, V[r][cc].x, fma(-ai, V[r][cc].y, -beta * old[r][cc].x));
+              im = fma(ar, V[r][cc].y, fma(ai, V[r][cc].x, -beta * old[r][cc].y));
+            }
   #pragma unroll
             for (int k = 0; k < D; ++k) {
               re = fma(X[r][k].x, cur[k][cc].x, re);

@@ -251,10 +251,19 @@ __global__ void __launch_bounds__(32 * WPC) lane_d8_kernel(PSJob pj,
         for (int i = 1; i < 4; ++i) {
           if (i >= s) break;
           const double ar = pj.alpha[2 * (j * s + i)], ai = pj.alpha[2 * (j * s + i) + 1];
+          const int kind = alpha_kind(pj, j * s + i);
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            qr[e] = fma(ar, Tr[i - 1][e], fma(-ai, Ti[i - 1][e], qr[e]));
-            qi[e] = fma(ar, Ti[i - 1][e], fma(ai, Tr[i - 1][e], qi[e]));
+            if (kind == 1) {
+              qr[e] = fma(ar, Tr[i - 1][e], qr[e]);
+              qi[e] = fma(ar, Ti[i - 1][e], qi[e]);
+            } else if (kind == 2) {
+              qr[e] = fma(-ai, Ti[i - 1][e], qr[e]);
+              qi[e] = fma(ai, Tr[i - 1][e], qi[e]);
+            } else {
+              qr[e] = fma(ar, Tr[i - 1][e], fma(-ai, Ti[i - 1][e], qr[e]));
+              qi[e] = fma(ar, Ti[i - 1][e], fma(ai, Tr[i - 1][e], qi[e]));
+            }
           }
         }
       };

@@ -53,7 +53,16 @@ struct PSJob {
   SliceJob base;
   int s, r;
   double alpha[2 * PS_MAXC];  // alpha_{j,i} at (j*s + i), complex
+  // alpha_{j,i} is exactly real for even j*s + i and imaginary for odd (the
+  // plan's (-i)^k structure survives the regrouping): Q_j accumulates with
+  // real-by-complex products
+  int alt;
 };
+
+// 0: general complex alpha, 1: real, 2: imaginary (uniform per (j, i))
+__device__ __forceinline__ int alpha_kind(const PSJob& pj, int q) {
+  return pj.alt ? 1 + (q & 1) : 0;
+}
 
 // SC, RC > 0: the (s, r) split fixed at compile time (as lane_d8_kernel):
 // the power / Clenshaw loops unroll and the power-block locations resolve
@@ -167,11 +176,28 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll UNR
     for (int i = 1; i < s; ++i) {
       const double ar = pj.alpha[2 * (j * s + i)], ai = pj.alpha[2 * (j * s + i) + 1];
+      const int kind = alpha_kind(pj, j * s + i);
+      if (kind == 1) {
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        const double2 tv = tp_load(i - 1, e);
-        qr[e] = fma(ar, tv.x, fma(-ai, tv.y, qr[e]));
-        qi[e] = fma(ar, tv.y, fma(ai, tv.x, qi[e]));
+        for (int e = 0; e < NE; ++e) {
+          const double2 tv = tp_load(i - 1, e);
+          qr[e] = fma(ar, tv.x, qr[e]);
+          qi[e] = fma(ar, tv.y, qi[e]);
+        }
+      } else if (kind == 2) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const double2 tv = tp_load(i - 1, e);
+          qr[e] = fma(-ai, tv.y, qr[e]);
+          qi[e] = fma(ai, tv.x, qi[e]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const double2 tv = tp_load(i - 1, e);
+          qr[e] = fma(ar, tv.x, fma(-ai, tv.y, qr[e]));
+          qi[e] = fma(ar, tv.y, fma(ai, tv.x, qi[e]));
+        }
       }
     }
   };

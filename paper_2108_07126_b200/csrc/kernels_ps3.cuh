@@ -216,10 +216,25 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       const double ar = pj.alpha[2 * (j * s + i)], ai = pj.alpha[2 * (j * s + i) + 1];
       double tr[NE], ti[NE];
       tmem_load_block<NE>(tm(i), tr, ti);
+      const int kind = alpha_kind(pj, j * s + i);
+      if (kind == 1) {
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        qr[e] = fma(ar, tr[e], fma(-ai, ti[e], qr[e]));
-        qi[e] = fma(ar, ti[e], fma(ai, tr[e], qi[e]));
+        for (int e = 0; e < NE; ++e) {
+          qr[e] = fma(ar, tr[e], qr[e]);
+          qi[e] = fma(ar, ti[e], qi[e]);
+        }
+      } else if (kind == 2) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          qr[e] = fma(-ai, ti[e], qr[e]);
+          qi[e] = fma(ai, tr[e], qi[e]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          qr[e] = fma(ar, tr[e], fma(-ai, ti[e], qr[e]));
+          qi[e] = fma(ar, ti[e], fma(ai, tr[e], qi[e]));
+        }
       }
     }
   };

@@ -218,3 +218,29 @@ def test_spin_chain_against_oracle(pts, algo):
     dev = lambda m: np.linalg.norm(m.conj().T @ m - np.eye(32))
     assert dev(u) <= max(1e-12, 4.0 * dev(ref))
     ctx.close()
+
+
+@pytest.mark.parametrize("m", list(range(3, 26, 2)))
+@pytest.mark.parametrize("d", [3, 4])
+def test_small_family_every_series_order_against_oracle(d, m):
+    """d = 3, 4 compile the series order in for every order of the plan grid
+    (and use the plan's alternating real / imaginary coefficients): each
+    order against the oracle with the same pinned m, pairwise and
+    cumulative."""
+    import oracle
+    from cases import random_inputs
+    h0, hs, values, dt = random_inputs(d, 2, 300, 500 + 10 * d + m)
+    ref, _, plan = oracle.equiprop(h0, hs, values, dt, m_max=m)
+    ref_seq, _, _ = oracle.equiprop(h0, hs, values, dt, m_max=m, reduction="sequential")
+    ref_all, _, _ = oracle.equiprop_all(h0, hs, values, dt, m_max=m)
+    tol, _ = parity_tolerance(ref, ref_seq, "fp64")
+    ctx = sp.create(m_max=m)
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+    amps = sp.ControlAmplitudes(values, dt)
+    res = ctx.equiprop(amps)
+    assert res.plan["m_max"] == m
+    assert rel_fro(res.u, ref) <= tol
+    cum = ctx.equiprop_all(amps)
+    for k in (0, 1, 150, 299):
+        assert rel_fro(cum.u_all[k], ref_all[k]) <= tol, k
+    ctx.close()
