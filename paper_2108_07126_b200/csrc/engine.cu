@@ -211,7 +211,7 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   int fam = FAM_NONE, D = 0;
   DevBuf terms, amps, lanes, ctab, tree0, tree1, xglob, gctr, result, out, cumP, cumE, cumO,
-      fold_scratch, psA, tpriv, viol, terms3, tailctr, seqA, scanEin, lstarts;
+      fold_scratch, psA, tpriv, viol, terms3, tailctr, seqA, scanEin, lstarts, scanS, scanA;
   cudaStream_t viol_stream = nullptr;
   int64_t viol_pts = 0;
   int algo = 0;          // Algo
@@ -559,7 +559,7 @@ using AP512 = TCCfg<512, 8, 4, 1, 8, 1, 64, false>;
 
 template <class C>
 int ap_launch(sp_ctx* ctx, const double* P, const double2* E, int64_t n, int lanes, void* out,
-              cudaStream_t st) {
+              cudaStream_t st, int out_d = -1, int out_fp32 = -1) {
   const size_t smem = (size_t)C::BDBL * sizeof(double);
   CUDA_TRY(ctx, cudaFuncSetAttribute(apply_prefix_tc_kernel<C>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -567,23 +567,83 @@ int ap_launch(sp_ctx* ctx, const double* P, const double2* E, int64_t n, int lan
   const int64_t spb = std::max<int64_t>(1, (n + target - 1) / target);
   const int64_t chunks = (n + spb - 1) / spb;
   apply_prefix_tc_kernel<C><<<dim3((unsigned)chunks, C::GPL), C::THREADS, smem, st>>>(
-      P, E, n, lanes, spb, ctx->dim, ctx->bits == 32, out);
+      P, E, n, lanes, spb, out_d >= 0 ? out_d : ctx->dim,
+      out_fp32 >= 0 ? out_fp32 : (ctx->bits == 32 ? 1 : 0), out);
   CUDA_TRY(ctx, cudaGetLastError());
   ++ctx->launches;
   return SP_OK;
 }
 
+// (out_d / out_fp32: the output block size and dtype, default the context's d
+// and working dtype; the scan below writes full D x D complex128 blocks)
 int tc_apply(sp_ctx* ctx, const double* P, const double2* E, int64_t n, int lanes, void* out,
-             cudaStream_t st) {
+             cudaStream_t st, int out_d = -1, int out_fp32 = -1) {
   switch (ctx->fam) {
-    case FAM_T16: return ap_launch<AP16>(ctx, P, E, n, lanes, out, st);
-    case FAM_T32: return ap_launch<AP32>(ctx, P, E, n, lanes, out, st);
-    case FAM_T64: return ap_launch<AP64>(ctx, P, E, n, lanes, out, st);
-    case FAM_T128: return ap_launch<AP128>(ctx, P, E, n, lanes, out, st);
-    case FAM_T256: return ap_launch<AP256>(ctx, P, E, n, lanes, out, st);
-    case FAM_T512: return ap_launch<AP512>(ctx, P, E, n, lanes, out, st);
+    case FAM_T16: return ap_launch<AP16>(ctx, P, E, n, lanes, out, st, out_d, out_fp32);
+    case FAM_T32: return ap_launch<AP32>(ctx, P, E, n, lanes, out, st, out_d, out_fp32);
+    case FAM_T64: return ap_launch<AP64>(ctx, P, E, n, lanes, out, st, out_d, out_fp32);
+    case FAM_T128: return ap_launch<AP128>(ctx, P, E, n, lanes, out, st, out_d, out_fp32);
+    case FAM_T256: return ap_launch<AP256>(ctx, P, E, n, lanes, out, st, out_d, out_fp32);
+    case FAM_T512: return ap_launch<AP512>(ctx, P, E, n, lanes, out, st, out_d, out_fp32);
   }
   return fail(ctx, SP_E_INTERNAL, "no tensor-core apply for this family");
+}
+
+// count row-major complex D x D matrices -> A-native 2-plane layout (exact)
+__global__ void batch_afrag_kernel(const double2* __restrict__ in, int64_t count, int D,
+                                   double* __restrict__ out) {
+  const int64_t dd = (int64_t)D * D, total = count * dd;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t mtx = e / dd;
+    const int rc = (int)(e % dd), r = rc / D, c = rc % D;
+    double* o = out + mtx * 2 * dd;
+    o[xfrag_index(D, r, c, 0)] = in[e].x;
+    o[xfrag_index(D, r, c, 1)] = in[e].y;
+  }
+}
+
+// Exclusive prefixes of the lane products on tensor cores (tensor-core
+// families): E_0 = I, E_l = M_{l-1} ... M_0 into ctx->cumE, by a
+// Hillis-Steele scan: S <- (I, M_0, ..., M_{L-2}), then for o = 1, 2, 4, ...
+// S_l <- S_l S_{l-o} (l >= o) as one batched DMMA launch per level (the
+// prefix-application kernel with one "lane" per item).  log2(L) levels of
+// parallel GEMMs instead of L dependent ones on one SM (the SIMT fold: 13.6 ms
+// for 37 lanes of D = 128).  The sequential reduction uses the same E_{L-1},
+// so equiprop_all's last entry stays bitwise equal to it.
+int tc_scan(sp_ctx* ctx, const double2* prods, int L, cudaStream_t st) {
+  const int D = ctx->D;
+  const size_t dd = (size_t)D * D;
+  int rc = ensure(ctx, ctx->cumE, (size_t)L * dd * sizeof(double2));
+  if (rc) return rc;
+  rc = ensure(ctx, ctx->scanS, (size_t)L * dd * sizeof(double2));
+  if (rc) return rc;
+  rc = ensure(ctx, ctx->scanA, (size_t)L * 2 * dd * sizeof(double));
+  if (rc) return rc;
+  double2* S = (double2*)ctx->scanS.p;
+  double2* T = (double2*)ctx->cumE.p;
+  embed_kernel<<<grid_for((int64_t)dd, 256), 256, 0, st>>>(nullptr, 1, 0, D, S);
+  CUDA_TRY(ctx, cudaGetLastError());
+  ++ctx->launches;
+  if (L > 1)
+    CUDA_TRY(ctx, cudaMemcpyAsync(S + dd, prods, (size_t)(L - 1) * dd * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, st));
+  for (int o = 1; o < L; o <<= 1) {
+    const int64_t m = L - o;
+    batch_afrag_kernel<<<grid_for(m * (int64_t)dd, 256), 256, 0, st>>>(
+        S + (size_t)o * dd, m, D, (double*)ctx->scanA.p);
+    CUDA_TRY(ctx, cudaGetLastError());
+    ++ctx->launches;
+    CUDA_TRY(ctx, cudaMemcpyAsync(T, S, (size_t)o * dd * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, st));
+    rc = tc_apply(ctx, (const double*)ctx->scanA.p, S, m, (int)m, T + (size_t)o * dd, st, D, 0);
+    if (rc) return rc;
+    std::swap(S, T);
+  }
+  if (S != (double2*)ctx->cumE.p)
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->cumE.p, S, (size_t)L * dd * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, st));
+  return SP_OK;
 }
 
 // one CTA folds a chunk of CH consecutive products by the level-order smem
@@ -1174,19 +1234,14 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
     if (reduction == SP_REDUCE_SEQUENTIAL && !small) {
       // left fold to E_{L-1} = P_{L-2} ... P_0, then P_{L-1} E_{L-1} with the
       // same tensor-core routine equiprop_all uses for its last entry
-      rc = ensure(ctx, ctx->cumE, (size_t)cnt * dd * sizeof(double2));
-      if (rc) return rc;
-      rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
-      if (rc) return rc;
       rc = ensure(ctx, ctx->seqA, dd * sizeof(double2));
       if (rc) return rc;
-      fold_kernel<<<1, 1024, 0, st>>>(prods, cnt, D, (double2*)ctx->fold_scratch.p,
-                                       (double2*)ctx->cumE.p, (double2*)ctx->result.p);
-      CUDA_TRY(ctx, cudaGetLastError());
+      rc = tc_scan(ctx, prods, cnt, st);
+      if (rc) return rc;
       to_afrag_kernel<<<grid_for((int64_t)dd, 256), 256, 0, st>>>(
           prods + (size_t)(cnt - 1) * dd, D, (double*)ctx->seqA.p);
       CUDA_TRY(ctx, cudaGetLastError());
-      ctx->launches += 2;
+      ctx->launches += 1;
       return tc_apply(ctx, (const double*)ctx->seqA.p,
                       (const double2*)ctx->cumE.p + (size_t)(cnt - 1) * dd, 1, 1, d_out, st);
     }
@@ -1303,16 +1358,8 @@ int equiprop_all_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
     rc = plain_scan(ctx, prods, cnt, st);
     if (rc) return rc;
   } else {
-    rc = ensure(ctx, ctx->cumE, (size_t)cnt * dd * sizeof(double2));
+    rc = tc_scan(ctx, prods, cnt, st);
     if (rc) return rc;
-    rc = ensure(ctx, ctx->fold_scratch, 2 * dd * sizeof(double2));
-    if (rc) return rc;
-    rc = ensure(ctx, ctx->result, dd * sizeof(double2));
-    if (rc) return rc;
-    fold_kernel<<<1, 1024, 0, st>>>(prods, cnt, D, (double2*)ctx->fold_scratch.p,
-                                     (double2*)ctx->cumE.p, (double2*)ctx->result.p);
-    CUDA_TRY(ctx, cudaGetLastError());
-    ctx->launches += 1;
   }
   if (plain_family(ctx->fam)) {
     rc = ensure(ctx, ctx->lstarts, (size_t)(cnt + 1) * sizeof(int64_t));
@@ -1405,7 +1452,7 @@ int sp_free(sp_ctx* ctx) {
                       &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
                       &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch,
                       &ctx->psA,   &ctx->tpriv, &ctx->viol, &ctx->terms3, &ctx->tailctr,
-                      &ctx->seqA, &ctx->scanEin, &ctx->lstarts};
+                      &ctx->seqA, &ctx->scanEin, &ctx->lstarts, &ctx->scanS, &ctx->scanA};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);

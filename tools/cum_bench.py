@@ -27,7 +27,10 @@ CASES = [(2, 4_000_000), (4, 2_000_000), (8, 1_000_000), (16, 400_000), (32, 100
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "cum.jsonl"))
+    ap.add_argument("--dims", default="", help="comma-separated subset of the case dims")
+    ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
+    cases = [c for c in CASES if not a.dims or str(c[0]) in a.dims.split(",")]
     import torch
 
     import paper_2108_07126_b200 as sp
@@ -37,7 +40,7 @@ def main():
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     fh = open(a.out, "w")
-    for d, n in CASES:
+    for d, n in cases:
         rng = np.random.default_rng(20240911)
         h0 = unit_hermitian(rng, d)
         hs = [unit_hermitian(rng, d) for _ in range(2)]
@@ -53,7 +56,7 @@ def main():
         run()
         torch.cuda.synchronize(dev)
         ms = []
-        for _ in range(3):
+        for _ in range(a.reps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
