@@ -11,8 +11,15 @@ import numpy as np
 import paper_2108_07126_b200 as sp
 from cases import random_inputs
 
-for d, n in ((2, 300), (4, 64), (16, 16), (32, 8), (64, 6), (128, 3), (256, 2)):
-    for algo in ("clenshaw", "ps", "ps3m") if d >= 16 else ("auto",):
+# SANITIZE_NO_TMEM=1: skip the kernels that use tensor memory (tcgen05
+# alloc/ld/st: the ps3 / ps3g families), for tools that do not model it
+NO_TMEM = os.environ.get("SANITIZE_NO_TMEM") == "1"
+
+for d, n in ((2, 300), (3, 40), (4, 64), (8, 40), (16, 16), (32, 8), (64, 6), (128, 3),
+             (256, 2), (512, 2)):
+    for algo in ("clenshaw", "ps", "ps3m") if 16 <= d <= 256 else ("auto",):
+        if NO_TMEM and (algo == "ps3m" or (algo == "auto" and d >= 64)):
+            continue
         h0, hs, v, dt = random_inputs(d, 2, n, 7)
         ctx = sp.create()
         ctx.set_algorithm(algo)
