@@ -312,3 +312,43 @@ def test_violation_slots_across_fused_calls_and_graph_replays(d, rng):
         torch.cuda.synchronize(dev)
         assert ctx.amplitude_violation() == expect
     ctx.close()
+
+
+def test_more_than_2_31_slices_device_resident():
+    """64-bit slice indexing: 3 * 2^30 slices (a 51 GB table in HBM; row
+    index x controls > 2^32), the drive switching at row 2^31, against the
+    closed form exp(-i T2 H2) exp(-i T1 H1): rows past 2^31 read wrongly
+    (an int32 wrap) would change the result at O(1)."""
+    import torch
+    n1, n = 1 << 31, 3 << 30
+    dt = 3e-10
+    c1, c2 = (0.3, -0.4), (-0.8, 0.5)
+    ctx = sp.create()
+    sysm = driven_qubit()
+    ctx.set_hamiltonian(sysm)
+    dev = torch.device("cuda", 0)
+    d_amps = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    d_amps[:n1, 0], d_amps[:n1, 1] = c1
+    d_amps[n1:, 0], d_amps[n1:, 1] = c2
+    out = torch.empty((2, 2), dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    info = ctx.equiprop_device_ptr(d_amps.data_ptr(), n, 2, dt, out.data_ptr(),
+                                   stream=stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    assert info["slice_count"] == n
+    assert ctx.amplitude_violation() == -1
+    h1 = sysm.drift + c1[0] * sysm.controls[0] + c1[1] * sysm.controls[1]
+    h2 = sysm.drift + c2[0] * sysm.controls[0] + c2[1] * sysm.controls[1]
+    ref = expm_eigh((n - n1) * dt * h2) @ expm_eigh(n1 * dt * h1)
+    got = out.cpu().numpy()
+    # identical slices repeat the same rounding: the error grows ~ n eps
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
+    # a violation past the 2^32 index boundary is reported at its row
+    d_amps[n - 3, 1] = 1.5
+    ctx.equiprop_device_ptr(d_amps.data_ptr(), n, 2, dt, out.data_ptr(),
+                            stream=stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    assert ctx.amplitude_violation() == (n - 3) * 2 + 1
+    del d_amps
+    torch.cuda.empty_cache()
+    ctx.close()
