@@ -244,3 +244,23 @@ def test_small_family_every_series_order_against_oracle(d, m):
     for k in (0, 1, 150, 299):
         assert rel_fro(cum.u_all[k], ref_all[k]) <= tol, k
     ctx.close()
+
+
+@pytest.mark.parametrize("pts", [1000, 100_000, 1_000_000])
+def test_driven_qubit_against_extended_precision_oracle(pts):
+    """SURVEY.md §8(c) gate for d = 2: against the 80-bit oracle of the same
+    midpoint discretisation (exact per-slice rotations, long double pairwise
+    fold), the B200 result is at most twice as far off as the reference's
+    own (oracle restatement, complex128)."""
+    import oracle
+    from cases import qubit_inputs
+    h0, hs, values, dt = qubit_inputs(pts, "midpoint")
+    exact = oracle.midpoint_reference_ld(1.0, 0.1, 1.0, 6.0, pts)
+    ref, _, _ = oracle.equiprop(h0, hs, values, dt, mode="midpoint")
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+    got = ctx.equiprop(sp.ControlAmplitudes(values, dt)).u
+    err_ref = rel_fro(ref, exact)
+    err_gpu = rel_fro(got, exact)
+    assert err_gpu <= max(2.0 * err_ref, 1e-15), (err_gpu, err_ref)
+    ctx.close()
