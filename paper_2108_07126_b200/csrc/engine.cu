@@ -1366,9 +1366,20 @@ int equiprop_all_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
     if (rc) return rc;
     lane_starts_kernel<<<grid_for(cnt + 1, 256), 256, 0, st>>>(n, cnt, (int64_t*)ctx->lstarts.p);
     CUDA_TRY(ctx, cudaGetLastError());
-    apply_prefix_kernel<<<grid_for(n * d * d, 256), 256, 0, st>>>(
-        (const double2*)ctx->cumP.p, (const double2*)ctx->cumE.p,
-        (const int64_t*)ctx->lstarts.p, n, cnt, D, d, ctx->bits == 32, d_out);
+    const double2* cP = (const double2*)ctx->cumP.p;
+    const double2* cE = (const double2*)ctx->cumE.p;
+    const int64_t* ls = (const int64_t*)ctx->lstarts.p;
+    const int f32 = ctx->bits == 32;
+    // one CTA per lane
+    if (D == 2)
+      apply_prefix_lanes_kernel<2><<<cnt, 256, 0, st>>>(cP, cE, ls, d, f32, d_out);
+    else if (D == 4)
+      apply_prefix_lanes_kernel<4><<<cnt, 256, 0, st>>>(cP, cE, ls, d, f32, d_out);
+    else if (D == 8)
+      apply_prefix_lanes_kernel<8><<<cnt, 256, 0, st>>>(cP, cE, ls, d, f32, d_out);
+    else
+      apply_prefix_kernel<<<grid_for(n * d * d, 256), 256, 0, st>>>(cP, cE, ls, n, cnt, D, d,
+                                                                    f32, d_out);
     CUDA_TRY(ctx, cudaGetLastError());
     ctx->launches += 2;
   } else {

@@ -1292,6 +1292,48 @@ __global__ void apply_prefix_kernel(const double2* __restrict__ P, const double2
   }
 }
 
+// The same product organised by lane: one CTA per lane; thread t owns
+// output column c = t % D and keeps column c of E_lane in registers, and the
+// CTA's 256 / D slice groups stream the lane's contiguous slices (the P_s
+// rows are read once per slice group through L1, broadcast to the D threads
+// of the slice; no per-element lane lookup).  Same summation order as cdot
+// (k ascending, same fma pattern): the last entry stays bitwise equal to the
+// sequential total.
+template <int D>
+__global__ void __launch_bounds__(256) apply_prefix_lanes_kernel(
+    const double2* __restrict__ P, const double2* __restrict__ E,
+    const int64_t* __restrict__ starts, int d, int to_fp32, void* __restrict__ out) {
+  constexpr int dd = D * D, G = 256 / D;
+  const int l = blockIdx.x;
+  const int c = threadIdx.x % D, j = threadIdx.x / D;
+  double2 ec[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) ec[k] = E[(int64_t)l * dd + k * D + c];
+  const int64_t s1 = starts[l + 1];
+  if (c >= d) return;
+  for (int64_t s = starts[l] + j; s < s1; s += G) {
+    const double2* ps = P + s * dd;
+    const int64_t o = s * (int64_t)d * d + c;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      if (r >= d) break;
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double2 a = ps[r * D + k];
+        re = fma(a.x, ec[k].x, re);
+        re = fma(-a.y, ec[k].y, re);
+        im = fma(a.x, ec[k].y, im);
+        im = fma(a.y, ec[k].x, im);
+      }
+      if (to_fp32)
+        reinterpret_cast<float2*>(out)[o + (int64_t)r * d] = make_float2((float)re, (float)im);
+      else
+        reinterpret_cast<double2*>(out)[o + (int64_t)r * d] = make_double2(re, im);
+    }
+  }
+}
+
 // pad a (cnt, d, d) complex128 batch to (cnt, D, D) by embedding in the
 // top-left corner with an identity tail, and the reverse extraction
 __global__ void embed_kernel(const double2* __restrict__ in, int cnt, int d, int D,
