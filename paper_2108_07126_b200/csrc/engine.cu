@@ -1378,8 +1378,7 @@ int equiprop_all_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
     else if (D == 8)
       apply_prefix_lanes_kernel<8><<<cnt, 256, 0, st>>>(cP, cE, ls, d, f32, d_out);
     else
-      apply_prefix_kernel<<<grid_for(n * d * d, 256), 256, 0, st>>>(cP, cE, ls, n, cnt, D, d,
-                                                                    f32, d_out);
+      return fail(ctx, SP_E_INTERNAL, "no plain-layout prefix application for D = %d", D);
     CUDA_TRY(ctx, cudaGetLastError());
     ctx->launches += 2;
   } else {

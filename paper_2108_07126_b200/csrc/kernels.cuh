@@ -1267,31 +1267,8 @@ __global__ void lane_starts_kernel(int64_t n, int lanes, int64_t* __restrict__ s
 }
 
 // cumulative products: out[s] = P[s] E[lane(s)] with P[s] the in-lane prefix,
-// written straight into the (n, d, d) output in the output dtype, one element
-// per thread (plain-layout families, D <= 8); the lane of slice s comes from a
-// floating-point estimate checked against the lane start table (no 64-bit
-// division per element)
-__global__ void apply_prefix_kernel(const double2* __restrict__ P, const double2* __restrict__ E,
-                                    const int64_t* __restrict__ starts, int64_t n, int lanes,
-                                    int D, int d, int to_fp32, void* __restrict__ out) {
-  const int64_t dd = (int64_t)D * D, od = (int64_t)d * d;
-  const double ratio = (double)lanes / (double)n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * od;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = e / od;
-    const int rc = (int)(e - s * od), r = rc / d, c = rc - r * d;
-    int64_t l = (int64_t)((double)s * ratio);
-    if (l >= lanes) l = lanes - 1;
-    while (l > 0 && starts[l] > s) --l;
-    while (l + 1 < lanes && starts[l + 1] <= s) ++l;
-    const double2 v = cdot(P + s * dd + (int64_t)r * D, E + l * dd, D, c, D);
-    if (to_fp32)
-      reinterpret_cast<float2*>(out)[e] = make_float2((float)v.x, (float)v.y);
-    else
-      reinterpret_cast<double2*>(out)[e] = v;
-  }
-}
-
+// written straight into the (n, d, d) output in the output dtype
+// (plain-layout families, D <= 8).
 // The same product organised by lane: one CTA per lane; thread t owns
 // output column c = t % D and keeps column c of E_lane in registers, and the
 // CTA's 256 / D slice groups stream the lane's contiguous slices (the P_s
