@@ -290,6 +290,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     lane_sync<C>();
     PH(1);
     // ---- 3. powers T_k = 2X T_{k-1} - T_{k-2}, k = 2..s
+    // (single-strip smem-resident families: 2X / 2y fragments in registers
+    // across their GEMMs)
+    constexpr bool RA = C::S == 1 && C::MT == 1 && C::XS && !AG;
+    constexpr int KBR = RA ? C::KB : 1;
+    double2 fR[KBR], fI[KBR];
+    if constexpr (RA) load_afrag_strip<C>(ax_off, fR, fI, ln);
     int pb = 0;
 #pragma unroll UNR
     for (int k = 2; k <= s; ++k) {
@@ -308,7 +314,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
       }
       PH(8);
-      tile_mma<C, AG>(gx, ax_off, bo(pb), accR, accI, ms0, nt0, ln);
+      if constexpr (RA)
+        tile_mma_ra<C>(fR, fI, bo(pb), accR, accI, nt0, ln);
+      else
+        tile_mma<C, AG>(gx, ax_off, bo(pb), accR, accI, ms0, nt0, ln);
       PH(2);
       if (k < s) {
         write_B(bo(pb ^ 1), accR, accI, 1.0);
@@ -323,6 +332,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     PH(8);
     sync_all();
     PH(3);
+    if constexpr (RA) load_afrag_strip<C>(ay_off, fR, fI, ln);
     // ---- 4. Clenshaw in y = T_s with matrix coefficients Q_j
     if (r == 1) {
       load_Q(0, accR, accI);
@@ -345,7 +355,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           }
         }
         PH(9);
-        tile_mma<C, AG>(gy, ay_off, bo(pc), accR, accI, ms0, nt0, ln);
+        if constexpr (RA)
+          tile_mma_ra<C>(fR, fI, bo(pc), accR, accI, nt0, ln);
+        else
+          tile_mma<C, AG>(gy, ay_off, bo(pc), accR, accI, ms0, nt0, ln);
         PH(4);
         if (j >= 1) {
           write_B(bo(pc ^ 1), accR, accI, (j == 1) ? 0.5 : 1.0);

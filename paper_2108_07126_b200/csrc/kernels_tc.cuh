@@ -73,6 +73,55 @@ __device__ __forceinline__ void tile_mma(const double* __restrict__ Ag, int a_of
   }
 }
 
+// tile_mma for a single 16-row strip (S = MT = 1) whose A fragments are
+// already in registers (aR/aI[kb] = the lane's re/im pair of k block kb):
+// 2X and 2y are the A operand of several GEMMs per slice
+template <class C>
+__device__ __forceinline__ void load_afrag_strip(int a_off, double2 (&aR)[C::KB],
+                                                 double2 (&aI)[C::KB], int ln) {
+  extern __shared__ __align__(16) double smem[];
+#pragma unroll
+  for (int kb = 0; kb < C::KB; ++kb) {
+    const int idx = (kb * 2) * 64 + 2 * ln;
+    aR[kb] = *reinterpret_cast<const double2*>(&smem[a_off + idx]);
+    aI[kb] = *reinterpret_cast<const double2*>(&smem[a_off + idx + 64]);
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void tile_mma_ra(const double2 (&aR)[C::KB],
+                                            const double2 (&aI)[C::KB], int b_off,
+                                            double (&accR)[C::NT * 4],
+                                            double (&accI)[C::NT * 4], int nt0, int ln) {
+  static_assert(C::S == 1 && C::MT == 1, "single strip");
+  extern __shared__ __align__(16) double smem[];
+  constexpr int NT = C::NT, KB = C::KB;
+#pragma unroll
+  for (int kb = 0; kb < KB; ++kb) {
+    double bR[NT], bI[NT];
+#pragma unroll
+    for (int jn = 0; jn < NT; ++jn) {
+      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 2) * 32 + ln;
+      bR[jn] = smem[bi];
+      bI[jn] = smem[bi + 32];
+    }
+#pragma unroll
+    for (int jn = 0; jn < NT; ++jn) {
+      double* cr = &accR[jn * 4];
+      double* ci = &accI[jn * 4];
+      dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aR[kb].x, aR[kb].y, bR[jn]);
+      dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aR[kb].x, aR[kb].y, bI[jn]);
+    }
+#pragma unroll
+    for (int jn = 0; jn < NT; ++jn) {
+      double* cr = &accR[jn * 4];
+      double* ci = &accI[jn * 4];
+      dmma_16x8x4(cr[0], cr[1], cr[2], cr[3], aI[kb].x, aI[kb].y, -bI[jn]);
+      dmma_16x8x4(ci[0], ci[1], ci[2], ci[3], aI[kb].x, aI[kb].y, bR[jn]);
+    }
+  }
+}
+
 // Clenshaw form (the reference's recurrence applied to the running product):
 // b_m = a_m V ; b_j = a_j V + 2X b_{j+1} - (j == 0 ? 2 : 1) b_{j+2} ; V = b_0.
 // m GEMMs per slice; see kernels.cuh for the lane/group structure.
