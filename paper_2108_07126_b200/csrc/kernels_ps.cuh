@@ -290,12 +290,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     lane_sync<C>();
     PH(1);
     // ---- 3. powers T_k = 2X T_{k-1} - T_{k-2}, k = 2..s
-    // (single-strip smem-resident families: 2X / 2y fragments in registers
-    // across their GEMMs)
-    constexpr bool RA = C::S == 1 && C::MT == 1 && C::XS && !AG;
+    // (smem-resident families, one strip per warp: 2X / 2y fragments in
+    // registers across their GEMMs)
+    // (measured: D16 -3.6%, D32 -2.2% at (s, r) = (3, 5); D32 +9% at (2, 4),
+    // where one power GEMM does not pay for the registers)
+    constexpr bool RA = C::MT == 1 && C::XS && !AG && (C::S == 1 || SC >= 3);
     constexpr int KBR = RA ? C::KB : 1;
     double2 fR[KBR], fI[KBR];
-    if constexpr (RA) load_afrag_strip<C>(ax_off, fR, fI, ln);
+    if constexpr (RA) load_afrag_strip<C>(ax_off, fR, fI, ms0, ln);
     int pb = 0;
 #pragma unroll UNR
     for (int k = 2; k <= s; ++k) {
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     PH(8);
     sync_all();
     PH(3);
-    if constexpr (RA) load_afrag_strip<C>(ay_off, fR, fI, ln);
+    if constexpr (RA) load_afrag_strip<C>(ay_off, fR, fI, ms0, ln);
     // ---- 4. Clenshaw in y = T_s with matrix coefficients Q_j
     if (r == 1) {
       load_Q(0, accR, accI);

@@ -73,16 +73,16 @@ __device__ __forceinline__ void tile_mma(const double* __restrict__ Ag, int a_of
   }
 }
 
-// tile_mma for a single 16-row strip (S = MT = 1) whose A fragments are
+// tile_mma for one 16-row strip per warp (MT = 1) whose A fragments are
 // already in registers (aR/aI[kb] = the lane's re/im pair of k block kb):
 // 2X and 2y are the A operand of several GEMMs per slice
 template <class C>
 __device__ __forceinline__ void load_afrag_strip(int a_off, double2 (&aR)[C::KB],
-                                                 double2 (&aI)[C::KB], int ln) {
+                                                 double2 (&aI)[C::KB], int ms0, int ln) {
   extern __shared__ __align__(16) double smem[];
 #pragma unroll
   for (int kb = 0; kb < C::KB; ++kb) {
-    const int idx = (kb * 2) * 64 + 2 * ln;
+    const int idx = ((ms0 * C::KB + kb) * 2) * 64 + 2 * ln;
     aR[kb] = *reinterpret_cast<const double2*>(&smem[a_off + idx]);
     aI[kb] = *reinterpret_cast<const double2*>(&smem[a_off + idx + 64]);
   }
@@ -93,7 +93,7 @@ __device__ __forceinline__ void tile_mma_ra(const double2 (&aR)[C::KB],
                                             const double2 (&aI)[C::KB], int b_off,
                                             double (&accR)[C::NT * 4],
                                             double (&accI)[C::NT * 4], int nt0, int ln) {
-  static_assert(C::S == 1 && C::MT == 1, "single strip");
+  static_assert(C::MT == 1, "one strip per warp");
   extern __shared__ __align__(16) double smem[];
   constexpr int NT = C::NT, KB = C::KB;
 #pragma unroll
