@@ -215,6 +215,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       lane_sync<C>();
 
     // ---- 4. m Clenshaw steps: new = 2X cur - beta old + a_j V
+    // (smem-resident, one strip per warp, D <= 32: the 2X fragments stay in
+    // registers for the m GEMMs; measured D16 -2.2%, D32 -1.1%, D64 +2.1%)
+    constexpr bool RA = C::MT == 1 && C::XS && !AG && C::GPL == 1 && C::KB <= 8;
+    constexpr int KBR = RA ? C::KB : 1;
+    double2 fR[KBR], fI[KBR];
+    if constexpr (RA) load_afrag_strip<C>(x_off, fR, fI, ms0, ln);
     for (int jj = m - 1; jj >= 0; --jj) {
       const double ar = job.coef[2 * jj], ai = job.coef[2 * jj + 1];
       const int Bo = bo(p ^ 1);
@@ -232,7 +238,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         accR[e] = fma(ar, Vr[e], fma(-ai, Vi[e], -beta * orr));
         accI[e] = fma(ar, Vi[e], fma(ai, Vr[e], -beta * oi));
       }
-      tile_mma<C, AG>(xg, x_off, bo(p), accR, accI, ms0, nt0, ln);
+      if constexpr (RA)
+        tile_mma_ra<C>(fR, fI, bo(p), accR, accI, nt0, ln);
+      else
+        tile_mma<C, AG>(xg, x_off, bo(p), accR, accI, ms0, nt0, ln);
       if (jj > 0) {
         // new iterate becomes "cur" for the next step (own positions only)
 #pragma unroll

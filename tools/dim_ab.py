@@ -1,6 +1,6 @@
 """A/B kernel timing of random systems across library builds.
 
-    python tools/dim_ab.py "d,n_ctrl,slices,prec;..." LIB1.so LIB2.so ...
+    python tools/dim_ab.py "d,n_ctrl,slices,prec[,algo];..." LIB1.so LIB2.so ...
 
 Each library runs in its own process (SLICEPROP_B200_LIB); best of 10
 kernel times (CUDA events inside the library) per case, and the first
@@ -19,9 +19,12 @@ import paper_2108_07126_b200 as sp
 from cases import random_inputs
 out = {}
 for case in CASES.split(";"):
-    d, nc, n, prec = case.split(",")
+    d, nc, n, prec, *rest = case.split(",")
     h0, hs, v, dt = random_inputs(int(d), int(nc), int(n), 1)
-    ctx = sp.create(precision=prec); ctx.set_hamiltonian(sp.ControlSystem(h0, hs)); ctx.set_profiling(True)
+    ctx = sp.create(precision=prec)
+    if rest:
+        ctx.set_algorithm(rest[0])
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs)); ctx.set_profiling(True)
     amps = sp.ControlAmplitudes(v, dt)
     r = ctx.equiprop(amps)
     best = 1e9
