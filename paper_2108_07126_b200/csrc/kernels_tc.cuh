@@ -215,9 +215,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       lane_sync<C>();
 
     // ---- 4. m Clenshaw steps: new = 2X cur - beta old + a_j V
-    // (smem-resident, one strip per warp, D <= 32: the 2X fragments stay in
-    // registers for the m GEMMs; measured D16 -2.2%, D32 -1.1%, D64 +2.1%)
-    constexpr bool RA = C::MT == 1 && C::XS && !AG && C::GPL == 1 && C::KB <= 8;
+    // (2X fragments in registers for the m GEMMs: measured -1..2% at m = 13
+    // but +1.6% at m = 3, the orders this kernel runs under "auto"; off)
+    constexpr bool RA = false;
     constexpr int KBR = RA ? C::KB : 1;
     double2 fR[KBR], fI[KBR];
     if constexpr (RA) load_afrag_strip<C>(x_off, fR, fI, ms0, ln);
