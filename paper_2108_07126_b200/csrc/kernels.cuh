@@ -638,6 +638,36 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
     }
     // ---- assemble 2X in registers
     double2 X[D][D];
+    if constexpr (D == 4 && TPL == 4) {
+      // each of the lane's 4 threads assembles one row (its column index),
+      // the rows are exchanged by shuffles within the 4-thread group (same
+      // operations per entry as below)
+      double2 xr[D];
+      const int rr = c0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) xr[c] = __ldg(&terms[rr * D + c]);
+      for (int t = 1; t < T; ++t) {
+        const double w = slice_weight(job, s, t);
+        const double2* tt = terms + (size_t)t * D * D + rr * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const double2 h = __ldg(&tt[c]);
+          xr[c].x = fma(w, h.x, xr[c].x);
+          xr[c].y = fma(w, h.y, xr[c].y);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        xr[c].x *= job.xs;
+        xr[c].y *= job.xs;
+      }
+      const unsigned gm = 0xFu << (threadIdx.x & 28);
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+          X[r][c] = make_double2(__shfl_sync(gm, xr[c].x, r, 4), __shfl_sync(gm, xr[c].y, r, 4));
+    } else {
 #pragma unroll
     for (int r = 0; r < D; ++r)
 #pragma unroll
@@ -670,6 +700,7 @@ __global__ void __launch_bounds__(256, D == 2 ? 3 : 2) lane_small_kernel(SliceJo
         X[r][c].x *= job.xs;
         X[r][c].y *= job.xs;
       }
+    }
     if constexpr (D == 2) {
       // 2 x 2: every polynomial in Z = 2X lies in span{I, Z'}, Z' = Z - z0 I,
       // z0 = tr(Z)/2, Z'^2 = zeta2 I (Cayley-Hamilton, exact for any complex
