@@ -24,6 +24,9 @@ enum D8Alg { D8_CLENSHAW = 0, D8_PS = 1, D8_PS3 = 2 };
 // doubles per warp: XA, YA, B0, B1 (np planes of 64) + 256 weights
 __host__ __device__ constexpr int d8_slot(int np) { return 4 * 64 * np + 256; }
 constexpr int D8_TSM = 16;              // expansion terms kept in shared memory (per CTA)
+#ifndef SP_D8_TR
+#define SP_D8_TR 4  // expansion terms kept in registers (lane entries)
+#endif
 
 // m8n8k4 fragment-native positions (0..63) of element (r, c)
 __device__ __forceinline__ int d8_apos(int r, int c) { return (c >> 2) * 32 + ((r << 2) | (c & 3)); }
@@ -173,24 +176,55 @@ __global__ void __launch_bounds__(32 * WPC) lane_d8_kernel(PSJob pj,
   // raw samples of weight ln (>= 1) of the next slice, loaded a slice ahead
   WRaw wr{};
   if (s0 < s1 && ln >= 1 && ln < T) wr = weight_gather(job, s0, ln);
+  // up to TR terms: the lane's own entries of every term stay in registers
+  // for the whole lane and the weights travel by shuffles (no shared-memory
+  // round trip on the assembly's critical path)
+  constexpr int TR = SP_D8_TR;
+  const bool treg = T <= TR;
+  double2 hreg[TR][2];
+#pragma unroll
+  for (int tt = 0; tt < TR; ++tt)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks)
+      hreg[tt][ks] = (treg && tt < T) ? tsrc[tt * 64 + ks * 32 + ln] : make_double2(0.0, 0.0);
 
   for (int64_t sl = s0; sl < s1; ++sl) {
     // ---- weights (xs folded in) and 2X (A-native, NP planes)
-    if (ln < T) W[ln] = (ln == 0) ? job.xs : job.xs * weight_combine(job, sl, ln, wr);
-    for (int tt = ln + 32; tt < T; tt += 32) W[tt] = job.xs * slice_weight(job, sl, tt);
+    double myw = 0.0;
+    if (ln < T) myw = (ln == 0) ? job.xs : job.xs * weight_combine(job, sl, ln, wr);
+    if (!treg) {
+      if (ln < T) W[ln] = myw;
+      for (int tt = ln + 32; tt < T; tt += 32) W[tt] = job.xs * slice_weight(job, sl, tt);
+    }
     if (sl + 1 < s1 && ln >= 1 && ln < T) wr = weight_gather(job, sl + 1, ln);
     __syncwarp();
+    double wv[TR];
+#pragma unroll
+    for (int tt = 0; tt < TR; ++tt) wv[tt] = __shfl_sync(0xffffffffu, myw, tt);
     double afx[2][3];  // this thread's fragments of 2X (it assembles exactly those)
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       const int i = ks * 32 + ln;
-      double2 h = tsrc[i];
-      double xr = W[0] * h.x, xi = W[0] * h.y;
+      double xr, xi;
+      if (treg) {
+        xr = wv[0] * hreg[0][ks].x;
+        xi = wv[0] * hreg[0][ks].y;
+#pragma unroll
+        for (int tt = 1; tt < TR; ++tt) {
+          if (tt >= T) break;
+          xr = fma(wv[tt], hreg[tt][ks].x, xr);
+          xi = fma(wv[tt], hreg[tt][ks].y, xi);
+        }
+      } else {
+        double2 h = tsrc[i];
+        xr = W[0] * h.x;
+        xi = W[0] * h.y;
 #pragma unroll 4
-      for (int tt = 1; tt < T; ++tt) {
-        h = tsrc[tt * 64 + i];
-        xr = fma(W[tt], h.x, xr);
-        xi = fma(W[tt], h.y, xi);
+        for (int tt = 1; tt < T; ++tt) {
+          h = tsrc[tt * 64 + i];
+          xr = fma(W[tt], h.x, xr);
+          xi = fma(W[tt], h.y, xi);
+        }
       }
       XA[i] = xr;
       XA[64 + i] = xi;
