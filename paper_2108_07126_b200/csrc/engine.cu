@@ -214,6 +214,12 @@ struct sp_ctx {
       fold_scratch, psA, tpriv, viol, terms3, tailctr, seqA, scanEin, lstarts, scanS, scanA;
   cudaStream_t viol_stream = nullptr;
   int64_t viol_pts = 0;
+  // page-locked copy of the violation slots: the host entry points fetch it
+  // with the result before their one stream synchronisation
+  unsigned long long* viol_host = nullptr;
+  // page-locked staging of the d x d result of the host entry points
+  void* out_host = nullptr;
+  size_t out_host_bytes = 0;
   int algo = 0;          // Algo
   int last_algo = 0;     // algorithm of the last lane pass
   int last_gemms = 0;    // GEMMs per slice of the last lane pass
@@ -1077,12 +1083,19 @@ int arm_validation(sp_ctx* ctx, SliceJob* job, cudaStream_t st, bool fused = fal
 
 // after the stream work: SP_E_AMPLITUDE_BOUND with the reference's message
 // (hamiltonian.py:165-174) if any sample was outside [-1, 1]
-int read_violation(sp_ctx* ctx, const double* host_amps, int64_t* index_out) {
+// (fetched: the slots were copied into ctx->viol_host on the call's stream and
+// that stream has been synchronised)
+int read_violation(sp_ctx* ctx, const double* host_amps, int64_t* index_out,
+                   bool fetched = false) {
   unsigned long long v = ~0ull;
   if (ctx->viol.p) {
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->viol_stream));
     unsigned long long slots[3];
-    CUDA_TRY(ctx, cudaMemcpy(slots, ctx->viol.p, sizeof(slots), cudaMemcpyDeviceToHost));
+    if (fetched) {
+      for (int i = 0; i < 3; ++i) slots[i] = ctx->viol_host[i];
+    } else {
+      CUDA_TRY(ctx, cudaStreamSynchronize(ctx->viol_stream));
+      CUDA_TRY(ctx, cudaMemcpy(slots, ctx->viol.p, sizeof(slots), cudaMemcpyDeviceToHost));
+    }
     v = std::min(slots[0], std::min(slots[1], slots[2]));
   }
   if (index_out) *index_out = (v == ~0ull) ? -1 : (int64_t)v;
@@ -1095,6 +1108,15 @@ int read_violation(sp_ctx* ctx, const double* host_amps, int64_t* index_out) {
                 host_amps[v], k, i);
   return fail(ctx, SP_E_AMPLITUDE_BOUND,
               "control amplitude at sample %lld, control %lld lies outside [-1, 1]", k, i);
+}
+
+// queue the copy of the violation slots into page-locked host memory
+int fetch_violation(sp_ctx* ctx, cudaStream_t st) {
+  if (!ctx->viol.p) return SP_OK;
+  if (!ctx->viol_host) CUDA_TRY(ctx, cudaMallocHost((void**)&ctx->viol_host, 4 * sizeof(unsigned long long)));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->viol_host, ctx->viol.p, 3 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, st));
+  return SP_OK;
 }
 
 int prepare_device(sp_ctx* ctx) {
@@ -1468,6 +1490,8 @@ int sp_free(sp_ctx* ctx) {
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->viol_host) cudaFreeHost(ctx->viol_host);
+    if (ctx->out_host) cudaFreeHost(ctx->out_host);
   }
   delete ctx;
   return SP_OK;
@@ -1556,9 +1580,19 @@ int sp_equiprop(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double
   rc = equiprop_dev(ctx, (const double*)ctx->amps.p, pts, n_ctrl, dt, plan, reduction,
                     ctx->out.p, st);
   if (rc) return rc;
-  CUDA_TRY(ctx, cudaMemcpyAsync(u_out, ctx->out.p, obytes, cudaMemcpyDeviceToHost, st));
+  if (ctx->out_host_bytes < obytes) {
+    if (ctx->out_host) cudaFreeHost(ctx->out_host);
+    ctx->out_host = nullptr;
+    ctx->out_host_bytes = 0;
+    CUDA_TRY(ctx, cudaMallocHost(&ctx->out_host, obytes));
+    ctx->out_host_bytes = obytes;
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->out_host, ctx->out.p, obytes, cudaMemcpyDeviceToHost, st));
+  rc = fetch_violation(ctx, st);
+  if (rc) return rc;
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
-  return read_violation(ctx, amps, nullptr);
+  std::memcpy(u_out, ctx->out_host, obytes);
+  return read_violation(ctx, amps, nullptr, true);
 }
 
 int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
