@@ -205,6 +205,7 @@ class IntegratorContext:
         self._effective = effective
         self._magnus = magnus
         self._quadrature = quadrature
+        self._plan_cache = None  # the bound depends on the system and the mode
         self._state = _LOADED
 
     def close(self) -> None:
@@ -245,8 +246,21 @@ class IntegratorContext:
         return spectral_bound(self._system, step)
 
     def plan_for(self, dt: float) -> ChebyshevPlan:
+        # the plan depends only on dt for a loaded system: the last one is
+        # kept (with its native struct) for repeated calls at the same step
+        cache = getattr(self, "_plan_cache", None)
+        if cache is not None and cache[0] == dt and cache[1] is self._system:
+            return cache[2]  # (set_hamiltonian clears the cache)
         beta = self.bound(dt)
-        return make_plan(-beta, beta, self.precision, m_max=self.m_max)
+        plan = make_plan(-beta, beta, self.precision, m_max=self.m_max)
+        self._plan_cache = (dt, self._system, plan, plan.to_native())
+        return plan
+
+    def _native_plan(self, plan: ChebyshevPlan):
+        cache = getattr(self, "_plan_cache", None)
+        if cache is not None and cache[2] is plan:
+            return cache[3]
+        return plan.to_native()
 
     def _prepare(self, amps: ControlAmplitudes):
         self._require_loaded()
@@ -336,7 +350,7 @@ class IntegratorContext:
                                     plan=None)
         count, plan = self._prepare(amps)
         out = np.empty((d, d), dtype=self._out_dtype())
-        native = plan.to_native()
+        native = self._native_plan(plan)
         rc = lib.sp_equiprop(self._handle, amps.values.ctypes.data_as(ctypes.c_void_p),
                              amps.pts, amps.n_controls, amps.dt, ctypes.byref(native),
                              REDUCTION[reduction], out.ctypes.data_as(ctypes.c_void_p))
@@ -354,7 +368,7 @@ class IntegratorContext:
                                     slice_count=0, plan=None)
         count, plan = self._prepare(amps)
         out = np.empty((count, d, d), dtype=self._out_dtype())
-        native = plan.to_native()
+        native = self._native_plan(plan)
         rc = lib.sp_equiprop_all(self._handle, amps.values.ctypes.data_as(ctypes.c_void_p),
                                  amps.pts, amps.n_controls, amps.dt, ctypes.byref(native),
                                  out.ctypes.data_as(ctypes.c_void_p))
@@ -376,7 +390,7 @@ class IntegratorContext:
                              f"system has {self._system.n_controls}")
         count = self.slice_count(pts) if pts else 0
         plan = plan or self.plan_for(dt)
-        native = plan.to_native()
+        native = self._native_plan(plan)
         check(lib.sp_equiprop_device(self._handle, ctypes.c_void_p(amps_ptr), int(pts),
                                      int(n_ctrl), float(dt), ctypes.byref(native),
                                      REDUCTION[reduction], ctypes.c_void_p(out_ptr),
@@ -395,7 +409,7 @@ class IntegratorContext:
                              f"system has {self._system.n_controls}")
         count = self.slice_count(pts) if pts else 0
         plan = plan or self.plan_for(dt)
-        native = plan.to_native()
+        native = self._native_plan(plan)
         check(lib.sp_equiprop_all_device(self._handle, ctypes.c_void_p(amps_ptr), int(pts),
                                          int(n_ctrl), float(dt), ctypes.byref(native),
                                          ctypes.c_void_p(out_ptr), ctypes.c_void_p(stream)),
