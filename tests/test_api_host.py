@@ -276,3 +276,21 @@ class TestBindingErrors:
         assert seen["code"] == "state-machine"
         s.close()
         assert s.closed
+
+
+def test_plan_cache_follows_the_loaded_system():
+    """The host caches the last plan per step size; set_hamiltonian clears
+    it (the bound depends on the system and the mode)."""
+    sz = np.array([[1.0, 0.0], [0.0, -1.0]], dtype=complex)
+    sx = np.array([[0.0, 1.0], [1.0, 0.0]], dtype=complex)
+    ctx = sp.create()
+    ctx.set_hamiltonian(sp.ControlSystem(sz / 2, [sx / 2]))
+    p1 = ctx.plan_for(0.1)
+    assert ctx.plan_for(0.1) is p1
+    assert ctx.plan_for(0.2).beta == pytest.approx(2 * p1.beta)
+    ctx.set_hamiltonian(sp.ControlSystem(sz / 2, [sx / 2]), magnus=True)
+    p2 = ctx.plan_for(0.1)
+    assert p2 is not p1 and p2.beta != p1.beta
+    ctx.set_hamiltonian(sp.ControlSystem(2 * sz, [sx / 2]))
+    assert ctx.plan_for(0.1).beta > p1.beta
+    ctx.close()
