@@ -264,3 +264,26 @@ def test_driven_qubit_against_extended_precision_oracle(pts):
     err_gpu = rel_fro(got, exact)
     assert err_gpu <= max(2.0 * err_ref, 1e-15), (err_gpu, err_ref)
     ctx.close()
+
+
+@pytest.mark.parametrize("d", [2, 3, 4, 8, 16, 32])
+def test_cumulative_complex64_against_oracle(d):
+    """complex64 contexts (FP64 kernels, fp32 plan, complex64 output):
+    the cumulative stack against the oracle's fp32 restatement within the
+    complex64 gate, and the last entry equal to the sequential total."""
+    import oracle
+    from cases import random_inputs
+    h0, hs, values, dt = random_inputs(d, 2, 300, 9100 + d)
+    ref_all, _, _ = oracle.equiprop_all(h0, hs, values, dt, bits=32)
+    ref, _, _ = oracle.equiprop(h0, hs, values, dt, bits=32)
+    ref_seq, _, _ = oracle.equiprop(h0, hs, values, dt, bits=32, reduction="sequential")
+    tol, _ = parity_tolerance(ref, ref_seq, "fp32")
+    ctx = sp.create(precision="fp32")
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+    amps = sp.ControlAmplitudes(values, dt)
+    cum = ctx.equiprop_all(amps)
+    assert cum.u_all.dtype == np.complex64 and cum.u_all.shape == ref_all.shape
+    for k in (0, 1, 77, 150, 299):
+        assert rel_fro(cum.u_all[k], ref_all[k]) <= tol, k
+    assert np.array_equal(cum.final, ctx.equiprop(amps, reduction="sequential").u)
+    ctx.close()
