@@ -172,7 +172,7 @@ def test_d2_paths_against_oracle(pts, hermitian_exact):
 
 
 @pytest.mark.parametrize("d", [1, 2, 3, 6, 8, 12, 24, 40, 96])
-@pytest.mark.parametrize("mode", ["midpoint", "magnus"])
+@pytest.mark.parametrize("mode", ["midpoint", "simpson", "magnus"])
 def test_cumulative_every_family_against_oracle(d, mode):
     """equiprop_all for every kernel family (plain-layout d <= 8, DMMA
     prefix application above) against the oracle's cumulative stack, and the
@@ -186,7 +186,8 @@ def test_cumulative_every_family_against_oracle(d, mode):
     ref_seq, _, _ = oracle.equiprop(h0, hs, values, dt, mode=mode, reduction="sequential")
     tol, _ = parity_tolerance(ref, ref_seq, "fp64")
     ctx = sp.create()
-    ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus")
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                        quadrature=None if mode == "magnus" else mode)
     amps = sp.ControlAmplitudes(values, dt)
     cum = ctx.equiprop_all(amps)
     assert cum.u_all.shape == ref_all.shape
