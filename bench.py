@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Benchmark of the equiprop hot path on B200 (contract: see DESIGN.md §Measurement).
+"""Benchmark of the equiprop hot path on B200 (contract: see DESIGN.md §7).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU)
@@ -7,21 +7,25 @@
 Headline workload (BASELINE.json configs[3], the largest single-GPU config):
 C4 = dim-128 random unit-1-norm system, 4 controls, 1e6 slices, midpoint,
 complex128, beta = 0.5 (m = 13), time-sharded over the N GPUs (strong
-scaling: 1e6 slices in total).  Secondary lines (same JSON, "per_dim"): C3
-(dim 32, 2 controls, 1e6 slices; random and the coupled-spin chain of
-configs[2]), C1 (the paper's driven qubit, dim 2,
-1e5 slices) and c1m (the same qubit at the north star's 1e6 slices).
-A step is one full propagation U = U_{n-1} ... U_0 of the workload; value = slices / device time (CUDA events, max over ranks), with
-the amplitude table resident in HBM and L2 flushed between timed steps.
+scaling: 1e6 slices in total).  Secondary lines (same JSON, "per_dim"): the
+C4 magnus variant (pts = 2e6 + 1, 15 expansion terms, m = 15), C3 (dim 32,
+2 controls, 1e6 slices; random and the coupled-spin chain of configs[2]), C1
+(the paper's driven qubit, dim 2, 1e5 slices) and c1m (the same qubit at the
+north star's 1e6 slices).  A step is one full propagation U = U_{n-1} ... U_0
+of the workload; value = slices / device time (CUDA events, max over ranks),
+with the amplitude table resident in HBM and L2 flushed between timed steps.
 e2e = the same through the public API with the table in page-locked host
 memory (H2D + kernels + gather + D2H inside the timed region, wall clock,
 max over ranks).
 
---impl reference times the reference algorithm on the host cores: the CPU
-oracle (oracle/, a bit-exact numpy restatement of sliceprop 0.1.0, which
-itself cannot travel to the GPU box) on a bounded prefix of the same
-workload, extrapolated linearly (runtime linear in slices is a reference
-property, test_acceptance.py:229-245).
+The CPU side is the UNMODIFIED reference (sliceprop 0.1.0, pure Python +
+numpy/OpenBLAS) installed under baseline/_ref (tools/install_reference.sh),
+driven through its own public API (create / set_hamiltonian / equiprop) on a
+bounded prefix of the same workload; the oracle port (oracle/) stands in only
+if that install is missing.  The same prefix run on the GPU gives the
+``parity`` object of every line (rel-Frobenius vs the reference, with the
+reference's own pairwise-vs-sequential noise eps_self beside it).
+``--impl reference`` is that CPU arm alone; it never imports this package.
 """
 
 from __future__ import annotations
@@ -38,57 +42,120 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 METRIC = "time slices/sec (complex128) at dim 2/32/128, 1/2/4/8 B200; % FP64 roofline"
 UNIT = "slices/s"
 SEED = 20240911
 
 WORKLOADS = {
-    "c4": dict(d=128, n_ctrl=4, slices=1_000_000, kind="random",
+    "c4": dict(d=128, n_ctrl=4, slices=1_000_000, kind="random", mode="midpoint",
                label="C4: dim-128 random unit-norm system, 4 controls, 1e6 slices, midpoint, "
                      "complex128, beta=0.5 (m=13)"),
-    "c3": dict(d=32, n_ctrl=2, slices=1_000_000, kind="random",
+    "c4m": dict(d=128, n_ctrl=4, slices=1_000_000, kind="random", mode="magnus",
+                label="C4 magnus variant: dim-128 random unit-norm system, 4 controls, "
+                      "pts=2e6+1 (1e6 doubled steps), 4th-order Magnus (15 terms), "
+                      "complex128 (m=15)"),
+    "c3": dict(d=32, n_ctrl=2, slices=1_000_000, kind="random", mode="midpoint",
                label="C3: dim-32 random unit-norm system, 2 controls, 1e6 slices, midpoint, "
                      "complex128, beta=0.5 (m=13)"),
-    "c3s": dict(d=32, n_ctrl=2, slices=1_000_000, kind="spin",
+    "c3s": dict(d=32, n_ctrl=2, slices=1_000_000, kind="spin", mode="midpoint",
                 label="C3 physics variant: 5-spin coupled chain (d=32, 2 controls, "
                       "cos/sin drive over T=6), 1e6 slices, midpoint, complex128"),
-    "c1": dict(d=2, n_ctrl=2, slices=100_000, kind="qubit",
+    "c1": dict(d=2, n_ctrl=2, slices=100_000, kind="qubit", mode="midpoint",
                label="C1: paper's driven qubit (w0=1, w1=0.1, wrf=1, T=6), dim 2, 2 controls, "
                      "1e5 slices, midpoint, complex128 (m=3)"),
-    "c1m": dict(d=2, n_ctrl=2, slices=1_000_000, kind="qubit",
+    "c1m": dict(d=2, n_ctrl=2, slices=1_000_000, kind="qubit", mode="midpoint",
                 label="north-star d=2 target: the driven qubit at 1e6 slices, midpoint, "
                       "complex128 (m=3)"),
 }
 
+# secondary lines whose steps are seconds long run fewer timed steps
+SECONDARY_MAX_STEPS = {"c4m": 5}
 
-def fp64_peak():
+
+def fp64_peaks():
     with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
         return json.load(fh)
 
 
+# ---------------------------------------------------------------------------
+# synthetic inputs (numpy only: the reference arm must not load this package)
+# ---------------------------------------------------------------------------
+
+PAULI_X = np.array([[0.0, 1.0], [1.0, 0.0]], dtype=complex)
+PAULI_Y = np.array([[0.0, -1.0j], [1.0j, 0.0]], dtype=complex)
+PAULI_Z = np.array([[1.0, 0.0], [0.0, -1.0]], dtype=complex)
+
+
+def _one_norm(m):
+    return float(np.abs(m).sum(axis=0).max())
+
+
+def _site_op(p, i, n):
+    out = np.ones((1, 1), dtype=complex)
+    for k in range(n):
+        out = np.kron(out, p if k == i else np.eye(2, dtype=complex))
+    return out
+
+
+def _drive(pts, mode, duration=6.0, wrf=1.0):
+    """DrivenQubit sampling (reference studies.py:77-90)."""
+    if mode == "midpoint":
+        dt = duration / max(pts, 1)
+        t = (np.arange(pts) + 0.5) * dt
+    else:
+        dt = duration / (pts - 1)
+        t = np.arange(pts) * dt
+    return np.column_stack([np.cos(wrf * t), np.sin(wrf * t)]), dt
+
+
 def make_problem(wl):
-    """(system, amplitude table, dt) — deterministic synthetic inputs."""
-    import paper_2108_07126_b200 as sp
+    """(H0, [H_k], amplitude table, dt) — deterministic synthetic inputs.
+
+    random: reference bench_grid's unit 1-norm systems (studies.py:248-253)
+    with N controls, seed 20240911, dt = 0.5 / sum of 1-norms (beta = 0.5 for
+    midpoint), uniform(-1, 1) amplitudes; qubit: DrivenQubit(1, 0.1, 1, 6)
+    (studies.py:51-90); spin: the 5-spin chain of SpinChain."""
+    mode = wl["mode"]
+    pts = wl["slices"] if mode == "midpoint" else 2 * wl["slices"] + 1
     if wl["kind"] == "qubit":
-        q = sp.DrivenQubit(1.0, 0.1, 1.0, 6.0)
-        amps = q.amplitudes(wl["slices"])
-        return q.system(), np.ascontiguousarray(amps.values), amps.dt
+        values, dt = _drive(pts, mode)
+        return (0.5 * PAULI_Z, [0.05 * PAULI_X, 0.05 * PAULI_Y],
+                np.ascontiguousarray(values), dt)
     if wl["kind"] == "spin":
-        c = sp.SpinChain()
-        amps = c.amplitudes(wl["slices"])
-        return c.system(), np.ascontiguousarray(amps.values), amps.dt
+        n = 5
+        h0 = sum(0.5 * (1.0 + 0.05 * i) * _site_op(PAULI_Z, i, n) for i in range(n))
+        for i in range(n - 1):
+            for p in (PAULI_X, PAULI_Y, PAULI_Z):
+                h0 = h0 + 0.025 * (_site_op(p, i, n) @ _site_op(p, i + 1, n))
+        hx = sum(0.05 * _site_op(PAULI_X, i, n) for i in range(n))
+        hy = sum(0.05 * _site_op(PAULI_Y, i, n) for i in range(n))
+        values, dt = _drive(pts, mode)
+        return h0, [hx, hy], np.ascontiguousarray(values), dt
     rng = np.random.default_rng(SEED)
-    from paper_2108_07126_b200.studies import random_system
-    system = random_system(rng, wl["d"], wl["n_ctrl"])
-    dt = 0.5 / sum(system.norms)
-    values = rng.uniform(-1.0, 1.0, (wl["slices"], wl["n_ctrl"]))
-    return system, values, dt
+    d = wl["d"]
+
+    def unit_hermitian():
+        a = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+        h = 0.5 * (a + a.conj().T)
+        return h / _one_norm(h)
+
+    h0 = unit_hermitian()
+    hs = [unit_hermitian() for _ in range(wl["n_ctrl"])]
+    dt = 0.5 / sum(_one_norm(h) for h in [h0, *hs])
+    values = rng.uniform(-1.0, 1.0, (pts, wl["n_ctrl"]))
+    return h0, hs, values, dt
 
 
 def canonical_flops(d, m, n_terms):
     """F(d, m, T) = 8 d^3 (m + 1) + 4 d^2 T per slice."""
     return 8.0 * d ** 3 * (m + 1) + 4.0 * d * d * n_terms
+
+
+def n_terms_for(wl):
+    n = wl["n_ctrl"]
+    return 2 * n + n * (n - 1) // 2 + 1 if wl["mode"] == "magnus" else n + 1
 
 
 class Clocks:
@@ -140,22 +207,9 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample_rate(system, values, dt, target_s=8.0, max_slices=50_000):
-    """Oracle (reference algorithm, numpy/OpenBLAS, all host threads) on a
-    bounded prefix; returns (slices/s, slices timed, seconds, threads)."""
-    import oracle
-    h0, hs = system.drift, list(system.controls)
-    n0 = 64 if system.dim >= 64 else 4096
-    oracle.equiprop(h0, hs, values[:n0 // 4], dt, mode="midpoint")  # warm BLAS threads
-    t0 = time.perf_counter()
-    oracle.equiprop(h0, hs, values[:n0], dt, mode="midpoint")
-    per = (time.perf_counter() - t0) / n0
-    n = int(max(n0, min(max_slices, values.shape[0], target_s / max(per, 1e-9))))
-    t0 = time.perf_counter()
-    oracle.equiprop(h0, hs, values[:n], dt, mode="midpoint")
-    sec = time.perf_counter() - t0
-    return n / sec, n, sec, blas_threads()
-
+# ---------------------------------------------------------------------------
+# the CPU side: the unmodified reference (baseline/_ref), else the oracle port
+# ---------------------------------------------------------------------------
 
 def blas_threads():
     try:
@@ -166,42 +220,121 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
+class CpuArm:
+    """One equiprop of the reference on a prefix of the workload.
+
+    kind "reference": ``sliceprop`` imported from baseline/_ref through its
+    public API (create / set_hamiltonian / ControlAmplitudes / equiprop,
+    propagator.py:279-308); kind "port": the oracle restatement."""
+
+    def __init__(self, h0, hs, dt, mode):
+        self.h0, self.hs, self.dt, self.mode = h0, hs, dt, mode
+        self.kind, self.ref, self.where = "port", None, "oracle/ (numpy restatement)"
+        if os.path.isdir(os.path.join(REF_DIR, "sliceprop")):
+            if REF_DIR not in sys.path:
+                sys.path.insert(0, REF_DIR)
+            try:
+                import sliceprop
+                if os.path.abspath(sliceprop.__file__).startswith(REF_DIR):
+                    self.ref, self.kind = sliceprop, "reference"
+                    self.where = f"sliceprop {getattr(sliceprop, '__version__', '?')} " \
+                                 "(baseline/_ref, unmodified reference)"
+            except Exception as exc:  # fall back to the port, say why
+                self.where = f"oracle/ (reference import failed: {exc})"
+        if self.ref is not None:
+            self.ctx = self.ref.create()
+            self.ctx.set_hamiltonian(self.ref.ControlSystem(h0, hs), magnus=mode == "magnus",
+                                     quadrature=None if mode == "magnus" else mode)
+
+    def pts_for(self, slices):
+        return slices if self.mode == "midpoint" else 2 * slices + 1
+
+    def run(self, values, reduction="pairwise"):
+        if self.ref is not None:
+            amps = self.ref.ControlAmplitudes(values, self.dt)
+            return self.ctx.equiprop(amps, reduction=reduction).u
+        import oracle
+        u, _, _ = oracle.equiprop(self.h0, self.hs, values, self.dt, mode=self.mode,
+                                  reduction=reduction)
+        return u
+
+    def sample(self, values, target_s, repeats=3, max_slices=2_000_000):
+        """Bounded sample: one calibration call, then `repeats` timed calls of
+        the prefix sized to ~target_s / repeats each.  Returns a dict with the
+        rate, the prefix length and its pairwise output."""
+        n_avail = values.shape[0] if self.mode == "midpoint" else (values.shape[0] - 1) // 2
+        n0 = min(n_avail, 64 if self.h0.shape[0] >= 64 else 2048)
+        t0 = time.perf_counter()
+        self.run(values[:self.pts_for(n0)])
+        per = (time.perf_counter() - t0) / n0
+        n = int(max(n0, min(max_slices, n_avail, target_s / repeats / max(per, 1e-9))))
+        prefix = values[:self.pts_for(n)]
+        times, u = [], None
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            u = self.run(prefix)
+            times.append(time.perf_counter() - t0)
+        sec = statistics.median(times)
+        return {"rate": n / sec, "slices": n, "sec": sec, "repeats": repeats, "u": u,
+                "prefix": prefix, "threads": blas_threads()}
+
+    def baseline(self, s, full_slices):
+        return {"value": s["rate"], "unit": UNIT, "cores": s["threads"], "kind": self.kind,
+                "sample": f"first {s['slices']} of {full_slices} slices of the workload "
+                          f"({'full workload' if s['slices'] >= full_slices else 'prefix'}), "
+                          f"median of {s['repeats']} calls ({s['sec']:.2f} s each) of "
+                          f"{self.where}, OpenBLAS {s['threads']} threads on "
+                          f"{os.cpu_count()} host cpus"}
+
+    def close(self):
+        if self.ref is not None:
+            self.ctx.close()
+
+
 def run_reference(args):
-    """--impl reference: rank 0 times the reference algorithm on the host."""
+    """--impl reference: rank 0 times the reference on the host cores (the
+    other ranks exit without work).  Never imports paper_2108_07126_b200."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
     wl = WORKLOADS[args.workload]
-    system, values, dt = make_problem(wl)
-    import oracle
-    h0, hs = system.drift, list(system.controls)
-    _, n, sec, threads = cpu_sample_rate(system, values, dt, target_s=args.cpu_seconds)
+    h0, hs, values, dt = make_problem(wl)
+    arm = CpuArm(h0, hs, dt, wl["mode"])
+    cal = arm.sample(values, args.cpu_seconds, repeats=1)
+    n = cal["slices"]
+    prefix = cal["prefix"]
     for _ in range(args.warmup):
-        oracle.equiprop(h0, hs, values[:max(1, n // 4)], dt, mode="midpoint")
+        arm.run(prefix[:arm.pts_for(max(1, n // 4))])
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.equiprop(h0, hs, values[:n], dt, mode="midpoint")
+        arm.run(prefix)
         times.append(time.perf_counter() - t0)
     rate = n / statistics.median(times)
-    per_step_full_ms = wl["slices"] / rate * 1e3
+    threads = blas_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_step_full_ms, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": wl["slices"] / rate * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
         "config": {"workload": wl["label"], "dim": wl["d"], "n_ctrl": wl["n_ctrl"],
-                   "slices": wl["slices"], "mode": "midpoint",
-                   "sample_slices_per_step": n,
-                   "note": "ms_per_step extrapolated linearly from the sample"},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                   "slices": wl["slices"], "mode": wl["mode"],
+                   "sample_slices_per_step": n, "same_config": n >= wl["slices"],
+                   "note": "each step propagates the first sample_slices_per_step slices; "
+                           "ms_per_step is extrapolated linearly to the full workload "
+                           "(linear runtime: reference test_acceptance.py:229-245)"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": arm.kind,
                          "sample": f"first {n} slices of the workload per step, median of "
-                                   f"{args.steps} steps, oracle/ numpy restatement of the "
-                                   f"reference (OpenBLAS {threads} threads, host "
-                                   f"{os.cpu_count()} cpus)"},
+                                   f"{args.steps} steps, {arm.where}, OpenBLAS {threads} "
+                                   f"threads, host {os.cpu_count()} cpus"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    arm.close()
     print(json.dumps(line), flush=True)
 
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
 
 def max_over_ranks(dist, vals, dev):
     import torch
@@ -211,29 +344,71 @@ def max_over_ranks(dist, vals, dev):
     return red.tolist()
 
 
-def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
+def roofline_for(t, local_slices, wl, m, kern_ms, peaks):
+    """Dominant-kernel roofline.  frac = EXECUTED FP64 flops of the launch
+    (the instructions the kernel issues: PS / 3M forms, Cayley-Hamilton
+    pairs) / duration / the measured peak of the pipe it runs on (DFMA for
+    the register families d <= 4, DMMA above); canonical_frac = the
+    reference-algorithm work F(d, m, T) of SURVEY.md §8(d) on the same
+    denominator (above 1 when the kernel needs fewer flops than the
+    reference's Clenshaw count)."""
+    dfma = t["kernel"].startswith("lane_small")
+    peak = (peaks["fp64_dfma_tflops"] if dfma else peaks["fp64_dmma_tflops"]) * 1e12
+    F = canonical_flops(wl["d"], m, n_terms_for(wl))
+    executed = t["executed_flops"] / (kern_ms / 1e3)
+    canonical = local_slices * F / (kern_ms / 1e3)
+    traffic, traffic_note = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            cap = json.load(fh).get(t["kernel"])
+        if cap:
+            traffic = cap["dram_bytes"] * local_slices / cap["slices"]
+            traffic_note = (f"ncu --set full dram read+write of one launch at {cap['slices']} "
+                            f"slices ({cap['dram_bytes']:.3g} B), scaled linearly to this launch; "
+                            f"algorithmic bytes/slice = {8 * wl['n_ctrl']} (amplitude row)")
+    except (OSError, ValueError, KeyError):
+        pass
+    return {"bound": "tensor", "achieved": executed / 1e12, "peak": peak / 1e12,
+            "unit": "TFLOP/s", "frac": executed / peak, "traffic": traffic,
+            "traffic_note": traffic_note, "kernel": t["kernel"], "kernel_ms": kern_ms,
+            "executed_flops_per_launch": t["executed_flops"],
+            "canonical_achieved": canonical / 1e12, "canonical_frac": canonical / peak,
+            "canonical_flops_per_launch": local_slices * F,
+            "pipe": "FP64 DFMA (CUDA cores)" if dfma else "FP64 DMMA (mma.sync f64)",
+            "peak_source": "measured FP64 " + ("DFMA" if dfma else "DMMA")
+                           + " peak (tools/fp64_peak.cu, profiles/fp64_peak.json; "
+                             "MEASURED_PEAKS.json has no FP64 entry)"}
+
+
+def measure_gpu(args, name, rank, world, local_rank, dist, headline):
     import torch
 
     import paper_2108_07126_b200 as sp
     from paper_2108_07126_b200.sharding import (equiprop_sharded_device, partition,
                                                 shard_rows)
-    system, values, dt = make_problem(wl)
-    d, n = system.dim, values.shape[0]
+    wl = WORKLOADS[name]
+    steps = args.steps if headline else min(args.steps, SECONDARY_MAX_STEPS.get(name, 10**9))
+    h0, hs, values, dt = make_problem(wl)
+    mode = wl["mode"]
+    system = sp.ControlSystem(h0, hs)
+    d = system.dim
+    n = wl["slices"]
     ctx = sp.create(device=local_rank)
-    ctx.set_hamiltonian(system)
+    ctx.set_hamiltonian(system, magnus=mode == "magnus",
+                        quadrature=None if mode == "magnus" else mode)
     ctx.set_profiling(True)
     plan = ctx.plan_for(dt)
     a, b = partition(n, world)[rank]
-    lo, hi = shard_rows("midpoint", a, b)
+    lo, hi = shard_rows(mode, a, b)
     local = np.ascontiguousarray(values[lo:hi])
     dev = torch.device("cuda", local_rank)
-    d_amps = torch.from_numpy(local).to(dev)
+    d_amps = torch.from_numpy(local.copy()).to(dev)
     out = torch.empty((d, d), dtype=torch.complex128, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
     stream = torch.cuda.current_stream(dev)
 
     # amplitude validation (|c| <= 1) is part of the job: it runs inside the
-    # lane kernel and its flag is read after each timed step (sp_amplitude_violation)
+    # lane kernel and its flag is read after each timed step
     def validate():
         if ctx.amplitude_violation() >= 0:
             raise sp.AmplitudeBoundError("amplitude outside [-1, 1]")
@@ -251,11 +426,12 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
     torch.cuda.synchronize(dev)
     t = ctx.last_timing()
     launches_per_step = t["launches"]
+    lanes = ctx.last_lanes()
     # launch-latency-bound secondary workloads (C1: ~10 us of GPU work per
     # step) replay the step as a CUDA graph, the way a serving loop would;
     # the headline step (seconds of GPU work) is launched directly
     graph = None
-    if world == 1 and not headline and not args.no_graph:
+    if world == 1 and not headline and not args.no_graph and wl["d"] <= 32:
         try:
             ctx.set_profiling(False)
             cap = torch.cuda.Stream(dev)
@@ -276,10 +452,10 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
         dist.barrier()
     torch.cuda.synchronize(dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+           for _ in range(steps)]
     kernel_ms, launches = [], 0
     with Clocks(local_rank) as clk:
-        for k in range(args.steps):
+        for k in range(steps):
             flush.fill_(float(k))
             evs[k][0].record(stream)
             if graph is not None:
@@ -291,9 +467,9 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
                 stream.synchronize()
                 launches += launches_per_step
             else:
-                t = ctx.last_timing()
-                kernel_ms.append(t["main_kernel_ms"])
-                launches += t["launches"]
+                tk = ctx.last_timing()
+                kernel_ms.append(tk["main_kernel_ms"])
+                launches += tk["launches"]
             validate()
         torch.cuda.synchronize(dev)
     if graph is not None:  # kernel time bounded by the replayed step
@@ -306,37 +482,16 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
     kern = statistics.mean(kernel_ms)
     if dist is not None:
         total_ms, kern = max_over_ranks(dist, [total_ms, kern], dev)
-    value = n * args.steps / (total_ms / 1e3)
-    local_slices = b - a
-    F = canonical_flops(d, plan.m_max, 1 + wl["n_ctrl"])
-    peak = fp64_peak()["fp64_dmma_tflops"] * 1e12
-    achieved = local_slices * F / (kern / 1e3)
-    traffic, traffic_note = None, None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            cap = json.load(fh).get(t["kernel"])
-        if cap:
-            traffic = cap["dram_bytes"] * local_slices / cap["slices"]
-            traffic_note = (f"ncu --set full dram read+write of one launch at {cap['slices']} "
-                            f"slices ({cap['dram_bytes']:.3g} B), scaled linearly to this launch; "
-                            f"algorithmic bytes/slice = {8 * wl['n_ctrl']} (amplitude row)")
-    except (OSError, ValueError, KeyError):
-        pass
-    roofline = {"bound": "tensor", "achieved": achieved / 1e12, "peak": peak / 1e12,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "traffic_note": traffic_note,
-                "kernel": t["kernel"], "kernel_ms": kern,
-                "executed_frac": t["executed_flops"] / (kern / 1e3) / peak,
-                "series": ctx.last_algorithm(),
-                "algorithmic_flops_per_launch": local_slices * F,
-                "peak_source": "measured FP64 DMMA pipe peak (profiles/fp64_peak.json)"}
+    value = n * steps / (total_ms / 1e3)
+    roofline = roofline_for(t, b - a, wl, plan.m_max, kern, fp64_peaks())
 
     # ---- e2e: public API, page-locked host table, H2D + compute + D2H timed
     pinned = torch.empty(local.shape, dtype=torch.float64, pin_memory=True)
     pinned.numpy()[:] = local
     e2e_times = []
     amps_obj = sp.ControlAmplitudes(pinned.numpy(), dt, copy=False) if world == 1 else None
-    for k in range(args.warmup + args.steps):
+    u = None
+    for k in range(args.warmup + steps):
         flush.fill_(float(k))
         torch.cuda.synchronize(dev)
         if dist is not None:
@@ -354,25 +509,36 @@ def measure_gpu(args, wl, rank, world, local_rank, dist, headline):
     e2e_s = sum(e2e_times)
     if dist is not None:
         (e2e_s,) = max_over_ranks(dist, [e2e_s], dev)
-    e2e = {"value": n * args.steps / e2e_s, "unit": UNIT,
+    e2e = {"value": n * steps / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(local.nbytes), "d2h_bytes_per_step": int(d * d * 16),
-           "ms_per_step": e2e_s / args.steps * 1e3}
+           "ms_per_step": e2e_s / steps * 1e3}
     assert np.all(np.isfinite(u))
-    res = {"value": value, "ms_per_step": total_ms / args.steps, "roofline": roofline,
-           "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
-           "m": plan.m_max, "config": {"workload": wl["label"], "dim": d,
-                                       "n_ctrl": wl["n_ctrl"], "slices": n,
-                                       "mode": "midpoint", "m": plan.m_max,
-                                       "l2": "flushed between timed steps (256 MiB write)",
-                                       "parallelism": f"time-sharded x{world}",
-                                       "cuda_graph": graph is not None}}
-    res["cpu_sample"] = None
-    if headline and rank == 0 and world == 1 and not args.no_cpu:
-        rate, ns, sec, threads = cpu_sample_rate(system, values, dt, target_s=args.cpu_seconds)
-        res["cpu_sample"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"first {ns} slices of the workload ({sec:.1f} s), "
-                                       "oracle/ numpy restatement of the reference, OpenBLAS "
-                                       f"{threads} threads on {os.cpu_count()} host cpus"}
+    res = {"value": value, "ms_per_step": total_ms / steps, "steps": steps,
+           "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
+           "clocks": clk.summary(), "m": plan.m_max, "lanes": lanes,
+           "config": {"workload": wl["label"], "dim": d, "n_ctrl": wl["n_ctrl"],
+                      "slices": n, "mode": mode, "m": plan.m_max,
+                      "n_terms": n_terms_for(wl), "lanes": lanes,
+                      "l2": "flushed between timed steps (256 MiB write)",
+                      "parallelism": f"time-sharded x{world}",
+                      "cuda_graph": graph is not None}}
+
+    # ---- CPU reference on a bounded prefix + parity of the same prefix
+    res["cpu_sample"], res["parity"] = None, None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        arm = CpuArm(h0, hs, dt, mode)
+        target = args.cpu_seconds if headline else min(args.cpu_seconds, 4.0)
+        s = arm.sample(values, target)
+        res["cpu_sample"] = arm.baseline(s, n)
+        u_seq = arm.run(s["prefix"], reduction="sequential")
+        gpu_u = ctx.equiprop(sp.ControlAmplitudes(s["prefix"], dt)).u
+        den = np.linalg.norm(s["u"])
+        err = float(np.linalg.norm(gpu_u - s["u"]) / den)
+        eps_self = float(np.linalg.norm(u_seq - s["u"]) / den)
+        tol = max(1e-12, 4.0 * eps_self)
+        res["parity"] = {"slices": s["slices"], "against": arm.kind, "rel_fro": err,
+                         "eps_self": eps_self, "tol": tol, "pass": bool(err <= tol)}
+        arm.close()
     ctx.close()
     return res
 
@@ -384,9 +550,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
-    ap.add_argument("--secondary", default="c3,c3s,c1,c1m",
+    ap.add_argument("--secondary", default="c4m,c3,c3s,c1,c1m",
                     help="extra workloads reported under per_dim ('' for none)")
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--cpu-seconds", type=float, default=9.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the secondary workloads directly instead of as CUDA graphs")
@@ -414,15 +580,19 @@ def main():
             dist_mod.init_process_group(backend)
         dist = dist_mod
 
-    head = measure_gpu(args, WORKLOADS[args.workload], rank, world, local_rank, dist, True)
+    head = measure_gpu(args, args.workload, rank, world, local_rank, dist, True)
     per_dim = {}
     for name in [s for s in args.secondary.split(",") if s and s != args.workload]:
-        r = measure_gpu(args, WORKLOADS[name], rank, world, local_rank, dist, False)
+        r = measure_gpu(args, name, rank, world, local_rank, dist, False)
         per_dim[name] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
-                         "e2e": r["e2e"], "roofline_frac": r["roofline"]["frac"],
-                         "executed_frac": r["roofline"]["executed_frac"],
+                         "steps": r["steps"], "e2e": r["e2e"],
+                         "roofline_frac": r["roofline"]["frac"],
+                         "canonical_frac": r["roofline"]["canonical_frac"],
+                         "achieved_tflops": r["roofline"]["achieved"],
+                         "peak_tflops": r["roofline"]["peak"], "pipe": r["roofline"]["pipe"],
                          "kernel": r["roofline"]["kernel"], "workload": r["config"]["workload"],
-                         "cuda_graph": r["config"]["cuda_graph"]}
+                         "m": r["m"], "lanes": r["lanes"], "cuda_graph": r["config"]["cuda_graph"],
+                         "cpu_baseline": r["cpu_sample"], "parity": r["parity"]}
     if rank == 0:
         line = {
             "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world,
@@ -431,7 +601,7 @@ def main():
             "dtype": "complex128", "data": "synthetic (seeded random unit-norm Hermitian "
                                            "system, uniform(-1,1) amplitudes)",
             "config": head["config"], "roofline": head["roofline"],
-            "cpu_baseline": head["cpu_sample"], "e2e": head["e2e"],
+            "cpu_baseline": head["cpu_sample"], "parity": head["parity"], "e2e": head["e2e"],
             "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
             "per_dim": per_dim, "impl": "b200",
         }

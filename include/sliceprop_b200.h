@@ -139,6 +139,9 @@ int sp_slice_count(const sp_ctx* ctx, int64_t pts, int64_t* out);
  * in every case; only the rounding differs. */
 int sp_set_algorithm(sp_ctx* ctx, int algo);
 int sp_last_algorithm(const sp_ctx* ctx, int* algo, int* gemms_per_slice);
+/* number of lanes (contiguous runs of slices propagated by one warp / CTA /
+ * CTA group) of the last lane pass: slices per lane = slice_count / lanes */
+int sp_last_lanes(const sp_ctx* ctx, int* lanes);
 
 /* ---- measurement hooks ------------------------------------------------ */
 /* when enabled, the next propagations record CUDA events around the main

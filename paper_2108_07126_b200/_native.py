@@ -68,6 +68,7 @@ HEADER_SYMBOLS = {
     "sp_amplitude_violation": (_c.c_int, [_P, _c.POINTER(_c.c_int64)]),
     "sp_set_algorithm": (_c.c_int, [_P, _c.c_int]),
     "sp_last_algorithm": (_c.c_int, [_P, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)]),
+    "sp_last_lanes": (_c.c_int, [_P, _c.POINTER(_c.c_int)]),
     "sp_set_profiling": (_c.c_int, [_P, _c.c_int]),
     "sp_last_timing": (_c.c_int, [_P, _c.POINTER(_c.c_double), _c.POINTER(_c.c_int),
                                   _c.POINTER(_c.c_double), _c.c_char_p, _c.c_int]),

@@ -223,6 +223,7 @@ struct sp_ctx {
   int algo = 0;          // Algo
   int last_algo = 0;     // algorithm of the last lane pass
   int last_gemms = 0;    // GEMMs per slice of the last lane pass
+  int last_lanes = 0;    // lanes of the last lane pass
   // profiling
   bool prof = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -813,6 +814,7 @@ int d8_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_
   ctx->last_gemms = ps_s == 0 ? job.m : ps_cost(job.m, ps_s);
   *prods = (const double2*)ctx->lanes.p;
   *count = lanes;
+  ctx->last_lanes = lanes;
   return SP_OK;
 }
 
@@ -912,6 +914,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     ctx->last_gemms = job.m;
     *prods = lane_out;
     *count = cta_reduce ? blocks : lanes;
+    ctx->last_lanes = lanes;
     return SP_OK;
   }
   const int ps_s = (ctx->algo == ALGO_CLENSHAW) ? 0
@@ -958,6 +961,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     ctx->last_gemms = ps_cost(job.m, ps_s);
     *prods = lane_out;
     *count = lanes;
+    ctx->last_lanes = lanes;
     return SP_OK;
   }
   if (ps_s > 0) {
@@ -991,6 +995,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     ctx->last_gemms = ps_cost(job.m, ps_s);
     *prods = lane_out;
     *count = lanes;
+    ctx->last_lanes = lanes;
     return SP_OK;
   }
   ctx->last_algo = ALGO_CLENSHAW;
@@ -1017,6 +1022,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   if (rc) return rc;
   *prods = lane_out;
   *count = lanes;
+  ctx->last_lanes = lanes;
   return SP_OK;
 }
 
@@ -1665,6 +1671,12 @@ int sp_last_algorithm(const sp_ctx* ctx, int* algo, int* gemms_per_slice) {
   if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
   if (algo) *algo = ctx->last_algo;
   if (gemms_per_slice) *gemms_per_slice = ctx->last_gemms;
+  return SP_OK;
+}
+
+int sp_last_lanes(const sp_ctx* ctx, int* lanes) {
+  if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
+  if (lanes) *lanes = ctx->last_lanes;
   return SP_OK;
 }
 

@@ -452,6 +452,12 @@ class IntegratorContext:
         return {"algorithm": {0: "none", 1: "clenshaw", 2: "ps", 3: "ps3m"}.get(a.value, "?"),
                 "gemms_per_slice": g.value}
 
+    def last_lanes(self) -> int:
+        """Lanes of the last lane pass (slices per lane = slices / lanes)."""
+        n = ctypes.c_int()
+        check(lib.sp_last_lanes(self._handle, ctypes.byref(n)), self._handle)
+        return n.value
+
     def set_profiling(self, enabled: bool = True) -> None:
         check(lib.sp_set_profiling(self._handle, int(bool(enabled))), self._handle)
 
