@@ -131,6 +131,39 @@ int sp_amplitude_violation(sp_ctx* ctx, int64_t* index);
  * (propagator.py:245-252); SP_E_SAMPLING_PARITY for even/short 3-point tables */
 int sp_slice_count(const sp_ctx* ctx, int64_t pts, int64_t* out);
 
+/* ---- device batch layer (context-free; device buffers, caller's stream,
+ *      asynchronous).  For users who build / exponentiate / multiply their
+ *      own batches, as the reference's materialised path does; equiprop
+ *      never uses these (its three stages are fused in the lane kernels).
+ *      Batches: compact or strided runs of d x d row-major interleaved
+ *      complex matrices in the working dtype (complex128 for bits 64,
+ *      complex64 for bits 32), computed in that dtype's arithmetic. ---- */
+/* out[k] = scale (T_0 + sum_{i>=1} coeffs[k, i] T_i): terms complex128
+ * (n_terms x d x d), coeffs float64 (count x n_terms, column 0 all ones),
+ * out compact working dtype.  Replaces expand_linear_combination
+ * (linalg.py:246-288) under build_exponent_batch (hamiltonian.py:186-207)
+ * and build_magnus_exponent_batch (magnus.py:121-141). */
+int sp_expand_batch_device(int precision_bits, int dim, int n_terms, const void* d_terms,
+                           int64_t count, const double* d_coeffs, double scale, void* d_out,
+                           void* stream);
+/* U[k] = phase * p((2/span)(G[k] - center I)) with the plan's Chebyshev
+ * polynomial (expm_batch, chebyshev.py:259-306).  dim <= 64: one fused
+ * on-chip kernel (in place allowed); dim > 64: m+1 batched GEMM launches
+ * through d_scratch (sp_expm_batch_scratch_bytes; may alias neither g nor u).
+ * Strides in complex elements between consecutive matrices. */
+size_t sp_expm_batch_scratch_bytes(int precision_bits, int dim, int64_t count);
+int sp_expm_batch_device(int precision_bits, int dim, int64_t count, const void* d_g,
+                         int64_t stride_in, const sp_plan* plan, void* d_u, int64_t stride_out,
+                         void* d_scratch, void* stream);
+/* C[k] = alpha A[k] B[k] + beta C[k] + gamma I; alpha/beta/gamma are
+ * (re, im) pairs (NULL: 1, 0, 0); beta == 0 never reads C; C must not
+ * overlap A or B (gemm_strided_batched + diagonal_add_batched,
+ * linalg.py:204-237). */
+int sp_gemm_batched_device(int precision_bits, int dim, int64_t count, const void* d_a,
+                           int64_t stride_a, const void* d_b, int64_t stride_b,
+                           const double* alpha, const double* beta, const double* gamma,
+                           void* d_c, int64_t stride_c, void* stream);
+
 /* ---- evaluation scheme of the slice series ------------------------------
  * 0 auto (Paterson-Stockmeyer in the Chebyshev basis whenever it needs fewer
  * GEMMs per slice than the reference's Clenshaw recurrence), 1 Clenshaw

@@ -4,7 +4,10 @@ Same contract as the reference ``sliceprop/chebyshev.py:1-218``; the
 arithmetic runs in the C++ host plan of the native library
 (``csrc/plan.cpp``: 80-bit Miller recurrence for J_k, libm exp/pow for the
 error estimate), bit-for-bit equal to the reference (tests/test_plan.py).
-The series itself is evaluated on the GPU inside the lane kernels.
+The series itself is evaluated on the GPU: inside the lane kernels for
+equiprop, and by the batch kernels (``csrc/kernels_batch.cuh``) for the
+standalone ``expm_batch`` over a user's own exponent batch
+(``chebyshev.py:221-306``).
 """
 
 from __future__ import annotations
@@ -16,8 +19,9 @@ import numpy as np
 
 from . import _native
 from ._native import lib
-from .errors import ConfigError, DomainError, StepTooLargeError, raise_for
-from .linalg import Precision
+from .errors import (ConfigError, DomainError, HermiticityError, ShapeError, StepTooLargeError,
+                     raise_for)
+from .linalg import DeviceBackend, MatrixBatch, Precision, default_backend
 
 __all__ = [
     "ORDER_GRID",
@@ -27,6 +31,8 @@ __all__ = [
     "norm_capability",
     "ChebyshevPlan",
     "make_plan",
+    "Workspace",
+    "expm_batch",
 ]
 
 # odd truncation orders the selector may choose from (chebyshev.py:50-51)
@@ -145,3 +151,98 @@ def make_plan(alpha: float, beta: float, precision, m_max: int | None = None) ->
                          precision=precision, predicted_error=p.predicted_error)
 
 
+
+
+class Workspace:
+    """Scratch of ``expm_batch`` (``chebyshev.py:221-246``): three host
+    batches X, D0, D1 sized like G, bound to one dimension and precision,
+    capacity growing monotonically; the result of ``expm_batch`` is a view of
+    D0 valid until the next call on the same workspace.  The device-side
+    staging (input, output and, for d > 64, the X / D1 / D0 scratch of the
+    multi-launch path) is owned here too and grows the same way, so
+    back-to-back evaluations do not reallocate on either side."""
+
+    def __init__(self, dim: int, precision):
+        if dim < 1:
+            raise ShapeError(f"dim must be >= 1, got {dim}")
+        self.dim = int(dim)
+        self.precision = Precision.parse(precision)
+        self.capacity = 0
+        self._x = self._d0 = self._d1 = None
+        self._dev = {}
+
+    def ensure(self, count: int):
+        """Views of the three scratch batches with exactly ``count`` slices."""
+        if self._x is None or count > self.capacity:
+            self._x = MatrixBatch.zeros(self.dim, count, self.precision)
+            self._d0 = MatrixBatch.zeros(self.dim, count, self.precision)
+            self._d1 = MatrixBatch.zeros(self.dim, count, self.precision)
+            self.capacity = count
+        return (self._x.subview(0, count), self._d0.subview(0, count),
+                self._d1.subview(0, count))
+
+    def device_buffer(self, name: str, nbytes: int, device):
+        """Monotone device byte buffer ``name`` of at least ``nbytes``."""
+        import torch
+        buf = self._dev.get(name)
+        if buf is None or buf.numel() < nbytes or buf.device != device:
+            buf = torch.empty(max(16, nbytes), dtype=torch.uint8, device=device)
+            self._dev[name] = buf
+        return buf
+
+
+def _check_hermitian(g: MatrixBatch) -> None:
+    """checked=True validation (``chebyshev.py:249-256``), host-side."""
+    gv = g.matrices()
+    asym = np.abs(gv - gv.conj().transpose(0, 2, 1)).max() if g.count else 0.0
+    scale = np.abs(gv).max() if g.count else 0.0
+    tol = 100.0 * g.precision.roundoff * max(1.0, scale * g.dim)
+    if asym > tol:
+        raise HermiticityError(f"exponent batch asymmetry {asym:.3g} exceeds tolerance {tol:.3g}")
+
+
+def expm_batch(g: MatrixBatch, plan: ChebyshevPlan, workspace: Workspace,
+               backend: DeviceBackend | None = None, checked: bool = False) -> MatrixBatch:
+    """U[k] = exp(-i G[k]) for every matrix of the batch, on the B200
+    (``chebyshev.py:259-306``): the plan's Chebyshev polynomial evaluated by
+    the reference's Clenshaw recurrence, X = (2/span)(G - center I), in the
+    batch's working precision (complex64 batches in FP32 arithmetic).
+    d <= 64: one fused kernel keeps X and the iterates on chip; d > 64:
+    m + 1 batched GEMM launches.  The returned batch aliases the workspace."""
+    import torch
+
+    from ._native import check, lib
+    if backend is not None and not isinstance(backend, DeviceBackend):
+        raise ConfigError(f"expm_batch runs on the B200 DeviceBackend, got {backend!r}")
+    backend = backend or default_backend()
+    if g.precision is not plan.precision:
+        raise ShapeError(f"batch precision {g.precision.value} does not match plan "
+                         f"{plan.precision.value}")
+    if workspace.dim != g.dim or workspace.precision is not g.precision:
+        raise ShapeError("workspace dimension or precision does not match the batch")
+    if checked:
+        _check_hermitian(g)
+    x, d0, d1 = workspace.ensure(g.count)
+    if g.count == 0:
+        return d0
+    dev = backend.torch_device()
+    prec = g.precision
+    isz = prec.complex_dtype.itemsize
+    n, d = g.count, g.dim
+    d_g = workspace.device_buffer("g", n * d * d * isz, dev)
+    d_g[:n * d * d * isz].copy_(torch.from_numpy(
+        np.ascontiguousarray(g.matrices()).reshape(-1).view(np.uint8)))
+    d_u = workspace.device_buffer("u", n * d * d * isz, dev)
+    scratch_bytes = int(lib.sp_expm_batch_scratch_bytes(prec.bits, d, n))
+    d_s = workspace.device_buffer("scratch", scratch_bytes, dev) if scratch_bytes else None
+    native = plan.to_native()
+    stream = backend.stream()
+    check(lib.sp_expm_batch_device(prec.bits, d, n, ctypes.c_void_p(d_g.data_ptr()), d * d,
+                                   ctypes.byref(native), ctypes.c_void_p(d_u.data_ptr()), d * d,
+                                   ctypes.c_void_p(d_s.data_ptr() if d_s is not None else 0),
+                                   ctypes.c_void_p(stream)))
+    # batched products executed: the fused kernel skips the reference's first
+    # multiply-by-zero, the d > 64 path runs all m + 1
+    backend.gemm_calls += plan.m_max + (1 if d > 64 else 0)
+    d0.matrices()[:] = d_u[:n * d * d * isz].cpu().numpy().view(prec.complex_dtype).reshape(n, d, d)
+    return d0

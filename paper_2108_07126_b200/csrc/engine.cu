@@ -247,6 +247,18 @@ int fail(sp_ctx* ctx, int code, const char* fmt, ...) {
   return code;
 }
 
+}  // namespace
+
+int sp::set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+namespace {
+
 #define CUDA_TRY(ctx, call)                                                              \
   do {                                                                                   \
     cudaError_t e_ = (call);                                                             \
@@ -1138,9 +1150,24 @@ int prepare_device(sp_ctx* ctx) {
 
 double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
   const double D = ctx->D;
-  // D = 2: Clenshaw on (a, b) coefficient pairs (~32 flop/step) + forming U
-  // and V <- U V (~120 flop) (lane_small_kernel<2,1>)
-  if (ctx->fam == FAM_S2) return (double)n * (32.0 * m + 120.0 + 16.0 * ctx->n_terms);
+  // register families: FP64 flops per slice (DFMA = 2, DADD / DMUL = 1)
+  // calibrated on the SASS instruction counts of ncu
+  // (smsp__sass_thread_inst_executed_op_{dfma,dadd,dmul}_pred_on.sum,
+  // tools/ncu_small_flops.py, profiles/r02_ncu_small_flops.md), exact on
+  // every calibration point:
+  //   d = 2, real Cayley-Hamilton pairs (bitwise Hermitian terms, midpoint,
+  //          <= 2 controls): 125 + 16 m, +14 when m is not compiled in
+  //          (3, 7, 13, 15)
+  //   d = 2, complex pairs (other modes / more controls): 269 + 16 m + 43 T
+  //   d = 3, 4: 10.3 + 576 m + 64 T
+  if (ctx->fam == FAM_S2) {
+    const bool fast2 = ctx->herm_exact && ctx->mode == SP_MODE_MIDPOINT && ctx->n_terms <= 3;
+    const bool compiled = m == 3 || m == 7 || m == 13 || m == 15;
+    const double f = fast2 ? 125.0 + 16.0 * m + (compiled ? 0.0 : 14.0)
+                           : 269.0 + 16.0 * m + 43.0 * ctx->n_terms;
+    return (double)n * f;
+  }
+  if (ctx->fam == FAM_S4) return (double)n * (10.3 + 576.0 * m + 64.0 * ctx->n_terms);
   // 3-multiplication products execute 3/4 of the real FP64 MMA work
   const double f = (ctx->last_algo == ALGO_PS3) ? 6.0 : 8.0;
   return (double)n * (f * D * D * D * ctx->last_gemms + 4.0 * D * D * ctx->n_terms);

@@ -14,6 +14,8 @@ int select_m_max(double norm_bound, int bits, int* m_out, double* capability, ch
                  size_t errlen);
 int make_plan(double alpha, double beta, int bits, int m_override, sp_plan* out, char* err,
               size_t errlen);
+// record a context-free error (sp_last_error(NULL)) and return code
+int set_error(int code, const char* fmt, ...);
 
 // Everything one propagation needs on the device (all pointers device).
 struct SliceJob {

@@ -31,7 +31,7 @@ from .errors import (AmplitudeBoundError, ConfigError, HermiticityError, Samplin
                      StateMachineError)
 from .hamiltonian import (ControlAmplitudes, ControlSystem, Quadrature, check_pair,
                           simpson_triplets, spectral_bound)
-from .linalg import Precision
+from .linalg import DeviceBackend, Precision
 from .magnus import EffectiveSystem, build_effective_system, magnus_bound
 
 __all__ = [
@@ -137,12 +137,15 @@ class IntegratorContext:
     independent contexts may coexist.  Not thread-safe, not reentrant.
     """
 
-    def __init__(self, precision: Precision, m_max: int | None, checked: bool, device: int):
+    def __init__(self, precision: Precision, m_max: int | None, checked: bool, device: int,
+                 backend: DeviceBackend | None = None):
         self.precision = precision
         self.m_max = m_max
         self.checked = checked
         self.device = device
-        self.backend = BACKEND_NAME
+        # one batch backend per context (reference: one CpuBackend per
+        # context, test_propagator.py:228-238); its name is "b200"
+        self.backend = backend if backend is not None else DeviceBackend(device)
         self._state = _CREATED
         self._system: ControlSystem | None = None
         self._effective: EffectiveSystem | None = None
@@ -484,16 +487,20 @@ def create(precision="fp64", m_max: int | None = None, checked: bool = False,
     """New propagation context on one B200 (``propagator.py:334-355``).
 
     precision "fp32" | "fp64"; m_max pins the series order (odd 3..25);
-    checked enables the Hermiticity sanity pass.  backend accepts None or a
-    GPU token ("b200", "cuda", "gpu", "sm_100a") — the reference's "cpu"
-    backend is not offered: this package has no CPU path.
+    checked enables the Hermiticity sanity pass.  backend accepts None, a
+    ``DeviceBackend`` instance or a GPU token ("b200", "cuda", "gpu",
+    "sm_100a") — the reference's "cpu" backend is not offered: this package
+    has no CPU path.
     """
     precision = Precision.parse(precision)
     if m_max is not None and m_max not in ORDER_GRID:
         raise ConfigError(f"m_max override {m_max} not an odd integer in "
                           f"{ORDER_GRID[0]}..{ORDER_GRID[-1]}")
-    if backend is not None:
+    dev = _default_device() if device is None else int(device)
+    instance = None
+    if isinstance(backend, DeviceBackend):
+        instance, dev = backend, backend.device if device is None else dev
+    elif backend is not None:
         if not isinstance(backend, str) or backend.lower() not in _BACKEND_TOKENS:
             raise ConfigError(f"unknown backend {backend!r}; expected one of {_BACKEND_TOKENS}")
-    return IntegratorContext(precision, m_max, bool(checked),
-                             _default_device() if device is None else int(device))
+    return IntegratorContext(precision, m_max, bool(checked), dev, instance)

@@ -43,7 +43,7 @@ class TestLifecycle:
         ctx = sp.create()
         assert ctx.state == "created"
         assert ctx.precision.value == "fp64"
-        assert ctx.backend == "b200"
+        assert ctx.backend.name == "b200"
 
     def test_invalid_tokens(self):
         with pytest.raises(sp.ConfigError):
@@ -54,7 +54,7 @@ class TestLifecycle:
             sp.create(m_max=27)
         with pytest.raises(sp.ConfigError):
             sp.create(backend="cpu")
-        assert sp.create(backend="b200").backend == "b200"
+        assert sp.create(backend="b200").backend.name == "b200"
 
     def test_propagate_before_load(self):
         ctx = sp.create()

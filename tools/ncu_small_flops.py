@@ -30,3 +30,13 @@ for kind, d, n_ctrl, m in POINTS:
         u = ctx.equiprop(sp.ControlAmplitudes(v, dt)).u
         print(kind, d, n_ctrl, m, ctx.last_timing()["kernel"], ctx.last_lanes(), float(np.abs(u).sum()),
               flush=True)
+# complex-pair (generic) d = 2 path: more controls, three-point modes
+for mode, n_ctrl, m in (("midpoint", 3, 13), ("midpoint", 4, 3), ("midpoint", 4, 7),
+                        ("simpson", 2, 13), ("magnus", 2, 13)):
+    pts = N if mode == "midpoint" else 2 * N + 1
+    h0, hs, v, dt = random_inputs(2, n_ctrl, pts, 5 + n_ctrl + m, beta=0.1)
+    with sp.create(m_max=m) as ctx:
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                            quadrature=None if mode == "magnus" else mode)
+        u = ctx.equiprop(sp.ControlAmplitudes(v, dt)).u
+        print(mode, 2, n_ctrl, m, ctx.last_timing()["kernel"], float(np.abs(u).sum()), flush=True)
