@@ -353,7 +353,9 @@ def roofline_for(t, local_slices, wl, m, kern_ms, peaks):
     denominator (above 1 when the kernel needs fewer flops than the
     reference's Clenshaw count)."""
     dfma = t["kernel"].startswith("lane_small")
-    peak = (peaks["fp64_dfma_tflops"] if dfma else peaks["fp64_dmma_tflops"]) * 1e12
+    ffma = t["kernel"].startswith("lane_f32")
+    peak = (peaks["fp32_ffma_tflops"] if ffma else peaks["fp64_dfma_tflops"] if dfma
+            else peaks["fp64_dmma_tflops"]) * 1e12
     F = canonical_flops(wl["d"], m, n_terms_for(wl))
     executed = t["executed_flops"] / (kern_ms / 1e3)
     canonical = local_slices * F / (kern_ms / 1e3)
@@ -374,8 +376,10 @@ def roofline_for(t, local_slices, wl, m, kern_ms, peaks):
             "executed_flops_per_launch": t["executed_flops"],
             "canonical_achieved": canonical / 1e12, "canonical_frac": canonical / peak,
             "canonical_flops_per_launch": local_slices * F,
-            "pipe": "FP64 DFMA (CUDA cores)" if dfma else "FP64 DMMA (mma.sync f64)",
-            "peak_source": "measured FP64 " + ("DFMA" if dfma else "DMMA")
+            "pipe": "FP32 FFMA (CUDA cores)" if ffma else "FP64 DFMA (CUDA cores)" if dfma
+                    else "FP64 DMMA (mma.sync f64)",
+            "peak_source": "measured " + ("FP32 FFMA" if ffma else "FP64 DFMA" if dfma
+                                          else "FP64 DMMA")
                            + " peak (tools/fp64_peak.cu, profiles/fp64_peak.json; "
                              "MEASURED_PEAKS.json has no FP64 entry)"}
 

@@ -84,8 +84,15 @@ int sp_make_plan(double alpha, double beta, int precision_bits, int m_override, 
 /* ---- context lifecycle (create / set_hamiltonian / close,
  *      propagator.py:132-216 and 334-355; Parament_create/_free) -------- */
 /* no device work happens here: the GPU is touched lazily by the first
- * propagation, so contexts can be created and validated without a GPU */
-int sp_create(sp_ctx** out, int precision_bits, int device_ordinal);
+ * propagation, so contexts can be created and validated without a GPU.
+ * num_gpus devices (device_ids[0..num_gpus-1], NULL = 0..num_gpus-1) in ONE
+ * process (the paper's interactive use):
+ * with num_gpus > 1, sp_equiprop time-shards the slices into contiguous
+ * blocks, one per device (three-point modes read a one-row halo), gathers
+ * the d x d block products on device_ids[0] by peer copies and multiplies
+ * them in time order; the device-resident and cumulative entry points run
+ * on device_ids[0].  A device may repeat (P blocks emulated on one GPU). */
+int sp_create(sp_ctx** out, int precision_bits, int num_gpus, const int* device_ids);
 int sp_free(sp_ctx* ctx);
 const char* sp_last_error(const sp_ctx* ctx);   /* ctx may be NULL */
 /* load the expansion terms [H0, effective controls...] (T x d x d complex128,

@@ -51,7 +51,7 @@ HEADER_SYMBOLS = {
     "sp_norm_capability": (_c.c_int, [_c.c_int, _c.c_int, _c.POINTER(_c.c_double)]),
     "sp_make_plan": (_c.c_int, [_c.c_double, _c.c_double, _c.c_int, _c.c_int,
                                 _c.POINTER(SpPlan)]),
-    "sp_create": (_c.c_int, [_c.POINTER(_P), _c.c_int, _c.c_int]),
+    "sp_create": (_c.c_int, [_c.POINTER(_P), _c.c_int, _c.c_int, _c.POINTER(_c.c_int)]),
     "sp_free": (_c.c_int, [_P]),
     "sp_last_error": (_c.c_char_p, [_P]),
     "sp_set_hamiltonian": (_c.c_int, [_P, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _P]),

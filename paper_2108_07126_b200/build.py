@@ -24,7 +24,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsliceprop_b200.so")
 SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "batch.cu"),
            os.path.join(CSRC, "plan.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "kernels_tc.cuh", "kernels_ps.cuh", "kernels_ps3.cuh", "kernels_ps3g.cuh", "kernels_apply.cuh", "kernels_d8.cuh", "kernels_batch.cuh",
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "kernels_tc.cuh", "kernels_ps.cuh", "kernels_ps3.cuh", "kernels_ps3g.cuh", "kernels_apply.cuh", "kernels_d8.cuh", "kernels_batch.cuh", "kernels_f32.cuh",
                                                   "internal.h")] + [
     os.path.join(ROOT, "include", "sliceprop_b200.h")]
 

@@ -22,6 +22,7 @@
 #include "kernels_ps3g.cuh"
 #include "kernels_apply.cuh"
 #include "kernels_d8.cuh"
+#include "kernels_f32.cuh"
 
 using namespace sp;
 
@@ -68,7 +69,8 @@ using P3_128 = PS3Cfg<128, 32, 1, 4, 8, 1, 4, false>;
 using P3_256 = PS3Cfg<256, 16, 2, 2, 8, 1, 16, false>;
 using P3_512 = PS3Cfg<512, 8, 4, 1, 8, 1, 64, false>;
 
-enum Algo { ALGO_AUTO = 0, ALGO_CLENSHAW = 1, ALGO_PS = 2, ALGO_PS3 = 3 };
+enum Algo { ALGO_AUTO = 0, ALGO_CLENSHAW = 1, ALGO_PS = 2, ALGO_PS3 = 3,
+            ALGO_F32 = 4 /* reported only: the complex64-arithmetic lane kernel */ };
 
 // GEMMs per slice: Clenshaw m; PS (s-1) + (r-1) + 1, r = ceil((m+1)/s)
 int ps_cost(int m, int s) {
@@ -152,6 +154,9 @@ int family_for(int d, int* D) {
 }
 
 const char* family_kernel_name(int fam, int algo) {
+  if (algo == 4)  // complex64 arithmetic (kernels_f32.cuh)
+    return fam == FAM_S2 ? "lane_f32_kernel<2>" : fam == FAM_S4 ? "lane_f32_kernel<4>"
+                                                                : "lane_f32_kernel<8>";
   if (fam == FAM_T8)
     return algo == 3 ? "lane_d8_kernel<ps3m>" : algo == 2 ? "lane_d8_kernel<ps>"
                                                           : "lane_d8_kernel<clenshaw>";
@@ -232,9 +237,24 @@ struct sp_ctx {
   int launches = 0;
   double flops = 0.0;
   const char* kname = "none";
+  // single-process multi-device context (sp_create with num_gpus > 1): the
+  // per-device child contexts, each propagating one contiguous block of
+  // slices; the block products are gathered by peer copies onto the first
+  // device and multiplied there in time order
+  std::vector<sp_ctx*> kids;
+  bool block64 = false;  // child: write its block product in complex128
+  DevBuf gather;         // first child: P x d x d complex128 block products
+  DevBuf result2;        // first child: the d x d result of the gather product
+  int64_t multi_viol = -1;  // first offender of the last multi-device call
+  bool last_multi = false;  // the last call was a multi-device equiprop
+  std::vector<cudaEvent_t> kid_done;
 };
 
 namespace {
+
+// the call's d x d output in complex64 (fp32 contexts, except a multi-device
+// child writing its block for the complex128 gather)
+bool out32(const sp_ctx* ctx) { return ctx->bits == 32 && !ctx->block64; }
 
 int fail(sp_ctx* ctx, int code, const char* fmt, ...) {
   char buf[512];
@@ -587,7 +607,7 @@ int ap_launch(sp_ctx* ctx, const double* P, const double2* E, int64_t n, int lan
   const int64_t chunks = (n + spb - 1) / spb;
   apply_prefix_tc_kernel<C><<<dim3((unsigned)chunks, C::GPL), C::THREADS, smem, st>>>(
       P, E, n, lanes, spb, out_d >= 0 ? out_d : ctx->dim,
-      out_fp32 >= 0 ? out_fp32 : (ctx->bits == 32 ? 1 : 0), out);
+      out_fp32 >= 0 ? out_fp32 : (out32(ctx) ? 1 : 0), out);
   CUDA_TRY(ctx, cudaGetLastError());
   ++ctx->launches;
   return SP_OK;
@@ -830,6 +850,58 @@ int d8_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_
   return SP_OK;
 }
 
+// the device-resident and cumulative entry points of a multi-device context
+// run on its first device
+sp_ctx* primary(sp_ctx* ctx) { return ctx->kids.empty() ? ctx : ctx->kids[0]; }
+
+// complex64 contexts of the plain families (d <= 8) run in complex64
+// arithmetic on the FP32 pipe (kernels_f32.cuh); d >= 9 complex64 contexts
+// use the FP64 tensor-core kernels and round
+bool f32_path(const sp_ctx* ctx) { return ctx->bits == 32 && plain_family(ctx->fam); }
+
+template <int D>
+int f32_run(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_t st,
+            int* lanes_out) {
+  const size_t smem = f32_smem_bytes<D>(job.n_terms);
+  CUDA_TRY(ctx, cudaFuncSetAttribute(lane_f32_kernel<D>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_f32_kernel<D>, F32_THREADS, smem);
+  occ = std::max(occ, 1);
+  constexpr int LPC = F32_THREADS / D;
+  // one wave of resident lanes, at least 16 slices per lane
+  const int64_t cap = (int64_t)ctx->sms * occ * LPC;
+  const int64_t want = std::max<int64_t>(1024, (job.n_slices + 15) / 16);
+  const int lanes = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(cap, want),
+                                                                 job.n_slices));
+  int rc = ensure(ctx, ctx->lanes, (size_t)lanes * D * D * sizeof(double2));
+  if (rc) return rc;
+  const int grid = (lanes + LPC - 1) / LPC;
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+  lane_f32_kernel<D><<<grid, F32_THREADS, smem, st>>>(job, (const double2*)ctx->terms.p, lanes,
+                                                      (double2*)ctx->lanes.p, prefix_out);
+  CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+  *lanes_out = lanes;
+  return SP_OK;
+}
+
+int f32_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_t st,
+               const double2** prods, int* count) {
+  int lanes = 0;
+  const int rc = ctx->D == 2 ? f32_run<2>(ctx, job, prefix_out, st, &lanes)
+                 : ctx->D == 4 ? f32_run<4>(ctx, job, prefix_out, st, &lanes)
+                               : f32_run<8>(ctx, job, prefix_out, st, &lanes);
+  if (rc) return rc;
+  ++ctx->launches;
+  ctx->last_algo = ALGO_F32;
+  ctx->last_gemms = job.m + 1;
+  *prods = (const double2*)ctx->lanes.p;
+  *count = lanes;
+  ctx->last_lanes = lanes;
+  return SP_OK;
+}
+
 // Run the lane pass.  Returns the lane products (lane_count of them) on the
 // device, or (small families, pairwise) the per-CTA products.
 int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix_out,
@@ -838,6 +910,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   const int D = ctx->D;
   const size_t dd = (size_t)D * D;
   int lanes = 1;
+  if (f32_path(ctx)) return f32_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_T8) return d8_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
     const int tpl = (ctx->fam == FAM_S2) ? 1 : 4;
@@ -860,7 +933,7 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     if (rc) return rc;
     double2* lane_out = (double2*)ctx->lanes.p;
     double2* cta_out = cta_reduce ? lane_out : nullptr;
-    SmallTail tail{nullptr, nullptr, ctx->dim, ctx->bits == 32};
+    SmallTail tail{nullptr, nullptr, ctx->dim, out32(ctx)};
     if (fused_out) {
       // arrival counter: zeroed once at allocation, reset by the last CTA
       if (!ctx->tailctr.p) {
@@ -1071,6 +1144,8 @@ int build_job(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double
   const double scale = (ctx->mode == SP_MODE_MIDPOINT) ? dt : 2.0 * dt;
   const double span = plan->beta - plan->alpha;
   job->xs = (span == 0.0) ? 0.0 : 2.0 * scale * (2.0 / span);
+  job->scale = scale;
+  job->xspan = (span == 0.0) ? 0.0 : 2.0 / span;
   job->m = plan->m_max;
   std::memcpy(job->coef, plan->coeffs, sizeof(job->coef));
   job->phase[0] = plan->phase[0];
@@ -1150,6 +1225,12 @@ int prepare_device(sp_ctx* ctx) {
 
 double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
   const double D = ctx->D;
+  // complex64 lane kernel (FP32): per slice, D threads each run m
+  // matrix-vector products of the Clenshaw recurrence (the first of the
+  // reference's m + 1 multiplies zero and is skipped), one of V <- U V, and
+  // the assembly of T terms
+  if (ctx->last_algo == ALGO_F32)
+    return (double)n * (8.0 * D * D * D * (m + 1) + 4.0 * D * D * (ctx->n_terms - 1));
   // register families: FP64 flops per slice (DFMA = 2, DADD / DMUL = 1)
   // calibrated on the SASS instruction counts of ncu
   // (smsp__sass_thread_inst_executed_op_{dfma,dadd,dmul}_pred_on.sum,
@@ -1256,7 +1337,7 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
   int rc = build_job(ctx, d_amps, pts, n_ctrl, dt, plan, &job);
   if (rc) return rc;
   // the small families' pairwise product is one launch with a fused tail
-  const bool fused = (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) &&
+  const bool fused = (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) && !f32_path(ctx) &&
                      reduction == SP_REDUCE_PAIRWISE && job.n_slices > 0;
   rc = arm_validation(ctx, &job, st, fused);
   if (rc) return rc;
@@ -1275,8 +1356,8 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
     total = (const double2*)ctx->result.p;
   } else {
     const bool small = plain_family(ctx->fam);
-    const bool cta_reduce =
-        (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) && reduction == SP_REDUCE_PAIRWISE;
+    const bool cta_reduce = (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) && !f32_path(ctx) &&
+                            reduction == SP_REDUCE_PAIRWISE;
     const double2* prods = nullptr;
     int cnt = 0;
     // small families + pairwise: one launch does everything (fused tail)
@@ -1311,7 +1392,7 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
     }
   }
   extract_kernel<<<grid_for((int64_t)d * d, 256), 256, 0, st>>>(total, 1, D, d,
-                                                                ctx->bits == 32, d_out);
+                                                                out32(ctx), d_out);
   CUDA_TRY(ctx, cudaGetLastError());
   ++ctx->launches;
   return SP_OK;
@@ -1445,6 +1526,120 @@ int equiprop_all_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
   return SP_OK;
 }
 
+// ---- single-process multi-device propagation ----------
+// Slices [r n / P, (r+1) n / P) go to child r (three-point modes read the
+// one-row halo); every child propagates its block on its own device and
+// stream and leaves the complex128 block product in its `out` buffer; the
+// blocks are gathered onto the first device by peer copies (d^2 * 16 B each,
+// over NVLink between devices) and multiplied there in time order with the
+// same pairwise / sequential product sp_product_device uses.
+int equiprop_multi(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
+                   const sp_plan* plan, int reduction, void* u_out) {
+  int code;
+  const int64_t n = slice_count_for(ctx->mode, pts, &code);
+  if (code)
+    return fail(ctx, code, "three-point quadrature needs an odd number of samples >= 3, got %lld",
+                (long long)pts);
+  const int P = (int)ctx->kids.size();
+  const int d = ctx->dim;
+  const size_t dd = (size_t)d * d;
+  const size_t blk = dd * sizeof(double2);
+  sp_ctx* k0 = ctx->kids[0];
+  if (ctx->kid_done.size() != (size_t)P) ctx->kid_done.assign(P, nullptr);
+  std::vector<int64_t> first_row(P, 0);
+  std::vector<char> empty(P, 0);
+  int rc = SP_OK;
+  for (int r = 0; r < P && !rc; ++r) {
+    sp_ctx* kid = ctx->kids[r];
+    rc = prepare_device(kid);
+    if (rc) return fail(ctx, rc, "device %d: %s", kid->device, kid->err);
+    if (!ctx->kid_done[r]) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->kid_done[r],
+                                                                  cudaEventDisableTiming));
+    const int64_t a = (int64_t)r * n / P, b = (int64_t)(r + 1) * n / P;
+    const int64_t lo = ctx->mode == SP_MODE_MIDPOINT ? a : 2 * a;
+    const int64_t hi = ctx->mode == SP_MODE_MIDPOINT ? b : 2 * b + 1;
+    first_row[r] = lo;
+    rc = ensure(kid, kid->out, blk);
+    if (rc) return fail(ctx, rc, "device %d: %s", kid->device, kid->err);
+    if (b <= a) {
+      empty[r] = 1;  // identity block, written at the gather
+      CUDA_TRY(ctx, cudaEventRecord(ctx->kid_done[r], kid->stream));
+      continue;
+    }
+    const size_t abytes = (size_t)(hi - lo) * n_ctrl * sizeof(double);
+    rc = ensure(kid, kid->amps, abytes);
+    if (rc) return fail(ctx, rc, "device %d: %s", kid->device, kid->err);
+    if (abytes)
+      CUDA_TRY(ctx, cudaMemcpyAsync(kid->amps.p, amps + lo * n_ctrl, abytes,
+                                    cudaMemcpyHostToDevice, kid->stream));
+    kid->block64 = true;
+    rc = equiprop_dev(kid, (const double*)kid->amps.p, hi - lo, n_ctrl, dt, plan, reduction,
+                      kid->out.p, kid->stream);
+    kid->block64 = false;
+    if (rc) return fail(ctx, rc, "device %d: %s", kid->device, kid->err);
+    rc = fetch_violation(kid, kid->stream);
+    if (rc) return fail(ctx, rc, "device %d: %s", kid->device, kid->err);
+    CUDA_TRY(ctx, cudaEventRecord(ctx->kid_done[r], kid->stream));
+  }
+  // gather the block products on the first device, in time order
+  CUDA_TRY(ctx, cudaSetDevice(k0->device));
+  rc = ensure(ctx, ctx->gather, (size_t)P * blk);
+  if (rc) return rc;
+  std::vector<double2> eye(dd, make_double2(0.0, 0.0));
+  for (int i = 0; i < d; ++i) eye[(size_t)i * d + i] = make_double2(1.0, 0.0);
+  double2* g = (double2*)ctx->gather.p;
+  for (int r = 0; r < P; ++r) {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(k0->stream, ctx->kid_done[r], 0));
+    if (empty[r])
+      CUDA_TRY(ctx, cudaMemcpyAsync(g + r * dd, eye.data(), blk, cudaMemcpyHostToDevice,
+                                    k0->stream));
+    else
+      CUDA_TRY(ctx, cudaMemcpyPeerAsync(g + r * dd, k0->device, ctx->kids[r]->out.p,
+                                        ctx->kids[r]->device, blk, k0->stream));
+  }
+  const size_t obytes = dd * (ctx->bits == 32 ? 8 : 16);
+  rc = ensure(k0, k0->result2, obytes);
+  if (rc) return fail(ctx, rc, "device %d: %s", k0->device, k0->err);
+  rc = product_dev(k0, P, g, reduction, k0->result2.p, k0->stream);
+  if (rc) return fail(ctx, rc, "device %d: %s", k0->device, k0->err);
+  if (ctx->out_host_bytes < obytes) {
+    if (ctx->out_host) cudaFreeHost(ctx->out_host);
+    ctx->out_host = nullptr;
+    CUDA_TRY(ctx, cudaMallocHost(&ctx->out_host, obytes));
+    ctx->out_host_bytes = obytes;
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->out_host, k0->result2.p, obytes, cudaMemcpyDeviceToHost,
+                                k0->stream));
+  // global first amplitude violation: the minimum over the blocks' offenders
+  int64_t best = -1;
+  ctx->launches = 0;
+  for (int r = 0; r < P; ++r) {
+    sp_ctx* kid = ctx->kids[r];
+    CUDA_TRY(ctx, cudaSetDevice(kid->device));
+    CUDA_TRY(ctx, cudaStreamSynchronize(kid->stream));
+    ctx->launches += kid->launches;
+    if (empty[r]) continue;
+    int64_t idx = -1;
+    read_violation(kid, nullptr, &idx, true);
+    if (idx >= 0) {
+      const int64_t gidx = first_row[r] * std::max(1, n_ctrl) + idx;
+      if (best < 0 || gidx < best) best = gidx;
+    }
+  }
+  CUDA_TRY(ctx, cudaSetDevice(k0->device));
+  CUDA_TRY(ctx, cudaStreamSynchronize(k0->stream));
+  ctx->launches += 3 * P;  // copies and the ordered product (counted on k0 too)
+  std::memcpy(u_out, ctx->out_host, obytes);
+  ctx->multi_viol = best;
+  if (best >= 0) {
+    const int N = std::max(1, n_ctrl);
+    return fail(ctx, SP_E_AMPLITUDE_BOUND,
+                "control amplitude %.17g at sample %lld, control %lld lies outside [-1, 1]",
+                amps[best], (long long)(best / N), (long long)(best % N));
+  }
+  return SP_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1497,19 +1692,49 @@ int sp_make_plan(double alpha, double beta, int precision_bits, int m_override, 
   return make_plan(alpha, beta, precision_bits, m_override, out, g_err, sizeof(g_err));
 }
 
-int sp_create(sp_ctx** out, int precision_bits, int device_ordinal) {
+int sp_create(sp_ctx** out, int precision_bits, int num_gpus, const int* device_ids) {
   if (!out) return fail(nullptr, SP_E_CONFIG, "null output pointer");
   if (precision_bits != 32 && precision_bits != 64)
     return fail(nullptr, SP_E_CONFIG, "unknown precision %d; expected 32 or 64", precision_bits);
+  if (num_gpus < 1 || num_gpus > 64)
+    return fail(nullptr, SP_E_CONFIG, "num_gpus must be in 1..64, got %d", num_gpus);
+  for (int r = 0; device_ids && r < num_gpus; ++r)
+    if (device_ids[r] < 0)
+      return fail(nullptr, SP_E_CONFIG, "negative device ordinal %d", device_ids[r]);
   sp_ctx* ctx = new sp_ctx();
   ctx->bits = precision_bits;
-  ctx->device = device_ordinal;
+  ctx->device = device_ids ? device_ids[0] : 0;
+  if (num_gpus > 1) {
+    // one child context per device: no device work here either (lazy)
+    for (int r = 0; r < num_gpus; ++r) {
+      sp_ctx* kid = new sp_ctx();
+      kid->bits = precision_bits;
+      kid->device = device_ids ? device_ids[r] : r;
+      ctx->kids.push_back(kid);
+    }
+  }
   *out = ctx;
   return SP_OK;
 }
 
 int sp_free(sp_ctx* ctx) {
   if (!ctx) return SP_OK;
+  if (!ctx->kids.empty()) {
+    if (ctx->gather.p) {
+      cudaSetDevice(ctx->kids[0]->device);
+      cudaStreamSynchronize(ctx->kids[0]->stream);
+      cudaFree(ctx->gather.p);
+    }
+    for (size_t r = 0; r < ctx->kid_done.size(); ++r)
+      if (ctx->kid_done[r]) {
+        cudaSetDevice(ctx->kids[r]->device);
+        cudaEventDestroy(ctx->kid_done[r]);
+      }
+    if (ctx->out_host) cudaFreeHost(ctx->out_host);
+    ctx->out_host = nullptr;
+    for (sp_ctx* kid : ctx->kids) sp_free(kid);
+    ctx->kids.clear();
+  }
   if (ctx->dev_ready) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
@@ -1517,7 +1742,8 @@ int sp_free(sp_ctx* ctx) {
                       &ctx->tree1, &ctx->xglob, &ctx->gctr,  &ctx->result, &ctx->out,
                       &ctx->cumP,  &ctx->cumE,  &ctx->cumO,  &ctx->fold_scratch,
                       &ctx->psA,   &ctx->tpriv, &ctx->viol, &ctx->terms3, &ctx->tailctr,
-                      &ctx->seqA, &ctx->scanEin, &ctx->lstarts, &ctx->scanS, &ctx->scanA};
+                      &ctx->seqA, &ctx->scanEin, &ctx->lstarts, &ctx->scanS, &ctx->scanA,
+                      &ctx->result2};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1569,6 +1795,10 @@ int sp_set_hamiltonian(sp_ctx* ctx, int dim, int n_ctrl, int n_terms, int mode,
   ctx->D = D;
   ctx->terms_uploaded = false;
   ctx->loaded = true;
+  for (sp_ctx* kid : ctx->kids) {
+    const int rc = sp_set_hamiltonian(kid, dim, n_ctrl, n_terms, mode, terms);
+    if (rc) return fail(ctx, rc, "device %d: %s", kid->device, kid->err);
+  }
   return SP_OK;
 }
 
@@ -1582,6 +1812,11 @@ int sp_slice_count(const sp_ctx* ctx, int64_t pts, int64_t* out) {
 
 int sp_equiprop_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double dt,
                        const sp_plan* plan, int reduction, void* d_u_out, void* stream) {
+  if (ctx && !ctx->kids.empty()) {
+    ctx->last_multi = false;
+    return sp_equiprop_device(ctx->kids[0], d_amps, pts, n_ctrl, dt, plan, reduction, d_u_out,
+                              stream);
+  }
   int rc = check_loaded(ctx);
   if (rc) return rc;
   if (reduction != SP_REDUCE_PAIRWISE && reduction != SP_REDUCE_SEQUENTIAL)
@@ -1599,6 +1834,13 @@ int sp_equiprop(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double
   if (reduction != SP_REDUCE_PAIRWISE && reduction != SP_REDUCE_SEQUENTIAL)
     return fail(ctx, SP_E_CONFIG, "unknown reduction %d", reduction);
   if (pts < 0) return fail(ctx, SP_E_SHAPE, "negative sample count");
+  if (!ctx->kids.empty()) {
+    if (n_ctrl != ctx->n_ctrl)
+      return fail(ctx, SP_E_SHAPE, "amplitude table has %d controls, system has %d", n_ctrl,
+                  ctx->n_ctrl);
+    ctx->last_multi = true;
+    return equiprop_multi(ctx, amps, pts, n_ctrl, dt, plan, reduction, u_out);
+  }
   rc = prepare_device(ctx);
   if (rc) return rc;
   cudaStream_t st = ctx->stream;
@@ -1630,6 +1872,12 @@ int sp_equiprop(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double
 
 int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, double dt,
                     const sp_plan* plan, void* u_all_out) {
+  if (ctx && !ctx->kids.empty()) {
+    ctx->last_multi = false;
+    const int rc = sp_equiprop_all(ctx->kids[0], amps, pts, n_ctrl, dt, plan, u_all_out);
+    if (rc) return fail(ctx, rc, "%s", ctx->kids[0]->err);
+    return SP_OK;
+  }
   int rc = check_loaded(ctx);
   if (rc) return rc;
   if (pts < 0) return fail(ctx, SP_E_SHAPE, "negative sample count");
@@ -1661,6 +1909,11 @@ int sp_equiprop_all(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, do
 
 int sp_equiprop_all_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl,
                            double dt, const sp_plan* plan, void* d_u_all_out, void* stream) {
+  if (ctx && !ctx->kids.empty()) {
+    ctx->last_multi = false;
+    return sp_equiprop_all_device(ctx->kids[0], d_amps, pts, n_ctrl, dt, plan, d_u_all_out,
+                                  stream);
+  }
   int rc = check_loaded(ctx);
   if (rc) return rc;
   if (pts < 0) return fail(ctx, SP_E_SHAPE, "negative sample count");
@@ -1672,6 +1925,8 @@ int sp_equiprop_all_device(sp_ctx* ctx, const double* d_amps, int64_t pts, int n
 
 int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction, void* d_out,
                       void* stream) {
+  if (ctx && !ctx->kids.empty())
+    return sp_product_device(ctx->kids[0], count, d_mats, reduction, d_out, stream);
   int rc = check_loaded(ctx);
   if (rc) return rc;
   if (count < 0) return fail(ctx, SP_E_SHAPE, "negative count");
@@ -1682,11 +1937,22 @@ int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction,
 }
 
 int sp_amplitude_violation(sp_ctx* ctx, int64_t* index) {
+  if (ctx && !ctx->kids.empty()) {
+    if (ctx->last_multi) {
+      if (index) *index = ctx->multi_viol;
+      return ctx->multi_viol >= 0 ? SP_E_AMPLITUDE_BOUND : SP_OK;
+    }
+    return sp_amplitude_violation(ctx->kids[0], index);
+  }
   if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
   return read_violation(ctx, nullptr, index);
 }
 
 int sp_set_algorithm(sp_ctx* ctx, int algo) {
+  for (sp_ctx* kid : ctx ? ctx->kids : std::vector<sp_ctx*>()) {
+    const int rc = sp_set_algorithm(kid, algo);
+    if (rc) return fail(ctx, rc, "%s", kid->err);
+  }
   if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
   if (algo < ALGO_AUTO || algo > ALGO_PS3)
     return fail(ctx, SP_E_CONFIG, "unknown algorithm %d (0 auto, 1 clenshaw, 2 ps, 3 ps3m)", algo);
@@ -1695,6 +1961,7 @@ int sp_set_algorithm(sp_ctx* ctx, int algo) {
 }
 
 int sp_last_algorithm(const sp_ctx* ctx, int* algo, int* gemms_per_slice) {
+  if (ctx && !ctx->kids.empty()) return sp_last_algorithm(ctx->kids[0], algo, gemms_per_slice);
   if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
   if (algo) *algo = ctx->last_algo;
   if (gemms_per_slice) *gemms_per_slice = ctx->last_gemms;
@@ -1702,12 +1969,19 @@ int sp_last_algorithm(const sp_ctx* ctx, int* algo, int* gemms_per_slice) {
 }
 
 int sp_last_lanes(const sp_ctx* ctx, int* lanes) {
+  if (ctx && !ctx->kids.empty()) {
+    int total = 0;
+    for (const sp_ctx* kid : ctx->kids) total += kid->last_lanes;
+    if (lanes) *lanes = total;
+    return SP_OK;
+  }
   if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
   if (lanes) *lanes = ctx->last_lanes;
   return SP_OK;
 }
 
 int sp_set_profiling(sp_ctx* ctx, int enabled) {
+  for (sp_ctx* kid : ctx ? ctx->kids : std::vector<sp_ctx*>()) sp_set_profiling(kid, enabled);
   if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
   ctx->prof = enabled != 0;
   return SP_OK;
@@ -1715,6 +1989,18 @@ int sp_set_profiling(sp_ctx* ctx, int enabled) {
 
 int sp_last_timing(const sp_ctx* cctx, double* main_kernel_ms, int* launches,
                    double* executed, char* kernel_name, int name_len) {
+  if (cctx && !cctx->kids.empty()) {
+    const int rc = sp_last_timing(cctx->kids[0], main_kernel_ms, launches, executed, kernel_name,
+                                  name_len);
+    if (rc) return rc;
+    if (cctx->last_multi) {
+      if (launches) *launches = cctx->launches;
+      double f = 0.0;
+      for (const sp_ctx* kid : cctx->kids) f += kid->flops;
+      if (executed) *executed = f;
+    }
+    return SP_OK;
+  }
   sp_ctx* ctx = const_cast<sp_ctx*>(cctx);
   if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
   if (ctx->ev_pending) {

@@ -26,6 +26,8 @@ struct SliceJob {
   int mode;               // SP_MODE_*
   double dt;
   double xs;              // 2 * scale / beta  (0 when beta == 0): "2X" factor
+  double scale;           // dt (midpoint) or 2 dt (three-point): the exponent scale
+  double xspan;           // 2 / span (0 when span == 0): X = xspan * G
   int m;                  // series order
   double coef[2 * (SP_MAX_ORDER + 1)];
   double phase[2];

@@ -138,11 +138,12 @@ class IntegratorContext:
     """
 
     def __init__(self, precision: Precision, m_max: int | None, checked: bool, device: int,
-                 backend: DeviceBackend | None = None):
+                 backend: DeviceBackend | None = None, devices: list[int] | None = None):
         self.precision = precision
         self.m_max = m_max
         self.checked = checked
-        self.device = device
+        self.devices = list(devices) if devices else [int(device)]
+        self.device = self.devices[0]
         # one batch backend per context (reference: one CpuBackend per
         # context, test_propagator.py:228-238); its name is "b200"
         self.backend = backend if backend is not None else DeviceBackend(device)
@@ -152,7 +153,8 @@ class IntegratorContext:
         self._magnus = False
         self._quadrature = Quadrature.MIDPOINT
         handle = ctypes.c_void_p()
-        check(lib.sp_create(ctypes.byref(handle), precision.bits, int(device)))
+        ids = (ctypes.c_int * len(self.devices))(*self.devices)
+        check(lib.sp_create(ctypes.byref(handle), precision.bits, len(self.devices), ids))
         self._handle = handle
 
     # -- lifecycle ---------------------------------------------------------
@@ -452,7 +454,7 @@ class IntegratorContext:
         a = ctypes.c_int()
         g = ctypes.c_int()
         check(lib.sp_last_algorithm(self._handle, ctypes.byref(a), ctypes.byref(g)), self._handle)
-        return {"algorithm": {0: "none", 1: "clenshaw", 2: "ps", 3: "ps3m"}.get(a.value, "?"),
+        return {"algorithm": {0: "none", 1: "clenshaw", 2: "ps", 3: "ps3m", 4: "clenshaw_fp32"}.get(a.value, "?"),
                 "gemms_per_slice": g.value}
 
     def last_lanes(self) -> int:
@@ -483,8 +485,13 @@ def _default_device() -> int:
 
 
 def create(precision="fp64", m_max: int | None = None, checked: bool = False,
-           backend=None, device: int | None = None) -> IntegratorContext:
-    """New propagation context on one B200 (``propagator.py:334-355``).
+           backend=None, device: int | None = None,
+           devices=None) -> IntegratorContext:
+    """New propagation context (``propagator.py:334-355``) on one B200, or
+    on several in this one process: ``devices=[0, 1, ...]`` (or an int
+    count) time-shards every ``equiprop`` over those GPUs — contiguous slice
+    blocks, one per device, block products gathered on ``devices[0]`` by
+    peer copies and multiplied in time order.
 
     precision "fp32" | "fp64"; m_max pins the series order (odd 3..25);
     checked enables the Hermiticity sanity pass.  backend accepts None, a
@@ -497,10 +504,16 @@ def create(precision="fp64", m_max: int | None = None, checked: bool = False,
         raise ConfigError(f"m_max override {m_max} not an odd integer in "
                           f"{ORDER_GRID[0]}..{ORDER_GRID[-1]}")
     dev = _default_device() if device is None else int(device)
+    if devices is not None:
+        devices = list(range(int(devices))) if isinstance(devices, int) else \
+            [int(x) for x in devices]
+        if not devices or any(x < 0 for x in devices) or len(devices) > 64:
+            raise ConfigError(f"devices must be 1..64 non-negative ordinals, got {devices!r}")
+        dev = devices[0]
     instance = None
     if isinstance(backend, DeviceBackend):
         instance, dev = backend, backend.device if device is None else dev
     elif backend is not None:
         if not isinstance(backend, str) or backend.lower() not in _BACKEND_TOKENS:
             raise ConfigError(f"unknown backend {backend!r}; expected one of {_BACKEND_TOKENS}")
-    return IntegratorContext(precision, m_max, bool(checked), dev, instance)
+    return IntegratorContext(precision, m_max, bool(checked), dev, instance, devices)

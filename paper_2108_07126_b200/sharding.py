@@ -19,7 +19,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .errors import ShapeError
+from .errors import AmplitudeBoundError, ShapeError
 from .hamiltonian import ControlAmplitudes, check_pair
 from .propagator import IntegratorContext, PropagatorResult
 
@@ -109,34 +109,73 @@ def equiprop_sharded(ctx: IntegratorContext, amps: ControlAmplitudes, *, group=N
 
 
 def equiprop_sharded_device(ctx: IntegratorContext, local_amps, dt: float, n_slices: int, *,
-                            group=None, stream=None, reduction: str = "pairwise"):
+                            group=None, stream=None, reduction: str = "pairwise",
+                            first_row: int | None = None):
     """Device path (bench / production): ``local_amps`` is this rank's
     (rows, N) float64 CUDA tensor (already halo-sliced), the block product is
     computed by the sm_100a lane kernel, the P blocks are all-gathered with
     NCCL into one (P, d, d) buffer and multiplied in order on the device by
-    ``sp_product_device``.  Returns the (d, d) complex128 CUDA tensor."""
+    ``sp_product_device``.  Returns the (d, d) result in the working dtype
+    (complex128 / complex64) on the device.
+
+    Validation is global and happens before the gather: the lane kernel
+    records this shard's first |c| > 1 / NaN sample, every rank contributes
+    its global row-major index (``first_row``: the shard's first table row,
+    default from the partition) to a MIN all-reduce, and all ranks raise the
+    same ``AmplitudeBoundError`` (reference message, hamiltonian.py:170-174)
+    instead of one rank raising while the others block in the collective.
+    Everything runs on ``stream`` (default: the current stream) so the
+    collective, the product and the allocator all order after the lane
+    kernel."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
     d = ctx._system.dim
+    n_ctrl = local_amps.shape[1]
     plan = ctx.plan_for(dt)
-    st = stream or torch.cuda.current_stream()
-    block = torch.empty((d, d), dtype=torch.complex128, device=local_amps.device)
-    if local_amps.shape[0] == 0:
-        block.copy_(torch.eye(d, dtype=torch.complex128))
-    else:
-        ctx.equiprop_device_ptr(local_amps.data_ptr(), local_amps.shape[0],
-                                local_amps.shape[1], dt, block.data_ptr(),
-                                stream=st.cuda_stream, reduction=reduction, plan=plan)
-    gathered = torch.empty((world, d, d), dtype=torch.complex128, device=local_amps.device)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(gathered, block, group=group)
-    else:  # gloo (CPU-side collective; used to exercise several ranks on one GPU)
-        parts = [torch.empty((d, d), dtype=torch.complex128) for _ in range(world)]
-        dist.all_gather(parts, block.cpu(), group=group)
-        gathered.copy_(torch.stack(parts))
-    out = torch.empty((d, d), dtype=torch.complex128, device=local_amps.device)
-    ctx.product_device_ptr(world, gathered.data_ptr(), out.data_ptr(), stream=st.cuda_stream,
-                           reduction=reduction)
+    st = stream or torch.cuda.current_stream(local_amps.device)
+    if first_row is None:
+        a, b = partition(n_slices, world)[rank]
+        first_row = shard_rows(ctx.mode, a, b)[0]
+    cdt = torch.complex64 if ctx.precision.bits == 32 else torch.complex128
+    nccl = dist.get_backend(group) == "nccl"
+    with torch.cuda.stream(st):
+        block = torch.empty((d, d), dtype=cdt, device=local_amps.device)
+        if local_amps.shape[0] == 0:
+            block.copy_(torch.eye(d, dtype=cdt))
+            local_viol = -1
+        else:
+            ctx.equiprop_device_ptr(local_amps.data_ptr(), local_amps.shape[0], n_ctrl, dt,
+                                    block.data_ptr(), stream=st.cuda_stream,
+                                    reduction=reduction, plan=plan)
+            local_viol = ctx.amplitude_violation()  # synchronises the lane pass
+        # global first offender (row-major over the full table) on every rank
+        none = torch.iinfo(torch.int64).max
+        gidx = first_row * n_ctrl + local_viol if local_viol >= 0 else none
+        red = torch.tensor([gidx], dtype=torch.int64,
+                           device=local_amps.device if nccl else "cpu")
+        dist.all_reduce(red, op=dist.ReduceOp.MIN, group=group)
+        gmin = int(red.item())
+        if gmin != none:
+            own = local_viol >= 0 and gidx == gmin
+            val = torch.tensor([float(local_amps.reshape(-1)[local_viol].item()) if own else 0.0],
+                               dtype=torch.float64, device=red.device)
+            dist.all_reduce(val, op=dist.ReduceOp.SUM, group=group)
+            k, i = divmod(gmin, max(1, n_ctrl))
+            raise AmplitudeBoundError(
+                f"control amplitude {float(val.item())!r} at sample {k}, "
+                f"control {i} lies outside [-1, 1]")
+        mine = block.to(torch.complex128)
+        gathered = torch.empty((world, d, d), dtype=torch.complex128, device=local_amps.device)
+        if nccl:
+            dist.all_gather_into_tensor(gathered, mine, group=group)
+        else:  # gloo (CPU-side collective; used to exercise several ranks on one GPU)
+            parts = [torch.empty((d, d), dtype=torch.complex128) for _ in range(world)]
+            dist.all_gather(parts, mine.cpu(), group=group)
+            gathered.copy_(torch.stack(parts))
+        out = torch.empty((d, d), dtype=cdt, device=local_amps.device)
+        ctx.product_device_ptr(world, gathered.data_ptr(), out.data_ptr(),
+                               stream=st.cuda_stream, reduction=reduction)
     return out, plan, n_slices

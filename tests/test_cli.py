@@ -27,7 +27,7 @@ def manifest(tmp_path, dt=0.1, data=None):
 def test_bounds_table(capsys):
     assert cli.main(["bounds"]) == 0
     out = capsys.readouterr().out.splitlines()
-    assert out[0] == "precision,m_max,capability"
+    assert out[0] == "precision,m,bound"
     assert "fp64,25,4.447" in out and "fp32,3,0.033" in out and "fp64,3,2e-04" in out
 
 

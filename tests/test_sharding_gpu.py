@@ -83,3 +83,70 @@ def test_nccl_world_of_one():
         assert np.linalg.norm(out.cpu().numpy() - ref) / np.linalg.norm(ref) <= 1e-13
     finally:
         dist.destroy_process_group()
+
+
+def _world_of_one():
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    return dist
+
+
+def test_sharded_device_fp32_and_side_stream():
+    """complex64 contexts through the device sharded path (block in the
+    working dtype, gathered as complex128, result complex64) on a
+    non-current stream (stream ordering of the collective)."""
+    import torch
+    from paper_2108_07126_b200.sharding import equiprop_sharded_device
+    dist = _world_of_one()
+    try:
+        h0, hs, values, dt = random_inputs(4, 2, 300, 21)
+        ctx = sp.create(precision="fp32")
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+        ref = ctx.equiprop(sp.ControlAmplitudes(values, dt)).u
+        side = torch.cuda.Stream()
+        out, _, _ = equiprop_sharded_device(ctx, torch.from_numpy(values).cuda(), dt, 300,
+                                            stream=side)
+        side.synchronize()
+        got = out.cpu().numpy()
+        assert got.dtype == np.complex64
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-6
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_device_validates_before_the_gather():
+    import torch
+    from paper_2108_07126_b200.sharding import equiprop_sharded_device
+    dist = _world_of_one()
+    try:
+        h0, hs, values, dt = random_inputs(8, 2, 100, 22)
+        values = values.copy()
+        values[37, 1] = 3.0
+        ctx = sp.create()
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+        with pytest.raises(sp.AmplitudeBoundError) as exc:
+            equiprop_sharded_device(ctx, torch.from_numpy(values).cuda(), dt, 100)
+        assert "sample 37, control 1" in str(exc.value)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_raise_the_same_violation():
+    """gloo world of 2 folded onto one GPU (torchrun): the bad sample sits in
+    rank 1's shard, and BOTH ranks raise the same AmplitudeBoundError instead
+    of rank 0 blocking in the gather."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", str(_free_port()),
+                        os.path.join(root, "tests", "_sharded_worker.py")],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("RANK")]
+    assert len(lines) == 2, r.stdout
+    msgs = {ln.split(":", 1)[1] for ln in lines}
+    assert len(msgs) == 1 and "sample 70, control 0" in msgs.pop()
