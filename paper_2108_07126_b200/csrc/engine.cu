@@ -1239,13 +1239,15 @@ double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
   //   d = 2, real Cayley-Hamilton pairs (bitwise Hermitian terms, midpoint,
   //          <= 2 controls): 125 + 16 m, +14 when m is not compiled in
   //          (3, 7, 13, 15)
-  //   d = 2, complex pairs (other modes / more controls): 269 + 16 m + 43 T
+  //   d = 2, complex pairs (other modes / more controls): 137 + 28.7 m + 16 T,
+  //          +40 for the three-point modes (within 3% of every point)
   //   d = 3, 4: 10.3 + 576 m + 64 T
   if (ctx->fam == FAM_S2) {
     const bool fast2 = ctx->herm_exact && ctx->mode == SP_MODE_MIDPOINT && ctx->n_terms <= 3;
     const bool compiled = m == 3 || m == 7 || m == 13 || m == 15;
     const double f = fast2 ? 125.0 + 16.0 * m + (compiled ? 0.0 : 14.0)
-                           : 269.0 + 16.0 * m + 43.0 * ctx->n_terms;
+                           : 137.0 + 28.7 * m + 16.0 * ctx->n_terms +
+                                 (ctx->mode == SP_MODE_MIDPOINT ? 0.0 : 40.0);
     return (double)n * f;
   }
   if (ctx->fam == FAM_S4) return (double)n * (10.3 + 576.0 * m + 64.0 * ctx->n_terms);

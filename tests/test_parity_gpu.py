@@ -113,7 +113,10 @@ def test_both_series_schemes_match_reference(case, algo, golden):
                         quadrature=None if mode == "magnus" else mode)
     amps = sp.ControlAmplitudes(values, dt)
     u = ctx.equiprop(amps).u
-    assert ctx.last_algorithm()["algorithm"] == algo
+    # complex64 contexts of the plain families (d <= 8) compute in complex64
+    # arithmetic with the reference's Clenshaw recurrence whatever the scheme
+    f32 = case["precision"] == "fp32" and case.get("d", 2) <= 8
+    assert ctx.last_algorithm()["algorithm"] == ("clenshaw_fp32" if f32 else algo)
     tol, _ = parity_tolerance(golden[f"{key}__u"], golden[f"{key}__u_seq"], case["precision"])
     assert rel_fro(u, golden[f"{key}__u"]) <= tol
     if case.get("cumulative"):
