@@ -14,8 +14,10 @@ ap.add_argument("--slices", type=int, default=2000)
 ap.add_argument("--repeat", type=int, default=2)
 a = ap.parse_args()
 wl = dict(bench.WORKLOADS[a.workload]); wl["slices"] = a.slices
-system, values, dt = bench.make_problem(wl)
-ctx = sp.create(); ctx.set_hamiltonian(system)
+h0, hs, values, dt = bench.make_problem(wl)
+ctx = sp.create()
+ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=wl["mode"] == "magnus",
+                    quadrature=None if wl["mode"] == "magnus" else wl["mode"])
 amps = sp.ControlAmplitudes(values, dt)
 for _ in range(a.repeat):
     u = ctx.equiprop(amps).u

@@ -8,10 +8,16 @@ amplitude table already in HBM, CUDA events on the launching stream, median
 of up to 3 steps after one warm-up).  Systems are the random unit-1-norm
 drift + 2 controls of C3(i) (seed 20240911, beta = 0.5 -> m = 13 fp64 / 7
 fp32), midpoint.  Points whose estimated GPU time exceeds --cap-s are skipped
-(d = 512 x 1e6 would take ~10 min).  The CPU column is the oracle (the
-reference algorithm, numpy/OpenBLAS on all host threads) on a bounded prefix
-of the same system, one rate per (dim, precision): its runtime is linear in
-the slice count (reference property, test_acceptance.py:229-245).
+(d = 512 x 1e6 would take ~10 min).  The CPU column is the reference
+itself (sliceprop from baseline/_ref through its public API, numpy/OpenBLAS
+on all host threads; bench.CpuArm, the oracle port only if the install is
+missing) on a bounded prefix of the same system, one rate per (dim,
+precision): its runtime is linear in the slice count (reference property,
+test_acceptance.py:229-245).  ``frac`` = executed flops of the lane kernel /
+its duration / the measured peak of the pipe it runs on (FP64 DMMA for the
+tensor-core families, FP64 DFMA for the d <= 4 register families, FP32 FFMA
+for the complex64 d <= 8 kernel); ``canonical_frac`` = the reference-algorithm
+work F(d, m, T) on the same denominator.
 """
 from __future__ import annotations
 
@@ -39,16 +45,21 @@ def canonical_flops(d, m, n_terms):
 
 
 def cpu_rate(h0, hs, values, dt, bits, target_s):
-    import oracle
-    n0 = 2 if h0.shape[0] >= 256 else 16 if h0.shape[0] >= 64 else 512
-    oracle.equiprop(h0, hs, values[:max(1, n0 // 4)], dt, bits=bits)
-    t0 = time.perf_counter()
-    oracle.equiprop(h0, hs, values[:n0], dt, bits=bits)
-    per = (time.perf_counter() - t0) / n0
-    n = int(max(n0, min(values.shape[0], target_s / max(per, 1e-9))))
-    t0 = time.perf_counter()
-    oracle.equiprop(h0, hs, values[:n], dt, bits=bits)
-    return n / (time.perf_counter() - t0), n
+    """(slices/s, prefix slices, kind) of the reference on the host cores."""
+    import bench
+    arm = bench.CpuArm(h0, hs, dt, "midpoint")
+    if bits == 32:
+        if arm.ref is not None:
+            arm.ctx.close()
+            arm.ctx = arm.ref.create(precision="fp32")
+            arm.ctx.set_hamiltonian(arm.ref.ControlSystem(h0, hs))
+        else:
+            import oracle
+            arm.run = lambda v, reduction="pairwise": oracle.equiprop(
+                h0, hs, v, dt, bits=32, reduction=reduction)[0]
+    s = arm.sample(values[:min(values.shape[0], 2_000_000)], target_s, repeats=1)
+    arm.close()
+    return s["rate"], s["slices"], arm.kind
 
 
 def main():
@@ -65,7 +76,12 @@ def main():
     from cases import unit_hermitian
 
     with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
-        peak = json.load(fh)["fp64_dmma_tflops"] * 1e12
+        peaks = json.load(fh)
+
+    def pipe_peak(kernel):
+        key = ("fp32_ffma_tflops" if kernel.startswith("lane_f32") else "fp64_dfma_tflops"
+               if kernel.startswith("lane_small") else "fp64_dmma_tflops")
+        return peaks[key] * 1e12
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
@@ -88,7 +104,7 @@ def main():
             out = torch.empty((d, d), dtype=torch.complex128 if bits == 64 else torch.complex64,
                               device=dev)
             rate_est = None
-            cpu, cpu_n = cpu_rate(h0, hs, values, dt, bits, args.cpu_s)
+            cpu, cpu_n, cpu_kind = cpu_rate(h0, hs, values, dt, bits, args.cpu_s)
             for n in SLICES:
                 if rate_est is not None and n / rate_est > args.cap_s:
                     rec = {"precision": prec, "dim": d, "slices": n, "skipped":
@@ -123,10 +139,11 @@ def main():
                        "slices_per_s": rate, "ms_per_step": step_ms,
                        "kernel": t["kernel"], "kernel_ms": kms, "launches": t["launches"],
                        "canonical_tflops": n * F / (step_ms / 1e3) / 1e12,
-                       "fp64_roofline_frac": n * F / (step_ms / 1e3) / peak,
-                       "executed_frac": t["executed_flops"] / (kms / 1e3) / peak,
-                       "series": ctx.last_algorithm(),
+                       "frac": t["executed_flops"] / (kms / 1e3) / pipe_peak(t["kernel"]),
+                       "canonical_frac": n * F / (kms / 1e3) / pipe_peak(t["kernel"]),
+                       "series": ctx.last_algorithm(), "lanes": ctx.last_lanes(),
                        "cpu_slices_per_s": cpu, "cpu_sample_slices": cpu_n,
+                       "cpu_kind": cpu_kind,
                        "gpu_over_cpu": rate / cpu}
                 print(json.dumps(rec), flush=True)
                 fh.write(json.dumps(rec) + "\n")
