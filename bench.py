@@ -70,8 +70,11 @@ WORKLOADS = {
                       "complex128 (m=3)"),
 }
 
-# secondary lines whose steps are seconds long run fewer timed steps
+# secondary lines whose steps are seconds long run fewer timed steps; the
+# microsecond-scale ones more (CUDA event timestamps tick in ~2 us steps on
+# this B200, so a mean over many steps is needed)
 SECONDARY_MAX_STEPS = {"c4m": 5}
+SECONDARY_MIN_STEPS = {"c1": 50, "c1m": 50, "c3": 10, "c3s": 10}
 
 
 def fp64_peaks():
@@ -352,7 +355,7 @@ def roofline_for(t, local_slices, wl, m, kern_ms, peaks):
     reference-algorithm work F(d, m, T) of SURVEY.md §8(d) on the same
     denominator (above 1 when the kernel needs fewer flops than the
     reference's Clenshaw count)."""
-    dfma = t["kernel"].startswith("lane_small")
+    dfma = t["kernel"].startswith(("lane_small", "lane_su2"))
     ffma = t["kernel"].startswith("lane_f32")
     peak = (peaks["fp32_ffma_tflops"] if ffma else peaks["fp64_dfma_tflops"] if dfma
             else peaks["fp64_dmma_tflops"]) * 1e12
@@ -370,7 +373,13 @@ def roofline_for(t, local_slices, wl, m, kern_ms, peaks):
                             f"algorithmic bytes/slice = {8 * wl['n_ctrl']} (amplitude row)")
     except (OSError, ValueError, KeyError):
         pass
-    return {"bound": "tensor", "achieved": executed / 1e12, "peak": peak / 1e12,
+    # amplitude bytes of the launch (midpoint: one row per slice; three-point
+    # modes: two new rows per slice) against the measured HBM copy bandwidth
+    rows = local_slices * (1 if wl["mode"] == "midpoint" else 2)
+    amp_bytes = rows * 8 * wl["n_ctrl"]
+    hbm_gbs = amp_bytes / (kern_ms / 1e3) / 1e9
+    hbm_peak = measured_hbm_gbs()
+    line = {"bound": "tensor", "achieved": executed / 1e12, "peak": peak / 1e12,
             "unit": "TFLOP/s", "frac": executed / peak, "traffic": traffic,
             "traffic_note": traffic_note, "kernel": t["kernel"], "kernel_ms": kern_ms,
             "executed_flops_per_launch": t["executed_flops"],
@@ -381,7 +390,25 @@ def roofline_for(t, local_slices, wl, m, kern_ms, peaks):
             "peak_source": "measured " + ("FP32 FFMA" if ffma else "FP64 DFMA" if dfma
                                           else "FP64 DMMA")
                            + " peak (tools/fp64_peak.cu, profiles/fp64_peak.json; "
-                             "MEASURED_PEAKS.json has no FP64 entry)"}
+                             "MEASURED_PEAKS.json has no FP64 entry)",
+            "amplitude_bytes_per_launch": amp_bytes, "hbm_achieved_gbs": hbm_gbs,
+            "hbm_peak_gbs": hbm_peak, "hbm_frac": hbm_gbs / hbm_peak if hbm_peak else None}
+    if hbm_peak and hbm_gbs / hbm_peak > executed / peak:
+        # the su(2) quaternion kernel executes ~34 FP64 instructions per 16-byte
+        # amplitude row: its bound is the amplitude stream, not the FP64 pipe
+        line.update({"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": hbm_gbs / hbm_peak, "fp64_frac": executed / peak,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy "
+                                    "bandwidth)"})
+    return line
+
+
+def measured_hbm_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6650.0  # B200_PROFILING.md fallback ("of fallback")
 
 
 def measure_gpu(args, name, rank, world, local_rank, dist, headline):
@@ -391,7 +418,8 @@ def measure_gpu(args, name, rank, world, local_rank, dist, headline):
     from paper_2108_07126_b200.sharding import (equiprop_sharded_device, partition,
                                                 shard_rows)
     wl = WORKLOADS[name]
-    steps = args.steps if headline else min(args.steps, SECONDARY_MAX_STEPS.get(name, 10**9))
+    steps = args.steps if headline else max(min(args.steps, SECONDARY_MAX_STEPS.get(name, 10**9)),
+                                            SECONDARY_MIN_STEPS.get(name, 0))
     h0, hs, values, dt = make_problem(wl)
     mode = wl["mode"]
     system = sp.ControlSystem(h0, hs)
@@ -408,7 +436,15 @@ def measure_gpu(args, name, rank, world, local_rank, dist, headline):
     dev = torch.device("cuda", local_rank)
     d_amps = torch.from_numpy(local.copy()).to(dev)
     out = torch.empty((d, d), dtype=torch.complex128, device=dev)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
+    # L2 flush between timed steps: write 256 MiB (> 126 MB L2), then read
+    # another 256 MiB so the write-backs of the flush itself finish before
+    # the timed region (L2 left cold for the inputs and clean)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    clean = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def l2_flush(k):
+        flush.fill_(float(k))
+        clean.sum()
     stream = torch.cuda.current_stream(dev)
 
     # amplitude validation (|c| <= 1) is part of the job: it runs inside the
@@ -460,7 +496,7 @@ def measure_gpu(args, name, rank, world, local_rank, dist, headline):
     kernel_ms, launches = [], 0
     with Clocks(local_rank) as clk:
         for k in range(steps):
-            flush.fill_(float(k))
+            l2_flush(k)
             evs[k][0].record(stream)
             if graph is not None:
                 graph.replay()
@@ -496,7 +532,7 @@ def measure_gpu(args, name, rank, world, local_rank, dist, headline):
     amps_obj = sp.ControlAmplitudes(pinned.numpy(), dt, copy=False) if world == 1 else None
     u = None
     for k in range(args.warmup + steps):
-        flush.fill_(float(k))
+        l2_flush(k)
         torch.cuda.synchronize(dev)
         if dist is not None:
             dist.barrier()
@@ -523,7 +559,7 @@ def measure_gpu(args, name, rank, world, local_rank, dist, headline):
            "config": {"workload": wl["label"], "dim": d, "n_ctrl": wl["n_ctrl"],
                       "slices": n, "mode": mode, "m": plan.m_max,
                       "n_terms": n_terms_for(wl), "lanes": lanes,
-                      "l2": "flushed between timed steps (256 MiB write)",
+                      "l2": "flushed between timed steps (256 MiB write, then 256 MiB read)",
                       "parallelism": f"time-sharded x{world}",
                       "cuda_graph": graph is not None}}
 

@@ -23,8 +23,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsliceprop_b200.so")
 SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "batch.cu"),
-           os.path.join(CSRC, "plan.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "kernels_tc.cuh", "kernels_ps.cuh", "kernels_ps3.cuh", "kernels_ps3g.cuh", "kernels_apply.cuh", "kernels_d8.cuh", "kernels_batch.cuh", "kernels_f32.cuh",
+           os.path.join(CSRC, "su2.cu"), os.path.join(CSRC, "plan.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "kernels_tc.cuh", "kernels_ps.cuh", "kernels_ps3.cuh", "kernels_ps3g.cuh", "kernels_apply.cuh", "kernels_d8.cuh", "kernels_batch.cuh", "kernels_f32.cuh", "kernels_su2.cuh",
                                                   "internal.h")] + [
     os.path.join(ROOT, "include", "sliceprop_b200.h")]
 
@@ -55,12 +55,36 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT,
     """Build the library (``out``/``defines``: instrumented variants for tools/)."""
     if not force and up_to_date(out):
         return out
-    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
-           "-I", CSRC, *SOURCES, "-o", out + ".tmp"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = res.stdout + res.stderr
+    # one nvcc per translation unit, in parallel, then one link step
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+    common = [nvcc(), *[f for f in NVCC_FLAGS if f != "-shared"],
+              *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    tmpdir = tempfile.mkdtemp(prefix="spbuild")
+    objs = [os.path.join(tmpdir, os.path.basename(src) + ".o") for src in SOURCES]
+
+    def compile_one(args):
+        src, obj = args
+        cmd = [*common, "-c", src, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return r.returncode, " ".join(cmd) + "\n" + r.stdout + r.stderr
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, zip(SOURCES, objs)))
+    log = "".join(r[1] for r in results)
+    rc = max(r[0] for r in results)
+    if rc == 0:
+        cmd = [nvcc(), "-shared", "-cudart", "static", "-Xcompiler", "-fPIC", *objs,
+               "-o", out + ".tmp"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        log += " ".join(cmd) + "\n" + r.stdout + r.stderr
+        rc = r.returncode
+    shutil.rmtree(tmpdir, ignore_errors=True)
+
+    class res:  # noqa: N801  (keeps the checks below unchanged)
+        returncode = rc
     with open(os.path.join(HERE, "build.log" if out == OUT else "build_variant.log"), "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + log)
+        fh.write(log)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{log[-4000:]}")
     if any(int(n) > 0 for n in re.findall(r"(\d+) bytes spill stores", log)):

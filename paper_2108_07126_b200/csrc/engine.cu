@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -70,7 +71,8 @@ using P3_256 = PS3Cfg<256, 16, 2, 2, 8, 1, 16, false>;
 using P3_512 = PS3Cfg<512, 8, 4, 1, 8, 1, 64, false>;
 
 enum Algo { ALGO_AUTO = 0, ALGO_CLENSHAW = 1, ALGO_PS = 2, ALGO_PS3 = 3,
-            ALGO_F32 = 4 /* reported only: the complex64-arithmetic lane kernel */ };
+            ALGO_F32 = 4 /* reported only: the complex64-arithmetic lane kernel */,
+            ALGO_SU2 = 5 /* reported only: the su(2) quaternion lane kernel */ };
 
 // GEMMs per slice: Clenshaw m; PS (s-1) + (r-1) + 1, r = ceil((m+1)/s)
 int ps_cost(int m, int s) {
@@ -154,6 +156,7 @@ int family_for(int d, int* D) {
 }
 
 const char* family_kernel_name(int fam, int algo) {
+  if (algo == 5) return "lane_su2_kernel";
   if (algo == 4)  // complex64 arithmetic (kernels_f32.cuh)
     return fam == FAM_S2 ? "lane_f32_kernel<2>" : fam == FAM_S4 ? "lane_f32_kernel<4>"
                                                                 : "lane_f32_kernel<8>";
@@ -209,6 +212,7 @@ struct sp_ctx {
   int dim = 0, n_ctrl = 0, n_terms = 0, mode = 0;
   std::vector<double> terms_host;  // T x d x d complex128 interleaved
   bool herm_exact = false;         // every term bitwise Hermitian
+  bool su2_terms = false;          // d = 2, every term bitwise Hermitian and traceless
   // device-side
   bool dev_ready = false;
   bool terms_uploaded = false;
@@ -902,6 +906,98 @@ int f32_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream
   return SP_OK;
 }
 
+// su(2) family: d = 2 traceless Hermitian terms, symmetric plan with
+// alternating coefficients (phase 1), fp64, pairwise, one fused launch
+// (kernels_su2.cuh).  SP_SU2=0 in the environment disables it (A/B timing).
+bool su2_applies(const sp_ctx* ctx, const SliceJob& job) {
+  static const int enabled = [] {
+    const char* e = getenv("SP_SU2");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  if (!enabled || !ctx->su2_terms || ctx->bits != 64 || !job.coef_alt) return false;
+  if (!(job.phase[0] == 1.0 && job.phase[1] == 0.0)) return false;
+  if (job.n_ctrl % 2 == 0 && ((uintptr_t)job.amps & 15u)) return false;  // vector row loads
+  return true;
+}
+
+int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_out,
+               const double2** prods, int* count) {
+  Su2Job sj;
+  std::memset(&sj, 0, sizeof(sj));
+  sj.amps = job.amps;
+  sj.n_slices = job.n_slices;
+  sj.n_ctrl = job.n_ctrl;
+  sj.mode = job.mode;
+  sj.m = job.m;
+  sj.dt6 = job.dt / 6.0;
+  for (int t = 0; t < ctx->n_terms; ++t) {
+    const double* h = &ctx->terms_host[(size_t)t * 8];  // 2 x 2 complex128, row-major
+    sj.tz[t][0] = job.xs * h[0];                        // H00 (= -H11)
+    sj.tz[t][1] = job.xs * h[2];                        // Re H01
+    sj.tz[t][2] = job.xs * h[3];                        // Im H01
+  }
+  for (int k = 0; k <= job.m; ++k) sj.cr[k] = job.coef[2 * k + (k & 1)];
+  sj.viol = job.viol;
+  sj.out = fused_out;
+  sj.to_fp32 = out32(ctx) ? 1 : 0;
+  // lanes: >= SPT slices each (tree and tail amortised), one CTA per SM
+  static const int spt = [] {
+    const char* e = getenv("SP_SU2_SPT");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  static const int tpb_env = [] {
+    const char* e = getenv("SP_SU2_TPB");
+    return e ? atoi(e) : 0;
+  }();
+  int tpb_max = su2_max_block(sj);
+  if (tpb_env >= 32) tpb_max = std::min(tpb_max, tpb_env & ~31);
+  const int64_t want = std::max<int64_t>(1, (job.n_slices + spt - 1) / spt);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->sms, (want + 31) / 32));
+  const int64_t per = (want + grid - 1) / grid;
+  const int block = (int)std::min<int64_t>(tpb_max, ((per + 31) / 32) * 32);
+  int rc = ensure(ctx, ctx->lanes, (size_t)grid * 4 * sizeof(double));
+  if (rc) return rc;
+  sj.cta_out = ctx->lanes.p;
+  if (!ctx->tailctr.p) {
+    rc = ensure(ctx, ctx->tailctr, sizeof(unsigned));
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->tailctr.p, 0, sizeof(unsigned), st));
+  }
+  sj.ctr = (unsigned*)ctx->tailctr.p;
+  // tools only: phase timestamps printed to stderr (SP_SU2_PROF=1)
+  static const bool phase_prof = getenv("SP_SU2_PROF") && getenv("SP_SU2_PROF")[0] == '1';
+  static unsigned long long* d_prof = nullptr;
+  if (phase_prof) {
+    if (!d_prof) CUDA_TRY(ctx, cudaMalloc(&d_prof, 16 * sizeof(unsigned long long)));
+    std::vector<unsigned long long> init(16);
+    for (int i = 0; i < 16; ++i) init[i] = (i & 1) ? 0ull : ~0ull;
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_prof, init.data(), 16 * 8, cudaMemcpyHostToDevice, st));
+    sj.prof = d_prof;
+  }
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+  CUDA_TRY(ctx, su2_run(sj, grid, block, st));
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+  if (phase_prof) {
+    unsigned long long h[16];
+    CUDA_TRY(ctx, cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    fprintf(stderr, "[su2 phases ns] n=%lld grid=%d block=%d", (long long)job.n_slices, grid,
+            block);
+    for (int k = 0; k < 6; ++k)
+      if (h[2 * k] != ~0ull)
+        fprintf(stderr, " p%d=[%lld,%lld]", k, (long long)(h[2 * k] - h[0]),
+                (long long)(h[2 * k + 1] - h[0]));
+    fprintf(stderr, "\n");
+  }
+  ++ctx->launches;
+  ctx->last_algo = ALGO_SU2;
+  ctx->last_gemms = job.m;
+  ctx->last_lanes = grid * block;
+  *prods = (const double2*)ctx->lanes.p;
+  *count = grid;
+  return SP_OK;
+}
+
 // Run the lane pass.  Returns the lane products (lane_count of them) on the
 // device, or (small families, pairwise) the per-CTA products.
 int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix_out,
@@ -912,6 +1008,9 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   int lanes = 1;
   if (f32_path(ctx)) return f32_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_T8) return d8_launch(ctx, job, prefix_out, st, prods, count);
+  if (ctx->fam == FAM_S2 && fused_out && cta_reduce && !prefix_out && !job.vinit &&
+      su2_applies(ctx, job))
+    return su2_launch(ctx, job, st, fused_out, prods, count);
   if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
     const int tpl = (ctx->fam == FAM_S2) ? 1 : 4;
     // pairwise: at least 4 slices per lane (short CTA tree and tail for the
@@ -1242,6 +1341,19 @@ double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
   //   d = 2, complex pairs (other modes / more controls): 137 + 28.7 m + 16 T,
   //          +40 for the three-point modes (within 3% of every point)
   //   d = 3, 4: 10.3 + 576 m + 64 T
+  if (ctx->last_algo == ALGO_SU2) {
+    // su(2) quaternion kernel (flops, DFMA = 2): 3 FMA per control term
+    // (assembly), 5 for zeta2, 4 per Clenshaw step after the peeled one
+    // (+2 at j = 0), 3 MUL for U, 28 for V <- U V; three-point control
+    // weights 4 each (the /6 counted as one), magnus commutator weights
+    // 2 (drift) / 4 (cross) each — calibrated in profiles/r02_ncu_su2.md
+    const int N = ctx->n_ctrl, T = ctx->n_terms;
+    double w = 0.0;
+    if (ctx->mode != SP_MODE_MIDPOINT) w += 4.0 * N;
+    if (ctx->mode == SP_MODE_MAGNUS) w += 2.0 * N + 4.0 * (N * (N - 1) / 2);
+    const double f = 6.0 * (T - 1) + 5.0 + 4.0 * (m - 1) + 2.0 + 3.0 + 28.0 + w;
+    return (double)n * f;
+  }
   if (ctx->fam == FAM_S2) {
     const bool fast2 = ctx->herm_exact && ctx->mode == SP_MODE_MIDPOINT && ctx->n_terms <= 3;
     const bool compiled = m == 3 || m == 7 || m == 13 || m == 15;
@@ -1793,6 +1905,13 @@ int sp_set_hamiltonian(sp_ctx* ctx, int dim, int n_ctrl, int n_terms, int mode,
           break;
         }
       }
+  // su(2) family (kernels_su2.cuh): 2 x 2 terms that are bitwise Hermitian
+  // and traceless, at most SU2_MAX_CTRL controls
+  ctx->su2_terms = dim == 2 && ctx->herm_exact && n_ctrl >= 1 && n_ctrl <= SU2_MAX_CTRL &&
+                   n_terms <= SU2_MAX_TERMS;
+  for (int t = 0; t < n_terms && ctx->su2_terms; ++t)
+    if (!(ctx->terms_host[(size_t)t * 8 + 0] == -ctx->terms_host[(size_t)t * 8 + 6]))
+      ctx->su2_terms = false;
   ctx->fam = fam;
   ctx->D = D;
   ctx->terms_uploaded = false;

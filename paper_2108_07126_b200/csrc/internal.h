@@ -5,6 +5,8 @@
 
 #include "sliceprop_b200.h"
 
+#include <cuda_runtime.h>
+
 namespace sp {
 
 int bessel_j(int k, double x, double* out, char* err, size_t errlen);
@@ -50,5 +52,33 @@ struct SliceJob {
   // second pass of the d = 2 cumulative path (lane_small_kernel)
   const void* vinit;
 };
+
+// Family SU2 (kernels_su2.cuh): d = 2, every term bitwise Hermitian and
+// traceless, symmetric plan with alternating coefficients, fp64, pairwise
+// reduction fused into the one launch.
+constexpr int SU2_MAX_TERMS = 16;
+constexpr int SU2_MAX_CTRL = 4;
+struct Su2Job {
+  const double* amps;  // (pts, n_ctrl) float64, 16-byte aligned rows when n_ctrl is even
+  int64_t n_slices;
+  int n_ctrl;
+  int mode;
+  int m;
+  double dt6;                       // dt / 6 (magnus commutator weights)
+  double tz[SU2_MAX_TERMS][3];      // per term: 2X factor x (H00, Re H01, Im H01)
+  double cr[SP_MAX_ORDER + 1];      // nonzero component of a_k: Re (k even), Im (k odd)
+  unsigned long long* viol;         // violation slots (epoch scheme of SliceJob), or null
+  unsigned* ctr;                    // arrival counter (zero between launches)
+  void* cta_out;                    // gridDim x 4 doubles: CTA products
+  void* out;                        // 2 x 2 result (complex128, or complex64 if to_fp32)
+  int to_fp32;
+  // phase timestamps (tools only, SP_SU2_PROF=1): [2k] = min, [2k+1] = max
+  // over CTAs of %globaltimer at phase k; null = off
+  unsigned long long* prof;
+};
+// launch lane_su2_kernel (su2.cu); grid x block threads are the lanes
+cudaError_t su2_run(const Su2Job& job, int grid, int block, cudaStream_t st);
+// registers / max threads of the instance a job would launch (host tuning)
+int su2_max_block(const Su2Job& job);
 
 }  // namespace sp

@@ -1,0 +1,515 @@
+// Family SU2: d = 2 systems whose expansion terms are all bitwise Hermitian
+// and traceless (the paper's driven qubit, any su(2) drive), symmetric plan.
+//
+// Why a separate family.  With Z = 2X = Z' traceless Hermitian (Z'^2 =
+// zeta2 I, zeta2 = dz^2 + |zc|^2 real) and the alternating plan coefficients
+// a_k = (-i)^k J_k(beta) (chebyshev.py:213-214; exact zeros in the other
+// component, checked on the host), the reference's Clenshaw recurrence
+// (chebyshev.py:298-303) on coefficient pairs b_j = A_j I + B_j Z' keeps A_j
+// purely real / imaginary by the parity of j and B_j by the parity of j + 1,
+// so it runs on ONE real number per pair entry:
+//     A_j = c_j + zeta2 B_{j+1} - beta_j A_{j+2},   B_j = A_{j+1} - beta_j B_{j+2}
+// (c_j = the nonzero component of a_j, beta_0 = 2, else 1), and
+//     U = A_0 I + i b_0 Z' = [[p, q], [-conj(q), conj(p)]],
+//     p = (A_0, b_0 dz),  q = (-b_0 Im zc, b_0 Re zc)      (Z'01 = zc)
+// — the same U, entry for entry, as lane_small_kernel<2,1>'s real pair path
+// (the dropped terms are exact zeros there).  Such matrices form the
+// quaternion algebra: closed under products, so every running product
+// V = U_k ... U_0 is [[v0, v1], [-conj(v1), conj(v0)]] and is carried as
+// (v0, v1): 4 doubles, 16 FP64 operations per product instead of 32, and the
+// row-0 entries are computed with exactly the reference's entry formula
+// (row 0 of U times V, same operand order).
+//
+// Per slice (midpoint, N controls, m compiled in): 3N FMA of assembly, 3 for
+// zeta2, ~2(m-1) for Clenshaw, 3 MUL for U, 16 for V <- U V: ~35 FP64
+// instructions at the qubit's N = 2, m = 3 — below the 16 B amplitude row's
+// share of HBM bandwidth, so a call streams the table at HBM speed.
+//
+// Structure: one CTA per SM (up to 1024 threads), each thread a lane of
+// contiguous slices whose amplitude rows stream DS slices ahead through a
+// per-thread cp.async ring in shared memory (~192 KB in flight per SM); ordered warp-shuffle products (later lanes on the
+// left), the CTA's warp products by warp 0, then the last CTA to arrive
+// (one acq_rel ticket) multiplies the <= 148 CTA products in time order and
+// writes the d x d result: the whole equiprop is one launch.
+// Amplitude bounds (|c| <= 1, NaN) are accumulated into a predicate; a lane
+// that saw an offender rescans its own rows for the first one (row-major)
+// and records it in the epoch slot (SliceJob::viol) — no branch per slice.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace sp {
+
+struct Quat {  // [[a, b], [-conj(b), conj(a)]]
+  double ar, ai, br, bi;
+};
+
+// tools only: %globaltimer at phase k, min / max over the CTAs (thread 0)
+__device__ __forceinline__ void su2_mark(const Su2Job& job, int k) {
+  if (job.prof != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(job.prof + 2 * k, t);
+    atomicMax(job.prof + 2 * k + 1, t);
+  }
+}
+
+__device__ __forceinline__ Quat quat_identity() { return Quat{1.0, 0.0, 0.0, 0.0}; }
+
+// P Q (P later in time, on the left): row 0 of the 2 x 2 complex product
+// with Q10 = -conj(Q.b), Q11 = conj(Q.a), summed in mat_mul's order
+__device__ __forceinline__ Quat quat_mul(const Quat& P, const Quat& Q) {
+  Quat R;
+  double re = P.ar * Q.ar;
+  re = fma(-P.ai, Q.ai, re);
+  re = fma(P.br, -Q.br, re);
+  re = fma(-P.bi, Q.bi, re);
+  double im = P.ar * Q.ai;
+  im = fma(P.ai, Q.ar, im);
+  im = fma(P.br, Q.bi, im);
+  im = fma(P.bi, -Q.br, im);
+  R.ar = re;
+  R.ai = im;
+  re = P.ar * Q.br;
+  re = fma(-P.ai, Q.bi, re);
+  re = fma(P.br, Q.ar, re);
+  re = fma(-P.bi, -Q.ai, re);
+  im = P.ar * Q.bi;
+  im = fma(P.ai, Q.br, im);
+  im = fma(P.br, -Q.ai, im);
+  im = fma(P.bi, Q.ar, im);
+  R.br = re;
+  R.bi = im;
+  return R;
+}
+
+__device__ __forceinline__ Quat quat_shfl_down(const Quat& q, int k) {
+  return Quat{__shfl_down_sync(0xffffffffu, q.ar, k), __shfl_down_sync(0xffffffffu, q.ai, k),
+              __shfl_down_sync(0xffffffffu, q.br, k), __shfl_down_sync(0xffffffffu, q.bi, k)};
+}
+
+// lane 0 ends with M_{31} ... M_1 M_0 (later lanes on the left)
+__device__ __forceinline__ void quat_warp_product(Quat& q) {
+#pragma unroll
+  for (int k = 1; k < 32; k <<= 1) q = quat_mul(quat_shfl_down(q, k), q);
+}
+
+// |v| <= 1 fails (also for NaN): accumulated without a branch
+__device__ __forceinline__ bool amp_bad(double v) { return !(fabs(v) <= 1.0); }
+
+template <int MODE, int NCC>
+struct Su2Shape {
+  // doubles read per slice: midpoint one row; three-point the rows 2s+1, 2s+2
+  // (row 2s is the previous slice's last row)
+  static constexpr int K = MODE == SP_MODE_MIDPOINT ? NCC : 2 * NCC;
+  static constexpr bool VEC = (NCC % 2) == 0;  // 16-byte rows (host-checked alignment)
+  static constexpr int UNIT = VEC ? 16 : 8;    // bytes per cp.async
+  static constexpr int CP = K * 8 / UNIT;      // cp.async per slice
+  // threads per CTA: 1024 (64 registers) except the three-point forms with
+  // >= 3 controls, whose weights need more registers
+  static constexpr int TPB = (MODE != SP_MODE_MIDPOINT && NCC >= 3) ? 512 : 1024;
+  // shared-memory ring: DS slices per thread in flight (<= 192 KB per CTA:
+  // the bytes in flight an SM needs to stream HBM at speed)
+  static constexpr int DS_RAW = (192 * 1024) / (TPB * K * 8);
+  static constexpr int DS = DS_RAW < 2 ? 2 : (DS_RAW > 16 ? 16 : DS_RAW);
+  static constexpr int SMEM_PER_THREAD = DS * K * 8;
+};
+
+__device__ __forceinline__ unsigned su2_smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+template <int UNIT>
+__device__ __forceinline__ void su2_cp_async(void* dst, const void* src) {
+  if constexpr (UNIT == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su2_smem_u32(dst)),
+                 "l"(src)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su2_smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void su2_cp_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void su2_cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// first offender of rows [r0, r1] (row-major index), ~0 if none
+__device__ __noinline__ unsigned long long su2_first_bad(const double* amps, int64_t r0,
+                                                         int64_t r1, int N) {
+  for (int64_t r = r0; r <= r1; ++r)
+    for (int c = 0; c < N; ++c)
+      if (amp_bad(amps[r * N + c])) return (unsigned long long)(r * N + c);
+  return ~0ull;
+}
+
+// One slice's propagator: weights from the slice's amplitude samples `cur`
+// (and, for the three-point modes, the carried row 2s in r1),
+// Z' = sum_t w_t tz_t, the real Clenshaw pairs, U = A I + i B Z'.
+template <int MODE, int NCC, int MC>
+__device__ __forceinline__ Quat su2_u(const Su2Job& job, int m, const double* cur,
+                                      double (&r1)[NCC]) {
+  constexpr int T = MODE == SP_MODE_MAGNUS ? 1 + 2 * NCC + NCC * (NCC - 1) / 2 : 1 + NCC;
+  static_assert(T <= SU2_MAX_TERMS, "too many su(2) terms");
+  // ---- slice weights (hamiltonian.py:199-205, magnus.py:88-106) and
+  // Z' = sum_t w_t tz_t (2X factor folded into tz on the host)
+  double dz = job.tz[0][0], zx = job.tz[0][1], zy = job.tz[0][2];
+  auto add = [&](int t, double w) {
+    dz = fma(w, job.tz[t][0], dz);
+    zx = fma(w, job.tz[t][1], zx);
+    zy = fma(w, job.tz[t][2], zy);
+  };
+  if constexpr (MODE == SP_MODE_MIDPOINT) {
+#pragma unroll
+    for (int q = 0; q < NCC; ++q) add(1 + q, cur[q]);
+  } else {
+    const double* c2 = cur;        // row 2s + 1
+    const double* c3 = cur + NCC;  // row 2s + 2
+#pragma unroll
+    for (int q = 0; q < NCC; ++q) add(1 + q, (r1[q] + 4.0 * c2[q] + c3[q]) / 6.0);
+    if constexpr (MODE == SP_MODE_MAGNUS) {
+#pragma unroll
+      for (int q = 0; q < NCC; ++q) add(1 + NCC + q, job.dt6 * (c3[q] - r1[q]));
+      int t = 1 + 2 * NCC;
+#pragma unroll
+      for (int a = 0; a < NCC; ++a)
+#pragma unroll
+        for (int b = a + 1; b < NCC; ++b) add(t++, job.dt6 * (r1[a] * c3[b] - c3[a] * r1[b]));
+    }
+#pragma unroll
+    for (int q = 0; q < NCC; ++q) r1[q] = c3[q];
+  }
+  const double zeta2 = fma(dz, dz, fma(zx, zx, zy * zy));
+  // ---- real Clenshaw pairs; the j = m - 1 step peeled (B_{m+1} = 0)
+  double A = job.cr[m - 1], B = job.cr[m], oA = job.cr[m], oB = 0.0;
+  constexpr int MU = MC > 0 ? MC : 1;
+#pragma unroll MU
+  for (int jj = m - 2; jj >= 0; --jj) {
+    const double beta = (jj == 0) ? 2.0 : 1.0;
+    const double nA = job.cr[jj] + fma(zeta2, B, -beta * oA);
+    const double nB = A - beta * oB;
+    oA = A;
+    oB = B;
+    A = nA;
+    B = nB;
+  }
+  return Quat{A, B * dz, -(B * zy), B * zx};
+}
+
+// V <- U(slice) V
+template <int MODE, int NCC, int MC>
+__device__ __forceinline__ void su2_slice(const Su2Job& job, int m, const double* cur,
+                                          double (&r1)[NCC], Quat& V) {
+  V = quat_mul(su2_u<MODE, NCC, MC>(job, m, cur, r1), V);
+}
+
+// After the lane loops: the lane's first amplitude offender (rare path; rows
+// [r0, rl] of the table), the ordered CTA product, the arrival ticket and, in
+// the last CTA, the ordered product of the CTA products and the d x d result.
+template <int NCC>
+__device__ __forceinline__ void su2_finish(const Su2Job& job, Quat V, bool bad, int64_t r0,
+                                           int64_t rl) {
+  if (bad && job.viol) {
+    const unsigned long long v = su2_first_bad(job.amps, r0, rl, NCC);
+    unsigned long long* slot = job.viol + (__ldcg(job.viol + 3) & 1ull);
+    atomicMin(slot, v);
+  }
+  // ---- ordered products: warps, then the CTA's warps (warp 0)
+  __shared__ Quat wq[32];
+  __shared__ bool last;
+  const int ln = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  auto cta_product = [&](Quat& q) {  // result in thread 0
+    quat_warp_product(q);
+    if (ln == 0) wq[wp] = q;
+    __syncthreads();
+    if (wp == 0) {
+      q = ln < nw ? wq[ln] : quat_identity();
+      quat_warp_product(q);
+    }
+    __syncthreads();
+  };
+  su2_mark(job, 2);
+  cta_product(V);
+  su2_mark(job, 3);
+  if (threadIdx.x == 0) {
+    reinterpret_cast<Quat*>(job.cta_out)[blockIdx.x] = V;
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old)
+                 : "l"(job.ctr)
+                 : "memory");
+    last = (old == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  su2_mark(job, 4);
+  // ---- fused tail: every thread folds a contiguous run of CTA products
+  // (later on the left), then one CTA-wide ordered product
+  const int G = (int)gridDim.x, per = (G + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int i0 = min(G, (int)threadIdx.x * per), i1 = min(G, i0 + per);
+  const double2* cp = reinterpret_cast<const double2*>(job.cta_out);
+  Quat M = quat_identity();
+  for (int i = i0; i < i1; ++i) {
+    const double2 a = __ldcg(cp + 2 * i), b = __ldcg(cp + 2 * i + 1);
+    M = quat_mul(Quat{a.x, a.y, b.x, b.y}, M);
+  }
+  cta_product(M);
+  if (threadIdx.x == 0) {
+    // [[a, b], [-conj(b), conj(a)]] in the output dtype
+    const double e[8] = {M.ar, M.ai, M.br, M.bi, -M.br, M.bi, M.ar, -M.ai};
+    if (job.to_fp32) {
+      float* o = reinterpret_cast<float*>(job.out);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (float)e[i];
+    } else {
+      double* o = reinterpret_cast<double*>(job.out);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = e[i];
+    }
+    su2_mark(job, 5);
+    *job.ctr = 0;  // ready for the next launch
+    if (job.viol) {  // rotate the violation slots (SliceJob::viol)
+      const unsigned long long ep = __ldcg(job.viol + 3);
+      job.viol[(ep + 1) & 1ull] = ~0ull;
+      job.viol[2] = ~0ull;
+      job.viol[3] = ep + 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// General form: every mode and control count.  Lane = contiguous slices
+// [lane n / lanes, (lane + 1) n / lanes); the rows stream through a
+// per-thread cp.async ring in shared memory.
+// ---------------------------------------------------------------------------
+template <int MODE, int NCC, int MC>
+__global__ void __launch_bounds__(Su2Shape<MODE, NCC>::TPB, 1) lane_su2_kernel(const Su2Job job) {
+  using S = Su2Shape<MODE, NCC>;
+  constexpr int K = S::K, DS = S::DS, CP = S::CP, UNIT = S::UNIT;
+  extern __shared__ __align__(16) unsigned char su2_ring[];
+  const int m = MC > 0 ? MC : job.m;
+  const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lanes = gridDim.x * blockDim.x;
+  const int64_t s0 = (int64_t)lane * job.n_slices / lanes;
+  const int64_t s1 = ((int64_t)lane + 1) * job.n_slices / lanes;
+  const int cnt = (int)(s1 - s0);
+
+  Quat V = quat_identity();
+  bool bad = false;
+  // first unit of this lane: row s0 (midpoint) or rows 2 s0 + 1, 2 s0 + 2
+  const unsigned char* unit0 = reinterpret_cast<const unsigned char*>(
+      job.amps + (MODE == SP_MODE_MIDPOINT ? s0 * NCC : (2 * s0 + 1) * NCC));
+  double r1[NCC];  // three-point: row 2s of the current slice
+  if constexpr (MODE != SP_MODE_MIDPOINT) {
+    if (cnt > 0) {
+#pragma unroll
+      for (int q = 0; q < NCC; ++q) {
+        r1[q] = __ldg(job.amps + 2 * s0 * NCC + q);
+        bad |= amp_bad(r1[q]);
+      }
+    }
+  }
+  // ring slot j, copy q of this thread: [slot][copy][thread] x UNIT bytes
+  // (a warp's copies and reads are contiguous: no bank conflicts)
+  const int nt = blockDim.x;
+  auto slot_ptr = [&](int j, int q) {
+    return su2_ring + ((size_t)(j * CP + q) * nt + threadIdx.x) * UNIT;
+  };
+  auto issue = [&](int k, int j) {  // unit k of the lane into slot j
+    if (k < cnt) {
+#pragma unroll
+      for (int q = 0; q < CP; ++q)
+        su2_cp_async<UNIT>(slot_ptr(j, q), unit0 + (size_t)k * K * 8 + q * UNIT);
+    }
+    su2_cp_commit();
+  };
+#pragma unroll
+  for (int j = 0; j < DS - 1; ++j) issue(j, j);
+
+  for (int k0 = 0; k0 < cnt; k0 += DS) {
+#pragma unroll
+    for (int j = 0; j < DS; ++j) {
+      if (k0 + j < cnt) {
+        issue(k0 + j + DS - 1, (j + DS - 1) % DS);
+        su2_cp_wait<DS - 1>();
+        double cur[K];
+#pragma unroll
+        for (int q = 0; q < CP; ++q) {
+          if constexpr (UNIT == 16) {
+            const double2 t = *reinterpret_cast<const double2*>(slot_ptr(j, q));
+            cur[2 * q] = t.x;
+            cur[2 * q + 1] = t.y;
+          } else {
+            cur[q] = *reinterpret_cast<const double*>(slot_ptr(j, q));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < K; ++q) bad |= amp_bad(cur[q]);
+        su2_slice<MODE, NCC, MC>(job, m, cur, r1, V);
+      }
+    }
+  }
+  su2_finish<NCC>(job, V, bad, MODE == SP_MODE_MIDPOINT ? s0 : 2 * s0,
+                  MODE == SP_MODE_MIDPOINT ? s1 - 1 : 2 * s1);
+}
+
+// ---------------------------------------------------------------------------
+// TMA form: midpoint, NCC in {2, 4} (the driven qubit).  Every lane owns L
+// consecutive slices (the last used lane fewer); the table is a 2-D tensor
+// [lane][L x NCC doubles] and one cp.async.bulk.tensor per warp and round
+// brings the next C rows of the warp's 32 lanes (32 x C x NCC x 8 bytes,
+// 128/64-byte swizzled so each thread's row reads are bank-conflict free)
+// into the warp's ring of NST stages, completion on the stage's mbarrier.
+// The partial last lane reads its rows from global memory directly.
+// ---------------------------------------------------------------------------
+template <int NCC, int C>
+struct Su2Tma {
+  static constexpr int ROWB = NCC * 8;       // bytes per amplitude row
+  static constexpr int LROWB = C * ROWB;     // bytes per lane per round (64 or 128)
+  static_assert(LROWB == 64 || LROWB == 128, "swizzle span");
+  static_assert(C % 2 == 0, "rounds are taken in slice pairs");
+  static constexpr int STAGE = 32 * LROWB;   // bytes per warp per stage
+  static constexpr int TPB = LROWB == 128 ? 512 : 1024;
+  static constexpr int NST = (192 * 1024) / ((TPB / 32) * STAGE);  // stages per warp
+  static constexpr int SMEM = (TPB / 32) * NST * STAGE + 1024;     // + alignment slack
+};
+
+__device__ __forceinline__ void su2_mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su2_smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void su2_mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su2_smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void su2_mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(su2_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void su2_tma_2d(void* dst, const void* tmap, int x, int y,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su2_smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(su2_smem_u32(bar))
+      : "memory");
+}
+
+template <int NCC, int MC, int C>
+__global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
+    lane_su2_tma_kernel(const Su2Job job, const __grid_constant__ CUtensorMap tmap,
+                        const int64_t L) {
+  using G = Su2Tma<NCC, C>;
+  constexpr int NST = G::NST, STAGE = G::STAGE, LROWB = G::LROWB, ROWB = G::ROWB;
+  extern __shared__ unsigned char su2_tma_raw[];
+  __shared__ __align__(8) uint64_t bars[(G::TPB / 32) * NST];
+  // 1024-byte aligned ring (the swizzle pattern follows absolute address
+  // bits); offsets from the shared array keep every access in the shared
+  // window (LDS, not generic loads)
+  const unsigned raw_u32 = su2_smem_u32(su2_tma_raw);
+  unsigned char* base = su2_tma_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
+  const int m = MC > 0 ? MC : job.m;
+  const int ln = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int64_t lane = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t wlane0 = lane - ln;  // first lane of the warp
+  const int64_t n = job.n_slices;
+  const int64_t s0 = min(n, lane * L), s1 = min(n, s0 + L);
+  const int cnt = (int)(s1 - s0);
+  const int64_t full = n / L;          // lanes with exactly L slices (tensor rows)
+  const bool direct = lane == full;    // the partial last lane: global loads
+  // rounds the warp needs: its first lane has the most slices
+  const int64_t wcnt = min(L, max((int64_t)0, n - wlane0 * L));
+  const int rounds = (int)((wcnt + C - 1) / C);
+  unsigned char* ring = base + (size_t)wp * NST * STAGE;
+  uint64_t* wb = bars + wp * NST;
+  const bool tma_warp = wlane0 < full;  // at least one tensor row in the box
+  su2_mark(job, 0);
+  if (ln == 0 && tma_warp) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) su2_mbar_init(wb + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < NST; ++s)
+      if (s < rounds) {
+        su2_mbar_expect_tx(wb + s, STAGE);
+        su2_tma_2d(ring + s * STAGE, &tmap, s * C * NCC, (int)wlane0, wb + s);
+      }
+  }
+  __syncwarp();
+
+  Quat V = quat_identity();
+  bool bad = false;
+  double r1[NCC];
+  const int sw = LROWB == 128 ? (ln & 7) : ((ln >> 1) & 3);  // swizzle of this lane's row
+  for (int r = 0; r < rounds; ++r) {
+    const int s = r % NST;
+    if (tma_warp) su2_mbar_wait(wb + s, (unsigned)((r / NST) & 1));
+    if (r == 0) su2_mark(job, 1);
+    const unsigned row = su2_smem_u32(ring + s * STAGE) + ln * LROWB;
+    auto smem_row = [&](int k, double (&cur)[NCC]) {
+#pragma unroll
+      for (int q = 0; q < NCC / 2; ++q) {
+        const int chunk = (k * ROWB) / 16 + q;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                     : "=d"(cur[2 * q]), "=d"(cur[2 * q + 1])
+                     : "r"(row + ((chunk ^ sw) << 4)));
+      }
+    };
+    if (!direct && (r + 1) * C <= cnt) {
+      // a whole round: the C slice propagators are independent (ILP), the
+      // running product takes them in adjacent pairs, later on the left
+      Quat U[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        double cur[NCC];
+        smem_row(k, cur);
+#pragma unroll
+        for (int q = 0; q < NCC; ++q) bad |= amp_bad(cur[q]);
+        U[k] = su2_u<SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1);
+      }
+#pragma unroll
+      for (int k = 0; k < C; k += 2) V = quat_mul(quat_mul(U[k + 1], U[k]), V);
+    } else {
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const int kk = r * C + k;
+        if (kk < cnt) {
+          double cur[NCC];
+          if (!direct) {
+            smem_row(k, cur);
+          } else {
+#pragma unroll
+            for (int q = 0; q < NCC; ++q) cur[q] = __ldg(job.amps + (s0 + kk) * NCC + q);
+          }
+#pragma unroll
+          for (int q = 0; q < NCC; ++q) bad |= amp_bad(cur[q]);
+          su2_slice<SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1, V);
+        }
+      }
+    }
+    __syncwarp();
+    if (ln == 0 && tma_warp && r + NST < rounds) {
+      // every lane is done with stage s (syncwarp): refill it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      su2_mbar_expect_tx(wb + s, STAGE);
+      su2_tma_2d(ring + s * STAGE, &tmap, (r + NST) * C * NCC, (int)wlane0, wb + s);
+    }
+  }
+  su2_finish<NCC>(job, V, bad, s0, s1 - 1);
+}
+
+}  // namespace sp
