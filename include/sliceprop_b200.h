@@ -171,6 +171,23 @@ int sp_gemm_batched_device(int precision_bits, int dim, int64_t count, const voi
                            const double* alpha, const double* beta, const double* gamma,
                            void* d_c, int64_t stride_c, void* stream);
 
+/* state propagation (apply, propagator.py:105-118): out[k] = U psi_k
+ * (kind 0: count x d vectors) or U rho_k U^+ (kind 1: count x d x d density
+ * matrices, through d_scratch of sp_apply_batch_scratch_bytes), U and the
+ * states device-resident in the working dtype. */
+size_t sp_apply_batch_scratch_bytes(int precision_bits, int dim, int64_t count, int kind);
+int sp_apply_batch_device(int precision_bits, int dim, const void* d_u, int64_t count, int kind,
+                          const void* d_states, void* d_out, void* d_scratch, void* stream);
+
+/* ---- analytic oracle on the device (studies.py:123-153) -----------------
+ * The driven qubit H(t) = (w0/2) sz + (w1/2)(cos(wrf t) sx + sin(wrf t) sy)
+ * propagated over steps midpoint slices of dt = duration / steps with EXACT
+ * per-slice SU(2) rotations (midpoint_reference): no series, no amplitude
+ * table.  u_out: 2 x 2 complex128 (host).  Identity for steps < 1 or no
+ * field (studies.py:131-139).  ctx: any created context (device, stream). */
+int sp_qubit_midpoint_reference(sp_ctx* ctx, double w0, double w1, double wrf,
+                                double duration, int64_t steps, double* u_out);
+
 /* ---- evaluation scheme of the slice series ------------------------------
  * 0 auto (Paterson-Stockmeyer in the Chebyshev basis whenever it needs fewer
  * GEMMs per slice than the reference's Clenshaw recurrence), 1 Clenshaw

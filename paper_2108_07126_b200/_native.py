@@ -75,6 +75,11 @@ HEADER_SYMBOLS = {
                                         _c.POINTER(SpPlan), _P, _c.c_int64, _P, _P]),
     "sp_gemm_batched_device": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int64, _P, _c.c_int64, _P,
                                           _c.c_int64, _P, _P, _P, _P, _c.c_int64, _P]),
+    "sp_apply_batch_scratch_bytes": (_c.c_size_t, [_c.c_int, _c.c_int, _c.c_int64, _c.c_int]),
+    "sp_apply_batch_device": (_c.c_int, [_c.c_int, _c.c_int, _P, _c.c_int64, _c.c_int, _P, _P,
+                                         _P, _P]),
+    "sp_qubit_midpoint_reference": (_c.c_int, [_P, _c.c_double, _c.c_double, _c.c_double,
+                                               _c.c_double, _c.c_int64, _P]),
     "sp_last_lanes": (_c.c_int, [_P, _c.POINTER(_c.c_int)]),
     "sp_set_profiling": (_c.c_int, [_P, _c.c_int]),
     "sp_last_timing": (_c.c_int, [_P, _c.POINTER(_c.c_double), _c.POINTER(_c.c_int),

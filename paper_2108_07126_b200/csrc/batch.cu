@@ -213,4 +213,53 @@ int sp_gemm_batched_device(int precision_bits, int dim, int64_t count, const voi
   return gemm_launch<float>(gp, d_a, d_b, d_c, d_c, st);
 }
 
+size_t sp_apply_batch_scratch_bytes(int precision_bits, int dim, int64_t count, int kind) {
+  if (kind != 1 || dim < 1 || count < 0) return 0;
+  const size_t el = precision_bits == 32 ? 8 : 16;
+  return ((size_t)count + 1) * dim * dim * el;
+}
+
+int sp_apply_batch_device(int precision_bits, int dim, const void* d_u, int64_t count, int kind,
+                          const void* d_states, void* d_out, void* d_scratch, void* stream) {
+  int rc = check_bits(precision_bits);
+  if (rc) return rc;
+  if (dim < 1 || count < 0) return set_error(SP_E_SHAPE, "apply needs dim >= 1, count >= 0");
+  if (kind != 0 && kind != 1)
+    return set_error(SP_E_SHAPE, "state kind must be 0 (vectors) or 1 (density matrices)");
+  if (count == 0) return SP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kind == 0) {
+    const int blocks = grid_stride_blocks(count * dim);
+    if (precision_bits == 64)
+      apply_vec_kernel<double><<<blocks, 256, 0, st>>>(dim, count, (const cplx<double>*)d_u,
+                                                       (const cplx<double>*)d_states,
+                                                       (cplx<double>*)d_out);
+    else
+      apply_vec_kernel<float><<<blocks, 256, 0, st>>>(dim, count, (const cplx<float>*)d_u,
+                                                      (const cplx<float>*)d_states,
+                                                      (cplx<float>*)d_out);
+    BATCH_TRY(cudaGetLastError());
+    return SP_OK;
+  }
+  if (!d_scratch) return set_error(SP_E_CONFIG, "density-matrix apply needs scratch");
+  // rho' = (U rho) U^+: two batched GEMMs (U and U^+ broadcast, stride 0)
+  const size_t el = precision_bits == 32 ? 8 : 16;
+  const size_t dd = (size_t)dim * dim;
+  char* tmp = (char*)d_scratch;
+  char* uadj = tmp + (size_t)count * dd * el;
+  const int ablocks = grid_stride_blocks((int64_t)dd);
+  if (precision_bits == 64)
+    adjoint_kernel<double><<<ablocks, 256, 0, st>>>(dim, (const cplx<double>*)d_u,
+                                                    (cplx<double>*)uadj);
+  else
+    adjoint_kernel<float><<<ablocks, 256, 0, st>>>(dim, (const cplx<float>*)d_u,
+                                                   (cplx<float>*)uadj);
+  BATCH_TRY(cudaGetLastError());
+  rc = sp_gemm_batched_device(precision_bits, dim, count, d_u, 0, d_states, (int64_t)dd,
+                              nullptr, nullptr, nullptr, tmp, (int64_t)dd, stream);
+  if (rc) return rc;
+  return sp_gemm_batched_device(precision_bits, dim, count, tmp, (int64_t)dd, uadj, 0, nullptr,
+                                nullptr, nullptr, d_out, (int64_t)dd, stream);
+}
+
 }  // extern "C"

@@ -2057,6 +2057,50 @@ int sp_product_device(sp_ctx* ctx, int count, const void* d_mats, int reduction,
   return product_dev(ctx, count, (const double2*)d_mats, reduction, d_out, st);
 }
 
+int sp_qubit_midpoint_reference(sp_ctx* ctx, double w0, double w1, double wrf,
+                                double duration, int64_t steps, double* u_out) {
+  if (ctx && !ctx->kids.empty())
+    return sp_qubit_midpoint_reference(ctx->kids[0], w0, w1, wrf, duration, steps, u_out);
+  if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
+  if (!u_out) return fail(ctx, SP_E_SHAPE, "null output");
+  // studies.py:131-139: identity for no steps or no field
+  const double vnorm = std::hypot(w1, w0);
+  if (steps < 1 || vnorm == 0.0) {
+    const double id[8] = {1, 0, 0, 0, 0, 0, 1, 0};
+    std::memcpy(u_out, id, sizeof(id));
+    return SP_OK;
+  }
+  int rc = device_init(ctx);
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const double dt = duration / (double)steps;
+  Su2Job sj;
+  std::memset(&sj, 0, sizeof(sj));
+  const int block = 512;
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(ctx->sms, (steps + (int64_t)block * 8 - 1) / ((int64_t)block * 8)));
+  rc = ensure(ctx, ctx->lanes, (size_t)grid * 4 * sizeof(double));
+  if (rc) return rc;
+  rc = ensure(ctx, ctx->result, 4 * sizeof(double2));
+  if (rc) return rc;
+  if (!ctx->tailctr.p) {
+    rc = ensure(ctx, ctx->tailctr, sizeof(unsigned));
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->tailctr.p, 0, sizeof(unsigned), st));
+  }
+  sj.cta_out = ctx->lanes.p;
+  sj.ctr = (unsigned*)ctx->tailctr.p;
+  sj.out = ctx->result.p;
+  CUDA_TRY(ctx, su2_qubit_reference(sj, steps, std::cos(vnorm * dt / 2.0),
+                                    std::sin(vnorm * dt / 2.0), w1 / vnorm, w0 / vnorm, wrf,
+                                    dt, grid, block, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(u_out, ctx->result.p, 4 * sizeof(double2),
+                                cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
 int sp_amplitude_violation(sp_ctx* ctx, int64_t* index) {
   if (ctx && !ctx->kids.empty()) {
     if (ctx->last_multi) {

@@ -80,5 +80,9 @@ struct Su2Job {
 cudaError_t su2_run(const Su2Job& job, int grid, int block, cudaStream_t st);
 // registers / max threads of the instance a job would launch (host tuning)
 int su2_max_block(const Su2Job& job);
+// the driven qubit's analytic midpoint reference (qubit_reference_kernel)
+cudaError_t su2_qubit_reference(const Su2Job& job, int64_t steps, double c, double s, double ax,
+                                double az, double wrf, double dt, int grid, int block,
+                                cudaStream_t st);
 
 }  // namespace sp

@@ -372,5 +372,41 @@ __global__ void phase_copy_kernel(const cplx<R>* __restrict__ in, int d, int64_t
   }
 }
 
+// ---- state propagation (apply, propagator.py:105-118) ----------------------
+// out[k] = U psi_k: one thread per output entry, psi_k = row k of the
+// (count, d) state batch
+template <class R>
+__global__ void __launch_bounds__(256) apply_vec_kernel(int d, int64_t count,
+                                                        const cplx<R>* __restrict__ U,
+                                                        const cplx<R>* __restrict__ psi,
+                                                        cplx<R>* __restrict__ out) {
+  const int64_t total = count * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / d;
+    const int i = (int)(e % d);
+    const cplx<R>* u = U + (size_t)i * d;
+    const cplx<R>* v = psi + (size_t)k * d;
+    R re = 0, im = 0;
+    for (int j = 0; j < d; ++j) {
+      re = fma(u[j].x, v[j].x, re);
+      re = fma(-u[j].y, v[j].y, re);
+      im = fma(u[j].x, v[j].y, im);
+      im = fma(u[j].y, v[j].x, im);
+    }
+    out[e] = cmk<R>(re, im);
+  }
+}
+
+// out = U^+ (conjugate transpose)
+template <class R>
+__global__ void adjoint_kernel(int d, const cplx<R>* __restrict__ U, cplx<R>* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d * d; e += gridDim.x * blockDim.x) {
+    const int i = e / d, j = e % d;
+    const cplx<R> v = U[(size_t)j * d + i];
+    out[e] = cmk<R>(v.x, -v.y);
+  }
+}
+
 }  // namespace batch
 }  // namespace sp

@@ -513,3 +513,39 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
 }
 
 }  // namespace sp
+
+namespace sp {
+
+// ---------------------------------------------------------------------------
+// Analytic oracle on the device (studies.py:123-153, midpoint_reference): the
+// driven qubit's midpoint-sliced propagator from EXACT per-slice SU(2)
+// rotations exp(-i (vnorm dt / 2) n_k . sigma), n_k = (ax cos phi_k,
+// ax sin phi_k, az), phi_k = wrf (k + 1/2) dt — no series, no amplitude
+// table; the same lanes and ordered tail as the su(2) propagation.
+// ---------------------------------------------------------------------------
+struct QubitRef {
+  int64_t steps;
+  double c, s;      // cos / sin of vnorm dt / 2
+  double ax, az;    // unit field axis in the rotating frame
+  double wrf, dt;
+};
+
+__global__ void __launch_bounds__(512, 1) qubit_reference_kernel(const Su2Job job,
+                                                                 const QubitRef q) {
+  const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lanes = gridDim.x * blockDim.x;
+  const int64_t s0 = (int64_t)lane * q.steps / lanes;
+  const int64_t s1 = ((int64_t)lane + 1) * q.steps / lanes;
+  Quat V = quat_identity();
+  for (int64_t k = s0; k < s1; ++k) {
+    const double t = ((double)k + 0.5) * q.dt;
+    double sn, cs;
+    sincos(q.wrf * t, &sn, &cs);
+    const double nx = q.ax * cs, ny = q.ax * sn;
+    // [[c - i s az, -i s (nx - i ny)], [-i s (nx + i ny), c + i s az]]
+    V = quat_mul(Quat{q.c, -q.s * q.az, -q.s * ny, -q.s * nx}, V);
+  }
+  su2_finish<1>(job, V, false, 0, 0);
+}
+
+}  // namespace sp

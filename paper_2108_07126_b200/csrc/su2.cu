@@ -149,4 +149,12 @@ cudaError_t su2_run(const Su2Job& job, int grid, int block, cudaStream_t st) {
 
 int su2_max_block(const Su2Job& job) { return su2_kernel_for(job).max_block; }
 
+cudaError_t su2_qubit_reference(const Su2Job& job, int64_t steps, double c, double s, double ax,
+                                double az, double wrf, double dt, int grid, int block,
+                                cudaStream_t st) {
+  const QubitRef q{steps, c, s, ax, az, wrf, dt};
+  qubit_reference_kernel<<<grid, block, 0, st>>>(job, q);
+  return cudaGetLastError();
+}
+
 }  // namespace sp

@@ -40,6 +40,7 @@ __all__ = [
     "CumulativeResult",
     "create",
     "apply",
+    "apply_batch",
 ]
 
 _CREATED, _LOADED, _CLOSED = "created", "loaded", "closed"
@@ -84,19 +85,57 @@ class CumulativeResult:
 
 def apply(u, state) -> np.ndarray:
     """Propagate a state vector (U psi) or a density matrix (U rho U^+)
-    (``propagator.py:105-118``)."""
+    (``propagator.py:105-118``) on the device (``sp_apply_batch_device``);
+    same shapes, dtype and errors as the reference."""
     m = u.u if isinstance(u, PropagatorResult) else np.asarray(u)
     if m.ndim != 2 or m.shape[0] != m.shape[1]:
         raise ShapeError(f"propagator must be a square matrix, got shape {m.shape}")
     d = m.shape[0]
     state = np.asarray(state)
     if state.shape == (d,):
-        return m @ state
+        return apply_batch(m, state[None, :])[0]
     if state.shape == (d, d):
-        return m @ state @ m.conj().T
+        return apply_batch(m, state[None, :, :])[0]
     raise ShapeError(
         f"state shape {state.shape} matches neither a vector ({d},) "
         f"nor a density matrix ({d}, {d})")
+
+
+def apply_batch(u, states) -> np.ndarray:
+    """``apply`` over a batch: (count, d) state vectors -> U psi_k, or
+    (count, d, d) density matrices -> U rho_k U^+, one device call (complex128,
+    or complex64 when both U and the states are complex64)."""
+    import torch
+
+    m = u.u if isinstance(u, PropagatorResult) else np.asarray(u)
+    if m.ndim != 2 or m.shape[0] != m.shape[1]:
+        raise ShapeError(f"propagator must be a square matrix, got shape {m.shape}")
+    d = m.shape[0]
+    states = np.asarray(states)
+    if states.ndim == 2 and states.shape[1] == d:
+        kind = 0
+    elif states.ndim == 3 and states.shape[1:] == (d, d):
+        kind = 1
+    else:
+        raise ShapeError(f"states of shape {states.shape} are neither (count, {d}) vectors nor "
+                         f"(count, {d}, {d}) density matrices")
+    c64 = m.dtype == np.complex64 and states.dtype == np.complex64
+    dtype, tdt, bits = ((np.complex64, torch.complex64, 32) if c64
+                        else (np.complex128, torch.complex128, 64))
+    count = states.shape[0]
+    if count == 0:
+        return np.zeros(states.shape, dtype=dtype)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    du = torch.from_numpy(np.ascontiguousarray(m, dtype=dtype)).to(dev)
+    ds = torch.from_numpy(np.ascontiguousarray(states, dtype=dtype)).to(dev)
+    out = torch.empty_like(ds)
+    nbytes = lib.sp_apply_batch_scratch_bytes(bits, d, count, kind)
+    scratch = torch.empty(max(1, nbytes), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    check(lib.sp_apply_batch_device(bits, d, du.data_ptr(), count, kind, ds.data_ptr(),
+                                    out.data_ptr(), scratch.data_ptr(), stream.cuda_stream))
+    stream.synchronize()
+    return out.cpu().numpy()
 
 
 def reduce_pairwise(batch, backend=None, scratch=None) -> np.ndarray:
