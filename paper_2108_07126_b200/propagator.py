@@ -181,6 +181,9 @@ class IntegratorContext:
         self.precision = precision
         self.m_max = m_max
         self.checked = checked
+        # scaling and squaring past the capability (scaling.py); off = the
+        # reference's StepTooLargeError
+        self.scaling = False
         self.devices = list(devices) if devices else [int(device)]
         self.device = self.devices[0]
         # one batch backend per context (reference: one CpuBackend per
@@ -392,7 +395,14 @@ class IntegratorContext:
         if amps.pts == 0:
             return PropagatorResult(u=np.eye(d, dtype=self._out_dtype()), slice_count=0,
                                     plan=None)
-        count, plan = self._prepare(amps)
+        try:
+            count, plan = self._prepare(amps)
+        except StepTooLargeError:
+            if not self.scaling:
+                raise
+            # past the series capability: scaling and squaring (scaling.py)
+            from .scaling import equiprop_scaled
+            return equiprop_scaled(self, amps, reduction)
         out = np.empty((d, d), dtype=self._out_dtype())
         native = self._native_plan(plan)
         rc = lib.sp_equiprop(self._handle, amps.values.ctypes.data_as(ctypes.c_void_p),
@@ -469,6 +479,14 @@ class IntegratorContext:
                                     REDUCTION[reduction], ctypes.c_void_p(out_ptr),
                                     ctypes.c_void_p(stream)), self._handle)
 
+    def set_scaling(self, enabled: bool = True) -> None:
+        """Propagate steps past the series capability by scaling and
+        squaring (``scaling.py``) instead of raising ``StepTooLargeError``
+        (the reference behaviour, kept by default).  ``equiprop`` only; steps
+        within the capability are unaffected."""
+        self._require_open()
+        self.scaling = bool(enabled)
+
     _ALGOS = {"auto": 0, "clenshaw": 1, "ps": 2, "ps3m": 3}
 
     def set_algorithm(self, algo: str = "auto") -> None:
@@ -525,7 +543,7 @@ def _default_device() -> int:
 
 def create(precision="fp64", m_max: int | None = None, checked: bool = False,
            backend=None, device: int | None = None,
-           devices=None) -> IntegratorContext:
+           devices=None, scaling: bool = False) -> IntegratorContext:
     """New propagation context (``propagator.py:334-355``) on one B200, or
     on several in this one process: ``devices=[0, 1, ...]`` (or an int
     count) time-shards every ``equiprop`` over those GPUs — contiguous slice
@@ -555,4 +573,6 @@ def create(precision="fp64", m_max: int | None = None, checked: bool = False,
     elif backend is not None:
         if not isinstance(backend, str) or backend.lower() not in _BACKEND_TOKENS:
             raise ConfigError(f"unknown backend {backend!r}; expected one of {_BACKEND_TOKENS}")
-    return IntegratorContext(precision, m_max, bool(checked), dev, instance, devices)
+    ctx = IntegratorContext(precision, m_max, bool(checked), dev, instance, devices)
+    ctx.scaling = bool(scaling)
+    return ctx
