@@ -47,7 +47,14 @@ enum {
 };
 
 /* slicing modes: propagator.py:175-201, hamiltonian.py:8-14, magnus.py:1-16 */
-enum { SP_MODE_MIDPOINT = 0, SP_MODE_SIMPSON = 1, SP_MODE_MAGNUS = 2 };
+enum { SP_MODE_MIDPOINT = 0, SP_MODE_SIMPSON = 1, SP_MODE_MAGNUS = 2,
+       /* extensions (north star; not in the reference): two samples per slice
+        * of length 2 dt at the Gauss-Legendre nodes (k + 1/2 -+ sqrt(3)/6) 2 dt;
+        * GAUSS2: terms [H0, H1..HN], weights (a + b)/2 (2nd order);
+        * GAUSS4: the magnus effective terms, weights (a + b)/2,
+        * (sqrt(3) dt / 6)(b - a), (sqrt(3) dt / 6)(a_k b_k' - a_k' b_k)
+        * (4th-order Gauss-Legendre Magnus) */
+       SP_MODE_GAUSS2 = 3, SP_MODE_GAUSS4 = 4 };
 
 /* reductions: propagator.py:279-308 ("pairwise" | "sequential") */
 enum { SP_REDUCE_PAIRWISE = 0, SP_REDUCE_SEQUENTIAL = 1 };

@@ -36,6 +36,7 @@ __all__ = [
     "commutator",
     "effective_terms",
     "slice_table",
+    "gauss_table",
     "spectral_bound",
     "expand",
     "expm_clenshaw",
@@ -212,6 +213,8 @@ def slice_table(values: np.ndarray, dt: float, mode: str):
     pts = v.shape[0]
     if mode == "midpoint":
         return np.column_stack([np.ones(pts), v]), dt, pts
+    if mode in ("gauss2", "gauss4"):
+        return gauss_table(v, dt, mode == "gauss4")
     c1, c2, c3 = v[0:pts - 1:2], v[1:pts:2], v[2:pts:2]
     if mode == "simpson":
         table = np.column_stack([np.ones(c1.shape[0]), (c1 + 4.0 * c2 + c3) / 6.0])
@@ -231,9 +234,36 @@ def slice_table(values: np.ndarray, dt: float, mode: str):
     return table, scale, c1.shape[0]
 
 
+def gauss_table(v: np.ndarray, dt: float, magnus: bool):
+    """Gauss-Legendre modes (north-star extension; no reference to pin —
+    "parity unpinned" for these rows, checked by convergence order instead):
+    slice k = rows a = 2k, b = 2k + 1 sampled at the Gauss nodes of a slice
+    of length h = 2 dt.  Omega = -i G with G = (h/2)(H(a) + H(b)) +
+    (sqrt(3) h^2 / 12) i[H(a), H(b)] (4th-order Magnus, Blanes-Casas-Ros
+    2000); expanded over [H0, Hk, i[H0,Hk], i[Hk,Hk']] at scale h the
+    weights are (a + b)/2, (sqrt(3) dt / 6)(b - a) and
+    (sqrt(3) dt / 6)(a_k b_k' - a_k' b_k).  gauss2 keeps the first column
+    only (2nd order)."""
+    a, b = v[0::2], v[1::2]
+    count = a.shape[0]
+    cols = [np.ones(count), 0.5 * (a + b)]
+    if magnus:
+        g = math.sqrt(3.0) * dt / 6.0
+        n = v.shape[1]
+        pairs = [(k, kp) for k in range(n) for kp in range(k + 1, n)]
+        cross = np.empty((count, len(pairs)))
+        for col, (k, kp) in enumerate(pairs):
+            cross[:, col] = g * (a[:, k] * b[:, kp] - a[:, kp] * b[:, k])
+        cols += [g * (b - a), cross]
+    return np.column_stack(cols), 2.0 * dt, count
+
+
 def spectral_bound(dt: float, mode: str, base_norms, dcomm_norms=(), ccomm_norms=()) -> float:
     """beta (``hamiltonian.py:156-162``, ``magnus.py:109-118``,
     step selection ``propagator.py:258-262``)."""
+    if mode == "gauss4":  # |weights| <= 1, sqrt(3) dt / 3 at scale 2 dt
+        return (2.0 * dt * sum(base_norms)
+                + (2.0 * math.sqrt(3.0) * dt * dt / 3.0) * (sum(dcomm_norms) + sum(ccomm_norms)))
     if mode == "magnus":
         return (2.0 * dt * sum(base_norms)
                 + (2.0 * dt * dt / 3.0) * sum(dcomm_norms)
@@ -359,8 +389,9 @@ def cumulative(u: np.ndarray) -> np.ndarray:
 
 def slice_propagators(h0, hs, values, dt, *, mode="midpoint", bits=64, m_max=None):
     """(U batch, plan) — expand, bound, plan, chunked Clenshaw
-    (``propagator.py:238-277``).  mode in {midpoint, simpson, magnus}."""
-    magnus = mode == "magnus"
+    (``propagator.py:238-277``).  mode in {midpoint, simpson, magnus} (+ the
+    gauss2 / gauss4 extensions)."""
+    magnus = mode in ("magnus", "gauss4")
     terms, bn, dn, cn = effective_terms(h0, hs, magnus)
     table, scale, count = slice_table(values, dt, mode)
     g = expand(terms, table, scale, bits)

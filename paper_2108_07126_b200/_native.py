@@ -19,7 +19,7 @@ __all__ = ["lib", "SpPlan", "LIB_PATH", "HEADER_SYMBOLS", "check", "MODE", "REDU
 LIB_PATH = os.environ.get("SLICEPROP_B200_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libsliceprop_b200.so")
 
-MODE = {"midpoint": 0, "simpson": 1, "magnus": 2}
+MODE = {"midpoint": 0, "simpson": 1, "magnus": 2, "gauss2": 3, "gauss4": 4}
 REDUCTION = {"pairwise": 0, "sequential": 1}
 MAX_ORDER = 25
 

@@ -440,11 +440,24 @@ int upload_terms(sp_ctx* ctx) {
 int64_t slice_count_for(int mode, int64_t pts, int* code) {
   *code = SP_OK;
   if (mode == SP_MODE_MIDPOINT) return pts;
+  if (mode >= SP_MODE_GAUSS2) {  // two Gauss-Legendre nodes per slice
+    if (pts < 2 || pts % 2 != 0) {
+      *code = SP_E_SAMPLING_PARITY;
+      return -1;
+    }
+    return pts / 2;
+  }
   if (pts < 3 || pts % 2 == 0) {
     *code = SP_E_SAMPLING_PARITY;
     return -1;
   }
   return (pts - 1) / 2;
+}
+
+const char* parity_message(int mode) {
+  return mode >= SP_MODE_GAUSS2
+             ? "Gauss-Legendre quadrature needs an even number of samples >= 2"
+             : "three-point quadrature needs an odd number of samples >= 3";
 }
 
 int grid_for(int64_t total, int threads) {
@@ -915,6 +928,7 @@ bool su2_applies(const sp_ctx* ctx, const SliceJob& job) {
     return (e && e[0] == '0') ? 0 : 1;
   }();
   if (!enabled || !ctx->su2_terms || ctx->bits != 64 || !job.coef_alt) return false;
+  if (job.mode > SP_MODE_MAGNUS) return false;  // Gauss-Legendre: general d = 2 kernel
   if (!(job.phase[0] == 1.0 && job.phase[1] == 0.0)) return false;
   if (job.n_ctrl % 2 == 0 && ((uintptr_t)job.amps & 15u)) return false;  // vector row loads
   return true;
@@ -1231,8 +1245,7 @@ int build_job(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double
   int code;
   const int64_t n = slice_count_for(ctx->mode, pts, &code);
   if (code)
-    return fail(ctx, code, "three-point quadrature needs an odd number of samples >= 3, got %lld",
-                (long long)pts);
+    return fail(ctx, code, "%s, got %lld", parity_message(ctx->mode), (long long)pts);
   std::memset(job, 0, sizeof(*job));
   job->amps = d_amps;
   job->pts = pts;
@@ -1245,6 +1258,7 @@ int build_job(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, double
   job->xs = (span == 0.0) ? 0.0 : 2.0 * scale * (2.0 / span);
   job->scale = scale;
   job->xspan = (span == 0.0) ? 0.0 : 2.0 / span;
+  job->gl = std::sqrt(3.0) * dt / 6.0;
   job->m = plan->m_max;
   std::memcpy(job->coef, plan->coeffs, sizeof(job->coef));
   job->phase[0] = plan->phase[0];
@@ -1652,8 +1666,7 @@ int equiprop_multi(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, dou
   int code;
   const int64_t n = slice_count_for(ctx->mode, pts, &code);
   if (code)
-    return fail(ctx, code, "three-point quadrature needs an odd number of samples >= 3, got %lld",
-                (long long)pts);
+    return fail(ctx, code, "%s, got %lld", parity_message(ctx->mode), (long long)pts);
   const int P = (int)ctx->kids.size();
   const int d = ctx->dim;
   const size_t dd = (size_t)d * d;
@@ -1671,7 +1684,9 @@ int equiprop_multi(sp_ctx* ctx, const double* amps, int64_t pts, int n_ctrl, dou
                                                                   cudaEventDisableTiming));
     const int64_t a = (int64_t)r * n / P, b = (int64_t)(r + 1) * n / P;
     const int64_t lo = ctx->mode == SP_MODE_MIDPOINT ? a : 2 * a;
-    const int64_t hi = ctx->mode == SP_MODE_MIDPOINT ? b : 2 * b + 1;
+    const int64_t hi = ctx->mode == SP_MODE_MIDPOINT ? b
+                       : ctx->mode >= SP_MODE_GAUSS2 ? 2 * b  // no shared node
+                                                     : 2 * b + 1;
     first_row[r] = lo;
     rc = ensure(kid, kid->out, blk);
     if (rc) return fail(ctx, rc, "device %d: %s", kid->device, kid->err);
@@ -1876,9 +1891,10 @@ int sp_set_hamiltonian(sp_ctx* ctx, int dim, int n_ctrl, int n_terms, int mode,
                        const double* terms) {
   if (!ctx) return fail(nullptr, SP_E_STATE_MACHINE, "null context");
   if (dim < 1) return fail(ctx, SP_E_SHAPE, "dim must be >= 1, got %d", dim);
-  if (mode < SP_MODE_MIDPOINT || mode > SP_MODE_MAGNUS)
+  if (mode < SP_MODE_MIDPOINT || mode > SP_MODE_GAUSS4)
     return fail(ctx, SP_E_CONFIG, "unknown mode %d", mode);
-  const int expect = (mode == SP_MODE_MAGNUS) ? 1 + 2 * n_ctrl + n_ctrl * (n_ctrl - 1) / 2
+  const int expect = (mode == SP_MODE_MAGNUS || mode == SP_MODE_GAUSS4)
+                         ? 1 + 2 * n_ctrl + n_ctrl * (n_ctrl - 1) / 2
                                               : 1 + n_ctrl;
   if (n_ctrl < 0 || n_terms != expect)
     return fail(ctx, SP_E_SHAPE, "%d expansion terms do not match %d controls in mode %d",
@@ -1927,7 +1943,7 @@ int sp_slice_count(const sp_ctx* ctx, int64_t pts, int64_t* out) {
   if (!ctx || !ctx->loaded) return fail(nullptr, SP_E_STATE_MACHINE, "no Hamiltonian loaded");
   int code;
   *out = slice_count_for(ctx->mode, pts, &code);
-  if (code) return fail(nullptr, code, "three-point quadrature needs an odd number of samples >= 3");
+  if (code) return fail(nullptr, code, "%s", parity_message(ctx->mode));
   return SP_OK;
 }
 

@@ -30,6 +30,7 @@ struct SliceJob {
   double xs;              // 2 * scale / beta  (0 when beta == 0): "2X" factor
   double scale;           // dt (midpoint) or 2 dt (three-point): the exponent scale
   double xspan;           // 2 / span (0 when span == 0): X = xspan * G
+  double gl;              // sqrt(3) dt / 6: Gauss-Legendre commutator weight factor
   int m;                  // series order
   double coef[2 * (SP_MAX_ORDER + 1)];
   double phase[2];

@@ -206,6 +206,34 @@ __device__ __forceinline__ void rotate_violation_slots(const SliceJob& j) {
 
 // Every amplitude of the table is read by exactly one weight t in 1..N of
 // some slice, so validating there covers the whole table in passing.
+// pair (k, k') < N of cross-commutator column e (magnus.py:55-59 order)
+__device__ __forceinline__ void cross_pair(int e, int N, int& k, int& kp) {
+  k = 0;
+  while (e >= N - 1 - k) {
+    e -= N - 1 - k;
+    ++k;
+  }
+  kp = k + 1 + e;
+}
+
+// Gauss-Legendre modes (extension): rows 2s (node a) and 2s + 1 (node b)
+__device__ __forceinline__ double gauss_weight(const SliceJob& j, int64_t s, int t) {
+  const int N = j.n_ctrl;
+  const double* ra = j.amps + (2 * s) * N;
+  const double* rb = ra + N;
+  int e = t - 1;
+  if (e < N) {
+    check_amp(j, 2 * s, e, ra[e]);
+    check_amp(j, 2 * s + 1, e, rb[e]);
+    return 0.5 * (ra[e] + rb[e]);
+  }
+  e -= N;
+  if (e < N) return j.gl * (rb[e] - ra[e]);
+  int k, kp;
+  cross_pair(e - N, N, k, kp);
+  return j.gl * (ra[k] * rb[kp] - ra[kp] * rb[k]);
+}
+
 __device__ __forceinline__ double slice_weight(const SliceJob& j, int64_t s, int t) {
   const int N = j.n_ctrl;
   if (j.mode == SP_MODE_MIDPOINT) {
@@ -213,6 +241,7 @@ __device__ __forceinline__ double slice_weight(const SliceJob& j, int64_t s, int
     check_amp(j, s, t - 1, v);
     return v;
   }
+  if (j.mode >= SP_MODE_GAUSS2) return gauss_weight(j, s, t);
   const double* r1 = j.amps + (2 * s) * N;
   const double* r2 = r1 + N;
   const double* r3 = r2 + N;
@@ -247,6 +276,24 @@ __device__ __forceinline__ WRaw weight_gather(const SliceJob& j, int64_t s, int 
   const int N = j.n_ctrl;
   if (j.mode == SP_MODE_MIDPOINT) {
     w.v[0] = j.amps[s * N + (t - 1)];
+    return w;
+  }
+  if (j.mode >= SP_MODE_GAUSS2) {
+    const double* ra = j.amps + (2 * s) * N;
+    const double* rb = ra + N;
+    int e = t - 1;
+    if (e >= N) e -= N;
+    if (e < N) {
+      w.v[0] = ra[e];
+      w.v[1] = rb[e];
+      return w;
+    }
+    int k, kp;
+    cross_pair(e - N, N, k, kp);
+    w.v[0] = ra[k];
+    w.v[1] = rb[kp];
+    w.v[2] = ra[kp];
+    w.v[3] = rb[k];
     return w;
   }
   const double* r1 = j.amps + (2 * s) * N;
@@ -284,6 +331,16 @@ __device__ __forceinline__ double weight_combine(const SliceJob& j, int64_t s, i
   if (j.mode == SP_MODE_MIDPOINT) {
     check_amp(j, s, t - 1, w.v[0]);
     return w.v[0];
+  }
+  if (j.mode >= SP_MODE_GAUSS2) {
+    const int e = t - 1;
+    if (e < N) {
+      check_amp(j, 2 * s, e, w.v[0]);
+      check_amp(j, 2 * s + 1, e, w.v[1]);
+      return 0.5 * (w.v[0] + w.v[1]);
+    }
+    if (e < 2 * N) return j.gl * (w.v[1] - w.v[0]);
+    return j.gl * (w.v[0] * w.v[1] - w.v[2] * w.v[3]);
   }
   int e = t - 1;
   if (e < N) {

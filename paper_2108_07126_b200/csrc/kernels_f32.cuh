@@ -40,6 +40,23 @@ __device__ __forceinline__ double f32_weight(const SliceJob& j, int64_t s, int t
     if (val) check_amp(j, s, t - 1, v);
     return v;
   }
+  if (j.mode >= SP_MODE_GAUSS2) {  // Gauss-Legendre modes: rows 2s, 2s + 1
+    const double* ra = j.amps + (2 * s) * N;
+    const double* rb = ra + N;
+    int e = t - 1;
+    if (e < N) {
+      if (val) {
+        check_amp(j, 2 * s, e, ra[e]);
+        check_amp(j, 2 * s + 1, e, rb[e]);
+      }
+      return 0.5 * (ra[e] + rb[e]);
+    }
+    e -= N;
+    if (e < N) return j.gl * (rb[e] - ra[e]);
+    int k, kp;
+    cross_pair(e - N, N, k, kp);
+    return j.gl * (ra[k] * rb[kp] - ra[kp] * rb[k]);
+  }
   const double* r1 = j.amps + (2 * s) * N;
   const double* r2 = r1 + N;
   const double* r3 = r2 + N;

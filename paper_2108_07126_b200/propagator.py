@@ -214,6 +214,8 @@ class IntegratorContext:
 
     @property
     def mode(self) -> str:
+        if self._quadrature is Quadrature.GAUSS:  # extension modes
+            return "gauss4" if self._magnus else "gauss2"
         if self._magnus:
             return "magnus"
         return self._quadrature.value
@@ -244,7 +246,10 @@ class IntegratorContext:
         effective = build_effective_system(system) if magnus else None
         terms = effective.terms() if magnus else system.terms()
         stacked = np.ascontiguousarray(np.stack(terms), dtype=np.complex128)
-        mode = "magnus" if magnus else quadrature.value
+        if quadrature is Quadrature.GAUSS:
+            mode = "gauss4" if magnus else "gauss2"  # extension modes
+        else:
+            mode = "magnus" if magnus else quadrature.value
         check(lib.sp_set_hamiltonian(self._handle, system.dim, system.n_controls,
                                      len(terms), MODE[mode],
                                      stacked.ctypes.data_as(ctypes.c_void_p)), self._handle)
@@ -278,6 +283,11 @@ class IntegratorContext:
 
     # -- host-side preparation (validation order of propagator.py:238-263) --
     def slice_count(self, pts: int) -> int:
+        if self._quadrature is Quadrature.GAUSS:
+            if pts < 2 or pts % 2:
+                raise SamplingParityError(
+                    f"Gauss-Legendre quadrature needs an even number of samples >= 2, got {pts}")
+            return pts // 2
         if self._quadrature is Quadrature.SIMPSON:
             if pts < 3 or pts % 2 == 0:
                 raise SamplingParityError(
@@ -288,6 +298,9 @@ class IntegratorContext:
     def bound(self, dt: float) -> float:
         """Global spectral bound beta for sample step dt (alpha = -beta)."""
         if self._magnus:
+            if self._quadrature is Quadrature.GAUSS:
+                from .magnus import gauss_magnus_bound
+                return gauss_magnus_bound(self._effective, dt)
             return magnus_bound(self._effective, dt)
         step = dt if self._quadrature is Quadrature.MIDPOINT else 2.0 * dt
         return spectral_bound(self._system, step)
@@ -352,7 +365,11 @@ class IntegratorContext:
         terms = [np.asarray(t).astype(cdt) for t in
                  (self._effective.terms() if self._magnus else self._system.terms())]
         v = amps.values
-        if self._magnus:
+        if self._quadrature is Quadrature.GAUSS:
+            from .magnus import gauss_table
+            full, scale = gauss_table(amps, self._magnus)
+            table = full[:, 1:]
+        elif self._magnus:
             from .magnus import magnus_coefficients
             scale = 2.0 * amps.dt
             table = magnus_coefficients(amps) / scale

@@ -47,6 +47,9 @@ def slice_table(ctx, amps) -> tuple[np.ndarray, float]:
     exponent scale of the loaded mode: midpoint [1, c_k] at dt
     (``hamiltonian.py:199-201``); Simpson [1, (c1 + 4 c2 + c3)/6] at 2 dt
     (``:202-205``); Magnus [1, table / (2 dt)] at 2 dt (``magnus.py:121-141``)."""
+    if ctx._quadrature is Quadrature.GAUSS:
+        from .magnus import gauss_table
+        return gauss_table(amps, ctx._magnus)
     if ctx._magnus:
         coeffs = magnus_coefficients(amps)
         scale = 2.0 * amps.dt

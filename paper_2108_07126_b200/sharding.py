@@ -41,6 +41,8 @@ def shard_rows(mode: str, a: int, b: int) -> tuple[int, int]:
         return 0, 0
     if mode == "midpoint":
         return a, b
+    if mode in ("gauss2", "gauss4"):  # two nodes per slice, no shared row
+        return 2 * a, 2 * b
     return 2 * a, 2 * b + 1
 
 
