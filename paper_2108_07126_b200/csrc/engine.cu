@@ -63,6 +63,9 @@ using P3_32 = PS3Cfg<32, 32, 1, 2, 4, 1, 1, true>;
 // D=64: 2 CTAs x 32 columns, 8 warps of 16 x 16 (measured: +2% over 4 warps
 // of 16 x 32; 4 CTAs x 16 columns -38%)
 using P3_64 = PS3Cfg<64, 32, 1, 2, 8, 1, 2, false>;
+// D=64 as ONE CTA per lane (all 64 columns, 8 warps of 16 x 32): CTA
+// barriers instead of group barriers, 4x the MMA work per step
+using P3_64s = PS3Cfg<64, 64, 1, 4, 8, 1, 1, false>;
 // D=128: 4 CTAs x 32 columns per lane, 8 warps, 1 CTA per SM.  (Measured:
 // 8 CTAs x 16 columns with 2 CTAs/SM is 1.4x slower — twice the L2 operand
 // traffic and an 8-way group barrier outweigh the barrier overlap.)
@@ -155,6 +158,8 @@ int family_for(int d, int* D) {
   return FAM_NONE;
 }
 
+bool d64_single();
+
 const char* family_kernel_name(int fam, int algo) {
   if (algo == 5) return "lane_su2_kernel";
   if (algo == 4)  // complex64 arithmetic (kernels_f32.cuh)
@@ -167,7 +172,8 @@ const char* family_kernel_name(int fam, int algo) {
     switch (fam) {
       case FAM_T16: return "lane_ps3_kernel<D16>";
       case FAM_T32: return "lane_ps3_kernel<D32>";
-      case FAM_T64: return "lane_ps3g_kernel<D64,group2>";
+      case FAM_T64:
+        return d64_single() ? "lane_ps3g_kernel<D64,group1>" : "lane_ps3g_kernel<D64,group2>";
       case FAM_T128: return "lane_ps3g_kernel<D128,group4>";
       case FAM_T256: return "lane_ps3g_kernel<D256,group16>";
       case FAM_T512: return "lane_ps3g_kernel<D512,group64>";
@@ -406,7 +412,10 @@ int upload_terms(sp_ctx* ctx) {
   switch (ctx->fam) {
     case FAM_T16: rc = ps3_prepare<P3_16>(ctx); break;
     case FAM_T32: rc = ps3_prepare<P3_32>(ctx); break;
-    case FAM_T64: rc = ps3_prepare<P3_64>(ctx); break;
+    case FAM_T64:
+      rc = ps3_prepare<P3_64>(ctx);
+      if (!rc) rc = ps3_prepare<P3_64s>(ctx);
+      break;
     case FAM_T128: rc = ps3_prepare<P3_128>(ctx); break;
     case FAM_T256: rc = ps3_prepare<P3_256>(ctx); break;
     case FAM_T512: rc = ps3_prepare<P3_512>(ctx); break;
@@ -511,7 +520,7 @@ int tc_launch(sp_ctx* ctx, const SliceJob& job, int lanes, double2* lane_out,
 // lane_ps_kernel (4 real products per complex product) or lane_ps3_kernel (3)
 template <class C, bool M3>
 constexpr auto ps_kernel() {
-  if constexpr (M3 && C::GPL > 1)
+  if constexpr (M3 && (C::GPL > 1 || !C::XS))
     return lane_ps3g_kernel<C>;  // group families: pipelined slice loop
   else if constexpr (M3)
     return lane_ps3_kernel<C>;
@@ -548,6 +557,14 @@ int ps_lanes(sp_ctx* ctx, int64_t n) {
 
 template <class C>
 int ps3_prepare(sp_ctx* ctx) { return ps_prepare<C, true>(ctx); }
+// D = 64 lane shape: one CTA (default) or a group of two (SP_D64_GROUP=2, A/B)
+bool d64_single() {
+  static const bool single = [] {
+    const char* e = getenv("SP_D64_GROUP");
+    return !(e && e[0] == '2');
+  }();
+  return single;
+}
 template <class C>
 int ps3_lanes(sp_ctx* ctx, int64_t n) { return ps_lanes<C, true>(ctx, n); }
 
@@ -563,22 +580,29 @@ int ps_launch(sp_ctx* ctx, const PSJob& pj, int lanes, double2* lane_out, double
   double2* tpriv = (double2*)ctx->tpriv.p;
   // the group PS3 kernel assembles from the 2-plane terms (and forms the sum
   // plane itself); the single-CTA PS3 kernel reads the 3-plane copy
-  const double* terms = (const double*)((M3 && C::GPL == 1) ? ctx->terms3.p : ctx->terms.p);
+  const double* terms =
+      (const double*)((M3 && C::GPL == 1 && C::XS) ? ctx->terms3.p : ctx->terms.p);
   double* ga = nullptr;
   unsigned* ctr = nullptr;
-  if (C::GPL > 1) {
+  if (C::GPL > 1 || (M3 && !C::XS)) {
     rc = ensure(ctx, ctx->psA, (size_t)groups * 3 * C::XDBL * sizeof(double));
     if (rc) return rc;
-    rc = ensure(ctx, ctx->gctr, (size_t)groups * sizeof(unsigned));
-    if (rc) return rc;
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->gctr.p, 0, (size_t)groups * sizeof(unsigned), st));
     ga = (double*)ctx->psA.p;
-    ctr = (unsigned*)ctx->gctr.p;
+    if (C::GPL > 1) {  // co-resident lane groups, arrival counters zeroed
+      rc = ensure(ctx, ctx->gctr, (size_t)groups * sizeof(unsigned));
+      if (rc) return rc;
+      CUDA_TRY(ctx, cudaMemsetAsync(ctx->gctr.p, 0, (size_t)groups * sizeof(unsigned), st));
+      ctr = (unsigned*)ctx->gctr.p;
+    }
     void* args[] = {(void*)&pj, (void*)&terms, (void*)&lanes, (void*)&ga, (void*)&ctr,
                     (void*)&tpriv, (void*)&lane_out, (void*)&prefix_out};
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
-    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)ps_kernel<C, M3>(), dim3(grid),
-                                              dim3(C::THREADS), args, C::SMEM, st));
+    if (C::GPL > 1)
+      CUDA_TRY(ctx, cudaLaunchCooperativeKernel((const void*)ps_kernel<C, M3>(), dim3(grid),
+                                                dim3(C::THREADS), args, C::SMEM, st));
+    else
+      CUDA_TRY(ctx, cudaLaunchKernel((const void*)ps_kernel<C, M3>(), dim3(grid),
+                                     dim3(C::THREADS), args, C::SMEM, st));
   } else {
     if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
     // smem-resident 4-product families: the (s, r) split of the common
@@ -1124,10 +1148,13 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   // D64 with 8 warps of 16 x 16: +2% for fp64 plans, -4% for the fp32 m = 7
   // plan); for the smem-resident D <= 32 its 1.5x operands cost occupancy
   // and the 4-product PS wins
+  // (D = 64 as one CTA per lane: PS3 measured 18% faster than the group-of-2
+  // form for fp64 and 17% faster than the 4-product PS for the fp32 plan)
   const bool three_m =
       ps_s > 0 && (ctx->algo == ALGO_PS3 ||
                    (ctx->algo == ALGO_AUTO &&
-                    (ctx->D >= 128 || (ctx->D == 64 && ctx->bits == 64))));
+                    (ctx->D >= 128 ||
+                     (ctx->D == 64 && (ctx->bits == 64 || d64_single())))));
   if (ps_s > 0 && three_m) {
     PSJob pj;
     std::memset(&pj, 0, sizeof(pj));
@@ -1138,7 +1165,9 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     switch (ctx->fam) {
       case FAM_T16: lanes = ps3_lanes<P3_16>(ctx, n); break;
       case FAM_T32: lanes = ps3_lanes<P3_32>(ctx, n); break;
-      case FAM_T64: lanes = ps3_lanes<P3_64>(ctx, n); break;
+      case FAM_T64:
+        lanes = d64_single() ? ps3_lanes<P3_64s>(ctx, n) : ps3_lanes<P3_64>(ctx, n);
+        break;
       case FAM_T128: lanes = ps3_lanes<P3_128>(ctx, n); break;
       case FAM_T256: lanes = ps3_lanes<P3_256>(ctx, n); break;
       case FAM_T512: lanes = ps3_lanes<P3_512>(ctx, n); break;
@@ -1149,7 +1178,10 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
     switch (ctx->fam) {
       case FAM_T16: rc = ps3_launch<P3_16>(ctx, pj, lanes, lane_out, prefix_out, st); break;
       case FAM_T32: rc = ps3_launch<P3_32>(ctx, pj, lanes, lane_out, prefix_out, st); break;
-      case FAM_T64: rc = ps3_launch<P3_64>(ctx, pj, lanes, lane_out, prefix_out, st); break;
+      case FAM_T64:
+        rc = d64_single() ? ps3_launch<P3_64s>(ctx, pj, lanes, lane_out, prefix_out, st)
+                          : ps3_launch<P3_64>(ctx, pj, lanes, lane_out, prefix_out, st);
+        break;
       case FAM_T128: rc = ps3_launch<P3_128>(ctx, pj, lanes, lane_out, prefix_out, st); break;
       case FAM_T256: rc = ps3_launch<P3_256>(ctx, pj, lanes, lane_out, prefix_out, st); break;
       case FAM_T512: rc = ps3_launch<P3_512>(ctx, pj, lanes, lane_out, prefix_out, st); break;

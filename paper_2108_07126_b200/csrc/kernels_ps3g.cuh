@@ -84,7 +84,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                      double* __restrict__ gA, unsigned* __restrict__ gctr,
                      double2* __restrict__ tpriv, double2* __restrict__ lane_out,
                      double2* __restrict__ prefix_out) {
-  static_assert(C::GPL > 1 && C::LPC == 1 && !C::XS, "group configuration");
+  // GPL == 1: a lane is one CTA owning every column (D = 64); its shared
+  // operands still go through the L2 exchange buffer, and the group
+  // barriers reduce to CTA barriers
+  static_assert(C::LPC == 1 && !C::XS, "group configuration");
   constexpr int D = C::D, WC = C::WC, MT = C::MT, NT = C::NT, NE = MT * NT * 4;
   constexpr int KB = C::KB;
   constexpr int KBC = WC / 4;                 // k-blocks of one column block
@@ -149,7 +152,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int T = job.n_terms;
   const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
   unsigned bar = 0;
-  auto gsync = [&]() { group_barrier(gctr + group, (++bar) * C::GPL); };
+  auto gsync = [&]() {
+    if constexpr (C::GPL > 1)
+      group_barrier(gctr + group, (++bar) * C::GPL);
+    else
+      __syncthreads();
+  };
 
   // weights of slice sl, then this CTA's column chunk of 2X (3-plane A
   // layout, L2) from the 2-plane terms, and T_1 = X[:, J] (B layout) into
