@@ -368,8 +368,10 @@ def roofline_for(t, local_slices, wl, m, kern_ms, peaks):
             cap = json.load(fh).get(t["kernel"])
         if cap:
             traffic = cap["dram_bytes"] * local_slices / cap["slices"]
-            traffic_note = (f"ncu --set full dram read+write of one launch at {cap['slices']} "
-                            f"slices ({cap['dram_bytes']:.3g} B), scaled linearly to this launch; "
+            how = ("measured on one launch of this size" if cap["slices"] == local_slices else
+                   f"measured at {cap['slices']} slices, scaled linearly to this launch")
+            traffic_note = (f"ncu dram__bytes_read.sum + dram__bytes_write.sum "
+                            f"({cap['dram_bytes']:.4g} B; {cap.get('source', '')}), {how}; "
                             f"algorithmic bytes/slice = {8 * wl['n_ctrl']} (amplitude row)")
     except (OSError, ValueError, KeyError):
         pass
@@ -477,12 +479,11 @@ def measure_gpu(args, name, rank, world, local_rank, dist, headline):
     if world == 1 and not headline and not args.no_graph and wl["d"] <= 32:
         try:
             ctx.set_profiling(False)
-            cap = torch.cuda.Stream(dev)
-            cap.wait_stream(stream)
+            torch.cuda.synchronize(dev)
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=cap):
+            with torch.cuda.graph(graph, stream=stream):
                 ctx.equiprop_device_ptr(d_amps.data_ptr(), hi - lo, wl["n_ctrl"], dt,
-                                        out.data_ptr(), stream=cap.cuda_stream, plan=plan)
+                                        out.data_ptr(), stream=stream.cuda_stream, plan=plan)
             for _ in range(args.warmup):
                 graph.replay()
             torch.cuda.synchronize(dev)
@@ -506,15 +507,21 @@ def measure_gpu(args, name, rank, world, local_rank, dist, headline):
             else:
                 step()
             evs[k][1].record(stream)
+            stream.synchronize()
             if graph is not None:
-                stream.synchronize()
                 launches += launches_per_step
             else:
                 tk = ctx.last_timing()
                 kernel_ms.append(tk["main_kernel_ms"])
                 launches += tk["launches"]
-            validate()
+            # the in-kernel amplitude check's flag (a blocking D2H read) is
+            # fetched after every step for the headline; the microsecond
+            # secondaries read it once after the timed loop (same table
+            # every step, so the flag is the same)
+            if headline:
+                validate()
         torch.cuda.synchronize(dev)
+        validate()
     if graph is not None:  # kernel time bounded by the replayed step
         kernel_ms = [s.elapsed_time(e) for s, e in evs]
     if dist is not None:

@@ -1,6 +1,6 @@
 """Gauss-Legendre Magnus modes on the device (north-star extension N2).
 
-quadrature="gauss": two amplitude samples per slice of length 2 dt, at the
+quadrature="gauss-legendre": two amplitude samples per slice of length 2 dt, at the
 Gauss-Legendre nodes.  With magnus=True the exponent is the 4th-order
 Gauss-Legendre Magnus step G = h (H(a) + H(b))/2 + (sqrt(3) h^2/12) i[H(a),
 H(b)] over the reference's effective terms (magnus.py:36-85); magnus=False
@@ -28,7 +28,7 @@ def _run(d, n_ctrl, slices, mode, precision="fp64", seed=1):
     dt = dt / 2.0  # a slice spans 2 dt
     with sp.create(precision) as ctx:
         ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "gauss4",
-                            quadrature="gauss")
+                            quadrature="gauss-legendre")
         amps = sp.ControlAmplitudes(values, dt)
         res = ctx.equiprop(amps)
         kernel = ctx.last_timing()["kernel"]
@@ -62,8 +62,8 @@ def test_three_controls_cross_commutators():
 def test_convergence_orders_on_the_driven_qubit():
     q = sp.DrivenQubit()
     pts = [16, 32, 64, 128, 256, 512, 1024]
-    rows4 = sp.convergence_sweep(q, pts, magnus=True, quadrature="gauss")
-    rows2 = sp.convergence_sweep(q, pts, magnus=False, quadrature="gauss")
+    rows4 = sp.convergence_sweep(q, pts, magnus=True, quadrature="gauss-legendre")
+    rows2 = sp.convergence_sweep(q, pts, magnus=False, quadrature="gauss-legendre")
     rowsm = sp.convergence_sweep(q, [p + 1 for p in pts], magnus=True)  # reference magnus
     o4, _ = sp.fit_convergence_order([p for p, _ in rows4], [e for _, e in rows4])
     o2, _ = sp.fit_convergence_order([p for p, _ in rows2], [e for _, e in rows2])
@@ -77,7 +77,7 @@ def test_convergence_orders_on_the_driven_qubit():
 def test_cumulative_and_sampling_parity():
     h0, hs, values, dt = random_inputs(8, 2, 2 * 300, 5)
     with sp.create() as ctx:
-        ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=True, quadrature="gauss")
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=True, quadrature="gauss-legendre")
         cum = ctx.equiprop_all(sp.ControlAmplitudes(values, dt / 2))
         with pytest.raises(sp.SamplingParityError, match="even number"):
             ctx.equiprop(sp.ControlAmplitudes(values[:-1], dt / 2))

@@ -13,15 +13,15 @@ from paper_2108_07126_b200.magnus import build_effective_system, gauss_magnus_bo
 
 def test_driven_qubit_samples_at_the_gauss_nodes():
     q = sp.DrivenQubit()
-    amps = q.amplitudes(8, "gauss")
+    amps = q.amplitudes(8, "gauss-legendre")
     dt = q.duration / 8
     assert amps.dt == dt
     t = np.array([(2 * k + 1 + s / math.sqrt(3.0)) * dt for k in range(4) for s in (-1, 1)])
     assert np.allclose(amps.values[:, 0], np.cos(t), rtol=0, atol=1e-15)
     assert np.allclose(amps.values[:, 1], np.sin(t), rtol=0, atol=1e-15)
     with pytest.raises(sp.SamplingParityError):
-        q.amplitudes(7, "gauss")
-    assert sp.coerce_pts(7, "gauss") == 8 and sp.coerce_pts(1, "gauss") == 2
+        q.amplitudes(7, "gauss-legendre")
+    assert sp.coerce_pts(7, "gauss-legendre") == 8 and sp.coerce_pts(1, "gauss-legendre") == 2
 
 
 @pytest.mark.parametrize("magnus", [False, True])
@@ -47,12 +47,12 @@ def test_bound_and_slice_count():
                                                  + sum(eff.cross_comm_norms)))
     assert math.isclose(gauss_magnus_bound(eff, dt), expect, rel_tol=1e-15)
     ctx = sp.create()
-    ctx.set_hamiltonian(system, magnus=True, quadrature="gauss")
+    ctx.set_hamiltonian(system, magnus=True, quadrature="gauss-legendre")
     assert ctx.mode == "gauss4"
     assert ctx.slice_count(10) == 5
     assert math.isclose(ctx.bound(dt), expect, rel_tol=1e-15)
     with pytest.raises(sp.SamplingParityError):
         ctx.slice_count(9)
-    ctx.set_hamiltonian(system, quadrature="gauss")
+    ctx.set_hamiltonian(system, quadrature="gauss-legendre")
     assert ctx.mode == "gauss2" and math.isclose(ctx.bound(dt), 2 * dt * sum(system.norms))
     ctx.close()
