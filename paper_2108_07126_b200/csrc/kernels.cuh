@@ -1177,6 +1177,24 @@ __device__ __forceinline__ void group_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
 }
 
+// the same barrier split in two, so CTA-local work can run while the other
+// CTAs of the group arrive: arrive after this CTA's stores, wait before
+// reading theirs
+__device__ __forceinline__ void group_arrive(unsigned* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+  }
+}
+__device__ __forceinline__ void group_wait(unsigned* ctr, unsigned target) {
+  if (threadIdx.x == 0) {
+    while (ld_acquire_gpu(ctr) < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // lane_tc_kernel (the Clenshaw form) lives in kernels_tc.cuh
 
 // ---------------------------------------------------------------------------

@@ -158,6 +158,19 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     else
       __syncthreads();
   };
+  // split form: CTA-local work between the arrival and the wait
+  auto garrive = [&]() {
+    if constexpr (C::GPL > 1)
+      group_arrive(gctr + group);
+    else
+      __syncthreads();
+  };
+  auto gwait = [&]() {
+    if constexpr (C::GPL > 1)
+      group_wait(gctr + group, (++bar) * C::GPL);
+    else
+      __syncthreads();
+  };
 
   // weights of slice sl, then this CTA's column chunk of 2X (3-plane A
   // layout, L2) from the 2-plane terms, and T_1 = X[:, J] (B layout) into
@@ -358,17 +371,20 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     PH(1);
     publish(gy, bo(pb ^ 1), accR, accI, 2.0, 0.0);
     PH(2);
-    gsync();  // 2y published (and everybody is done reading 2X)
-    first_frags(gy);
-    PH(3);
-    // ---- Clenshaw in y
+    // 2y published; the first Clenshaw B operand (own TMEM -> own smem) is
+    // staged while the group's other CTAs arrive (the arrival's CTA barrier
+    // also ends every read of the publication staging buffer)
+    garrive();
     int pc = 0;
     {
       double qr[NE], qi[NE];
       load_Q(r - 1, qr, qi);
       write_B(bo(pc), qr, qi, (r - 1 == 1) ? 0.5 : 1.0);
     }
-    __syncthreads();
+    gwait();  // everybody's 2y published (and done reading 2X); b_{r-1} staged
+    first_frags(gy);
+    PH(3);
+    // ---- Clenshaw in y
     for (int j = r - 2; j >= 0; --j) {
       load_Q(j, accR, accI);
       if (j + 2 <= r - 1) {
@@ -401,13 +417,15 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     if (more) assemble(sl + 1, bo(pc ^ 1));
     tb = pc ^ 1;
     PH(6);
-    // P (running product) into bo(pc) as the B operand of the product GEMM
+    garrive();  // U and the next 2X published
+    // P (running product) into bo(pc) as the B operand of the product GEMM,
+    // while the group arrives
     {
       double pr[NE], pi[NE];
       tmem_load_block<NE>(tm(0), pr, pi);
       write_B(bo(pc), pr, pi, 1.0);
     }
-    gsync();  // U and the next 2X published; P staged
+    gwait();  // everybody's U and next 2X published; P staged
     first_frags(gu);
     PH(7);
     // ---- V <- U V  (prefetches the next slice's first 2X fragments)
