@@ -69,6 +69,7 @@ def main():
     ap.add_argument("--cpu-s", type=float, default=2.0)
     ap.add_argument("--dims", default=",".join(map(str, DIMS)))
     ap.add_argument("--precisions", default="fp64,fp32")
+    ap.add_argument("--qubit", type=int, default=1, help="add the driven-qubit d = 2 series")
     args = ap.parse_args()
     import torch
 
@@ -80,7 +81,7 @@ def main():
 
     def pipe_peak(kernel):
         key = ("fp32_ffma_tflops" if kernel.startswith("lane_f32") else "fp64_dfma_tflops"
-               if kernel.startswith("lane_small") else "fp64_dmma_tflops")
+               if kernel.startswith(("lane_small", "lane_su2")) else "fp64_dmma_tflops")
         return peaks[key] * 1e12
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
@@ -150,7 +151,75 @@ def main():
                 fh.flush()
             ctx.close()
             del d_amps
+        if args.qubit:
+            qubit_series(args, prec, sp, torch, dev, stream, fh, pipe_peak)
     fh.close()
+
+
+def qubit_series(args, prec, sp, torch, dev, stream, fh, pipe_peak):
+    """The paper's driven qubit (d = 2, su(2) terms: the quaternion kernel for
+    fp64) at every slice count: the north-star d = 2 series.  Each point is
+    timed like the bench's qubit lines (CUDA graph, L2 written then read
+    between 30 replays, mean over the replays); ``hbm_frac`` = amplitude
+    bytes / kernel-bounded step time / the measured copy bandwidth."""
+    from cases import qubit_inputs
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm = float(json.load(f)["hbm_gbs"]) * 1e9
+    except (OSError, ValueError, KeyError):
+        hbm = 6.65e12
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    clean = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    st = torch.cuda.Stream(dev)
+    for n in SLICES:
+        h0, hs, values, dt = qubit_inputs(n, "midpoint")
+        ctx = sp.create(prec)
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+        plan = ctx.plan_for(dt)
+        d_amps = torch.from_numpy(values).to(dev)
+        out = torch.empty((2, 2), dtype=torch.complex128 if prec == "fp64" else torch.complex64,
+                          device=dev)
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                ctx.equiprop_device_ptr(d_amps.data_ptr(), n, 2, dt, out.data_ptr(),
+                                        stream=st.cuda_stream, plan=plan)
+        torch.cuda.synchronize(dev)
+        ctx.set_profiling(True)
+        ctx.equiprop_device_ptr(d_amps.data_ptr(), n, 2, dt, out.data_ptr(),
+                                stream=st.cuda_stream, plan=plan)
+        torch.cuda.synchronize(dev)
+        t = ctx.last_timing()
+        ctx.set_profiling(False)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            ctx.equiprop_device_ptr(d_amps.data_ptr(), n, 2, dt, out.data_ptr(),
+                                    stream=st.cuda_stream, plan=plan)
+        ts = []
+        with torch.cuda.stream(st):
+            for k in range(33):
+                flush.fill_(float(k))
+                clean.sum()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                g.replay()
+                b.record(st)
+                st.synchronize()
+                if k >= 3:
+                    ts.append(a.elapsed_time(b))
+        step_ms = statistics.mean(ts)
+        F = canonical_flops(2, plan.m_max, 3)
+        rec = {"precision": prec, "dim": 2, "system": "driven qubit", "slices": n,
+               "m": plan.m_max, "slices_per_s": n / (step_ms / 1e3), "ms_per_step": step_ms,
+               "kernel": t["kernel"], "fp64_frac": t["executed_flops"] / (step_ms / 1e3)
+               / pipe_peak(t["kernel"]),
+               "canonical_frac": n * F / (step_ms / 1e3) / pipe_peak(t["kernel"]),
+               "hbm_frac": n * 16 / (step_ms / 1e3) / hbm,
+               "timing": "CUDA graph, L2 flushed, mean of 30 replays (step, not kernel)"}
+        print(json.dumps(rec), flush=True)
+        fh.write(json.dumps(rec) + "\n")
+        fh.flush()
+        ctx.close()
 
 
 if __name__ == "__main__":
