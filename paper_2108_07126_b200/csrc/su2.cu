@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <set>
+#include <utility>
 
 #include "internal.h"
 #include "kernels_su2.cuh"
@@ -107,16 +108,19 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 cudaError_t su2_run(const Su2Job& job, int grid, int block, cudaStream_t st) {
   const Su2Kernel k = su2_kernel_for(job);
   if (!k.fn) return cudaErrorInvalidValue;
-  // dynamic shared memory (opt-in above 48 KB, set once per kernel)
+  // dynamic shared memory (opt-in above 48 KB, set once per kernel and
+  // device: multi-device contexts launch on several devices)
   static std::mutex mu;
-  static std::set<const void*> opted;
+  static std::set<std::pair<int, const void*>> opted;
   {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> g(mu);
-    if (!opted.count(k.fn)) {
-      const cudaError_t e =
-          cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
+    if (!opted.count({dev, k.fn})) {
+      e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
       if (e != cudaSuccess) return e;
-      opted.insert(k.fn);
+      opted.insert({dev, k.fn});
     }
   }
   if (!k.tma) {
