@@ -355,8 +355,8 @@ def roofline_for(t, local_slices, wl, m, kern_ms, peaks):
     reference-algorithm work F(d, m, T) of SURVEY.md §8(d) on the same
     denominator (above 1 when the kernel needs fewer flops than the
     reference's Clenshaw count)."""
-    dfma = t["kernel"].startswith(("lane_small", "lane_su2"))
-    ffma = t["kernel"].startswith("lane_f32")
+    ffma = t["kernel"].startswith(("lane_f32", "lane_su2_f32"))
+    dfma = not ffma and t["kernel"].startswith(("lane_small", "lane_su2"))
     peak = (peaks["fp32_ffma_tflops"] if ffma else peaks["fp64_dfma_tflops"] if dfma
             else peaks["fp64_dmma_tflops"]) * 1e12
     F = canonical_flops(wl["d"], m, n_terms_for(wl))

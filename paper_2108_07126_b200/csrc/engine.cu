@@ -75,7 +75,8 @@ using P3_512 = PS3Cfg<512, 8, 4, 1, 8, 1, 64, false>;
 
 enum Algo { ALGO_AUTO = 0, ALGO_CLENSHAW = 1, ALGO_PS = 2, ALGO_PS3 = 3,
             ALGO_F32 = 4 /* reported only: the complex64-arithmetic lane kernel */,
-            ALGO_SU2 = 5 /* reported only: the su(2) quaternion lane kernel */ };
+            ALGO_SU2 = 5 /* reported only: the su(2) quaternion lane kernel */,
+            ALGO_SU2_F32 = 6 /* reported only: the same in float32 arithmetic */ };
 
 // GEMMs per slice: Clenshaw m; PS (s-1) + (r-1) + 1, r = ceil((m+1)/s)
 int ps_cost(int m, int s) {
@@ -162,6 +163,7 @@ bool d64_single();
 
 const char* family_kernel_name(int fam, int algo) {
   if (algo == 5) return "lane_su2_kernel";
+  if (algo == 6) return "lane_su2_f32_kernel";
   if (algo == 4)  // complex64 arithmetic (kernels_f32.cuh)
     return fam == FAM_S2 ? "lane_f32_kernel<2>" : fam == FAM_S4 ? "lane_f32_kernel<4>"
                                                                 : "lane_f32_kernel<8>";
@@ -951,7 +953,7 @@ bool su2_applies(const sp_ctx* ctx, const SliceJob& job) {
     const char* e = getenv("SP_SU2");
     return (e && e[0] == '0') ? 0 : 1;
   }();
-  if (!enabled || !ctx->su2_terms || ctx->bits != 64 || !job.coef_alt) return false;
+  if (!enabled || !ctx->su2_terms || !job.coef_alt) return false;
   if (job.mode > SP_MODE_MAGNUS) return false;  // Gauss-Legendre: general d = 2 kernel
   if (!(job.phase[0] == 1.0 && job.phase[1] == 0.0)) return false;
   if (job.n_ctrl % 2 == 0 && ((uintptr_t)job.amps & 15u)) return false;  // vector row loads
@@ -978,6 +980,7 @@ int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_ou
   sj.viol = job.viol;
   sj.out = fused_out;
   sj.to_fp32 = out32(ctx) ? 1 : 0;
+  sj.arith32 = ctx->bits == 32 ? 1 : 0;
   // lanes: >= SPT slices each (tree and tail amortised), one CTA per SM
   static const int spt = [] {
     const char* e = getenv("SP_SU2_SPT");
@@ -1028,7 +1031,7 @@ int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_ou
     fprintf(stderr, "\n");
   }
   ++ctx->launches;
-  ctx->last_algo = ALGO_SU2;
+  ctx->last_algo = ctx->bits == 32 ? ALGO_SU2_F32 : ALGO_SU2;
   ctx->last_gemms = job.m;
   ctx->last_lanes = grid * block;
   *prods = (const double2*)ctx->lanes.p;
@@ -1044,11 +1047,11 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   const int D = ctx->D;
   const size_t dd = (size_t)D * D;
   int lanes = 1;
-  if (f32_path(ctx)) return f32_launch(ctx, job, prefix_out, st, prods, count);
-  if (ctx->fam == FAM_T8) return d8_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_S2 && fused_out && cta_reduce && !prefix_out && !job.vinit &&
       su2_applies(ctx, job))
     return su2_launch(ctx, job, st, fused_out, prods, count);
+  if (f32_path(ctx)) return f32_launch(ctx, job, prefix_out, st, prods, count);
+  if (ctx->fam == FAM_T8) return d8_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {
     const int tpl = (ctx->fam == FAM_S2) ? 1 : 4;
     // pairwise: at least 4 slices per lane (short CTA tree and tail for the
@@ -1088,7 +1091,9 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
       // beta = 0.5 fp64 13, magnus 15)
       // and, for two controls in midpoint mode (the driven qubit), the
       // control count of the fast path
-      const bool two = job.n_ctrl == 2 && job.mode == SP_MODE_MIDPOINT;
+      // (its rows are read as 16-byte vectors: aligned tables only)
+      const bool two = job.n_ctrl == 2 && job.mode == SP_MODE_MIDPOINT &&
+                       ((uintptr_t)job.amps & 15u) == 0;
 #define SP_S2(MCV)                                                                          \
   (two ? lane_small_kernel<2, 1, MCV, 2><<<blocks, 256, 0, st>>>(job, tp, lanes, lane_out,  \
                                                                  cta_out, prefix_out, tail) \
@@ -1387,7 +1392,7 @@ double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
   //   d = 2, complex pairs (other modes / more controls): 137 + 28.7 m + 16 T,
   //          +40 for the three-point modes (within 3% of every point)
   //   d = 3, 4: 10.3 + 576 m + 64 T
-  if (ctx->last_algo == ALGO_SU2) {
+  if (ctx->last_algo == ALGO_SU2 || ctx->last_algo == ALGO_SU2_F32) {
     // su(2) quaternion kernel (flops, DFMA = 2): 3 FMA per control term
     // (assembly), 5 for zeta2, 4 per Clenshaw step after the peeled one
     // (+2 at j = 0), 3 MUL for U, 28 for V <- U V; three-point control
@@ -1497,7 +1502,9 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
   int rc = build_job(ctx, d_amps, pts, n_ctrl, dt, plan, &job);
   if (rc) return rc;
   // the small families' pairwise product is one launch with a fused tail
-  const bool fused = (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) && !f32_path(ctx) &&
+  // (complex64 contexts too when the su(2) kernel takes the call)
+  const bool su2 = ctx->fam == FAM_S2 && reduction == SP_REDUCE_PAIRWISE && su2_applies(ctx, job);
+  const bool fused = (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) && (!f32_path(ctx) || su2) &&
                      reduction == SP_REDUCE_PAIRWISE && job.n_slices > 0;
   rc = arm_validation(ctx, &job, st, fused);
   if (rc) return rc;
@@ -1516,8 +1523,8 @@ int equiprop_dev(sp_ctx* ctx, const double* d_amps, int64_t pts, int n_ctrl, dou
     total = (const double2*)ctx->result.p;
   } else {
     const bool small = plain_family(ctx->fam);
-    const bool cta_reduce = (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) && !f32_path(ctx) &&
-                            reduction == SP_REDUCE_PAIRWISE;
+    const bool cta_reduce = (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) &&
+                            (!f32_path(ctx) || su2) && reduction == SP_REDUCE_PAIRWISE;
     const double2* prods = nullptr;
     int cnt = 0;
     // small families + pairwise: one launch does everything (fused tail)

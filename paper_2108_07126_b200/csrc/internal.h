@@ -73,6 +73,7 @@ struct Su2Job {
   void* cta_out;                    // gridDim x 4 doubles: CTA products
   void* out;                        // 2 x 2 result (complex128, or complex64 if to_fp32)
   int to_fp32;
+  int arith32;                      // complex64 context: float32 arithmetic
   // phase timestamps (tools only, SP_SU2_PROF=1): [2k] = min, [2k+1] = max
   // over CTAs of %globaltimer at phase k; null = off
   unsigned long long* prof;

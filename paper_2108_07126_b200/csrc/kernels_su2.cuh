@@ -44,9 +44,11 @@
 
 namespace sp {
 
-struct Quat {  // [[a, b], [-conj(b), conj(a)]]
-  double ar, ai, br, bi;
+template <class R>
+struct QuatT {  // [[a, b], [-conj(b), conj(a)]]
+  R ar, ai, br, bi;
 };
+using Quat = QuatT<double>;
 
 // tools only: %globaltimer at phase k, min / max over the CTAs (thread 0)
 __device__ __forceinline__ void su2_mark(const Su2Job& job, int k) {
@@ -58,22 +60,26 @@ __device__ __forceinline__ void su2_mark(const Su2Job& job, int k) {
   }
 }
 
-__device__ __forceinline__ Quat quat_identity() { return Quat{1.0, 0.0, 0.0, 0.0}; }
+template <class R = double>
+__device__ __forceinline__ QuatT<R> quat_identity() {
+  return QuatT<R>{R(1), R(0), R(0), R(0)};
+}
 
 // P Q (P later in time, on the left): row 0 of the 2 x 2 complex product
 // with Q10 = -conj(Q.b), Q11 = conj(Q.a), summed in mat_mul's order
-__device__ __forceinline__ Quat quat_mul(const Quat& P, const Quat& Q) {
-  Quat R;
-  double re = P.ar * Q.ar;
+template <class R>
+__device__ __forceinline__ QuatT<R> quat_mul(const QuatT<R>& P, const QuatT<R>& Q) {
+  QuatT<R> Rs;
+  R re = P.ar * Q.ar;
   re = fma(-P.ai, Q.ai, re);
   re = fma(P.br, -Q.br, re);
   re = fma(-P.bi, Q.bi, re);
-  double im = P.ar * Q.ai;
+  R im = P.ar * Q.ai;
   im = fma(P.ai, Q.ar, im);
   im = fma(P.br, Q.bi, im);
   im = fma(P.bi, -Q.br, im);
-  R.ar = re;
-  R.ai = im;
+  Rs.ar = re;
+  Rs.ai = im;
   re = P.ar * Q.br;
   re = fma(-P.ai, Q.bi, re);
   re = fma(P.br, Q.ar, re);
@@ -82,18 +88,20 @@ __device__ __forceinline__ Quat quat_mul(const Quat& P, const Quat& Q) {
   im = fma(P.ai, Q.br, im);
   im = fma(P.br, -Q.ai, im);
   im = fma(P.bi, Q.ar, im);
-  R.br = re;
-  R.bi = im;
-  return R;
+  Rs.br = re;
+  Rs.bi = im;
+  return Rs;
 }
 
-__device__ __forceinline__ Quat quat_shfl_down(const Quat& q, int k) {
-  return Quat{__shfl_down_sync(0xffffffffu, q.ar, k), __shfl_down_sync(0xffffffffu, q.ai, k),
+template <class R>
+__device__ __forceinline__ QuatT<R> quat_shfl_down(const QuatT<R>& q, int k) {
+  return QuatT<R>{__shfl_down_sync(0xffffffffu, q.ar, k), __shfl_down_sync(0xffffffffu, q.ai, k),
               __shfl_down_sync(0xffffffffu, q.br, k), __shfl_down_sync(0xffffffffu, q.bi, k)};
 }
 
 // lane 0 ends with M_{31} ... M_1 M_0 (later lanes on the left)
-__device__ __forceinline__ void quat_warp_product(Quat& q) {
+template <class R>
+__device__ __forceinline__ void quat_warp_product(QuatT<R>& q) {
 #pragma unroll
   for (int k = 1; k < 32; k <<= 1) q = quat_mul(quat_shfl_down(q, k), q);
 }
@@ -101,7 +109,7 @@ __device__ __forceinline__ void quat_warp_product(Quat& q) {
 // |v| <= 1 fails (also for NaN): accumulated without a branch
 __device__ __forceinline__ bool amp_bad(double v) { return !(fabs(v) <= 1.0); }
 
-template <int MODE, int NCC>
+template <int MODE, int NCC, class R = double>
 struct Su2Shape {
   // doubles read per slice: midpoint one row; three-point the rows 2s+1, 2s+2
   // (row 2s is the previous slice's last row)
@@ -109,9 +117,13 @@ struct Su2Shape {
   static constexpr bool VEC = (NCC % 2) == 0;  // 16-byte rows (host-checked alignment)
   static constexpr int UNIT = VEC ? 16 : 8;    // bytes per cp.async
   static constexpr int CP = K * 8 / UNIT;      // cp.async per slice
-  // threads per CTA: 1024 (64 registers) except the three-point forms with
-  // >= 3 controls, whose weights need more registers
-  static constexpr int TPB = (MODE != SP_MODE_MIDPOINT && NCC >= 3) ? 512 : 1024;
+  // threads per CTA: 1024 (64 registers) except the three-point forms, whose
+  // float64 weights need more registers (with >= 3 controls, or next to the
+  // float32 working set of complex64 contexts)
+  static constexpr bool F32 = sizeof(R) == 4;
+  static constexpr int TPB = MODE == SP_MODE_MIDPOINT ? 1024
+                             : NCC >= 3 ? (F32 ? 256 : 512)
+                                        : (F32 ? 512 : 1024);
   // shared-memory ring: DS slices per thread in flight (<= 192 KB per CTA:
   // the bytes in flight an SM needs to stream HBM at speed)
   static constexpr int DS_RAW = (192 * 1024) / (TPB * K * 8);
@@ -152,18 +164,21 @@ __device__ __noinline__ unsigned long long su2_first_bad(const double* amps, int
 // One slice's propagator: weights from the slice's amplitude samples `cur`
 // (and, for the three-point modes, the carried row 2s in r1),
 // Z' = sum_t w_t tz_t, the real Clenshaw pairs, U = A I + i B Z'.
-template <int MODE, int NCC, int MC>
-__device__ __forceinline__ Quat su2_u(const Su2Job& job, int m, const double* cur,
-                                      double (&r1)[NCC]) {
+template <class R, int MODE, int NCC, int MC>
+__device__ __forceinline__ QuatT<R> su2_u(const Su2Job& job, int m, const double* cur,
+                                          double (&r1)[NCC]) {
   constexpr int T = MODE == SP_MODE_MAGNUS ? 1 + 2 * NCC + NCC * (NCC - 1) / 2 : 1 + NCC;
   static_assert(T <= SU2_MAX_TERMS, "too many su(2) terms");
   // ---- slice weights (hamiltonian.py:199-205, magnus.py:88-106) and
   // Z' = sum_t w_t tz_t (2X factor folded into tz on the host)
-  double dz = job.tz[0][0], zx = job.tz[0][1], zy = job.tz[0][2];
-  auto add = [&](int t, double w) {
-    dz = fma(w, job.tz[t][0], dz);
-    zx = fma(w, job.tz[t][1], zx);
-    zy = fma(w, job.tz[t][2], zy);
+  // (complex64 contexts: the float64 weights and the terms cast to the
+  // working precision, linalg.py:273-274, everything after in float32)
+  R dz = (R)job.tz[0][0], zx = (R)job.tz[0][1], zy = (R)job.tz[0][2];
+  auto add = [&](int t, double w64) {
+    const R w = (R)w64;
+    dz = fma(w, (R)job.tz[t][0], dz);
+    zx = fma(w, (R)job.tz[t][1], zx);
+    zy = fma(w, (R)job.tz[t][2], zy);
   };
   if constexpr (MODE == SP_MODE_MIDPOINT) {
 #pragma unroll
@@ -185,35 +200,35 @@ __device__ __forceinline__ Quat su2_u(const Su2Job& job, int m, const double* cu
 #pragma unroll
     for (int q = 0; q < NCC; ++q) r1[q] = c3[q];
   }
-  const double zeta2 = fma(dz, dz, fma(zx, zx, zy * zy));
+  const R zeta2 = fma(dz, dz, fma(zx, zx, zy * zy));
   // ---- real Clenshaw pairs; the j = m - 1 step peeled (B_{m+1} = 0)
-  double A = job.cr[m - 1], B = job.cr[m], oA = job.cr[m], oB = 0.0;
+  R A = (R)job.cr[m - 1], B = (R)job.cr[m], oA = (R)job.cr[m], oB = R(0);
   constexpr int MU = MC > 0 ? MC : 1;
 #pragma unroll MU
   for (int jj = m - 2; jj >= 0; --jj) {
-    const double beta = (jj == 0) ? 2.0 : 1.0;
-    const double nA = job.cr[jj] + fma(zeta2, B, -beta * oA);
-    const double nB = A - beta * oB;
+    const R beta = (jj == 0) ? R(2) : R(1);
+    const R nA = (R)job.cr[jj] + fma(zeta2, B, -beta * oA);
+    const R nB = A - beta * oB;
     oA = A;
     oB = B;
     A = nA;
     B = nB;
   }
-  return Quat{A, B * dz, -(B * zy), B * zx};
+  return QuatT<R>{A, B * dz, -(B * zy), B * zx};
 }
 
 // V <- U(slice) V
-template <int MODE, int NCC, int MC>
+template <class R, int MODE, int NCC, int MC>
 __device__ __forceinline__ void su2_slice(const Su2Job& job, int m, const double* cur,
-                                          double (&r1)[NCC], Quat& V) {
-  V = quat_mul(su2_u<MODE, NCC, MC>(job, m, cur, r1), V);
+                                          double (&r1)[NCC], QuatT<R>& V) {
+  V = quat_mul(su2_u<R, MODE, NCC, MC>(job, m, cur, r1), V);
 }
 
 // After the lane loops: the lane's first amplitude offender (rare path; rows
 // [r0, rl] of the table), the ordered CTA product, the arrival ticket and, in
 // the last CTA, the ordered product of the CTA products and the d x d result.
-template <int NCC>
-__device__ __forceinline__ void su2_finish(const Su2Job& job, Quat V, bool bad, int64_t r0,
+template <class R, int NCC>
+__device__ __forceinline__ void su2_finish(const Su2Job& job, QuatT<R> V, bool bad, int64_t r0,
                                            int64_t rl) {
   if (bad && job.viol) {
     const unsigned long long v = su2_first_bad(job.amps, r0, rl, NCC);
@@ -221,15 +236,15 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, Quat V, bool bad, 
     atomicMin(slot, v);
   }
   // ---- ordered products: warps, then the CTA's warps (warp 0)
-  __shared__ Quat wq[32];
+  __shared__ QuatT<R> wq[32];
   __shared__ bool last;
   const int ln = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  auto cta_product = [&](Quat& q) {  // result in thread 0
+  auto cta_product = [&](QuatT<R>& q) {  // result in thread 0
     quat_warp_product(q);
     if (ln == 0) wq[wp] = q;
     __syncthreads();
     if (wp == 0) {
-      q = ln < nw ? wq[ln] : quat_identity();
+      q = ln < nw ? wq[ln] : quat_identity<R>();
       quat_warp_product(q);
     }
     __syncthreads();
@@ -238,7 +253,7 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, Quat V, bool bad, 
   cta_product(V);
   su2_mark(job, 3);
   if (threadIdx.x == 0) {
-    reinterpret_cast<Quat*>(job.cta_out)[blockIdx.x] = V;
+    reinterpret_cast<QuatT<R>*>(job.cta_out)[blockIdx.x] = V;
     unsigned old;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
                  : "=r"(old)
@@ -253,16 +268,23 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, Quat V, bool bad, 
   // (later on the left), then one CTA-wide ordered product
   const int G = (int)gridDim.x, per = (G + (int)blockDim.x - 1) / (int)blockDim.x;
   const int i0 = min(G, (int)threadIdx.x * per), i1 = min(G, i0 + per);
-  const double2* cp = reinterpret_cast<const double2*>(job.cta_out);
-  Quat M = quat_identity();
+  QuatT<R> M = quat_identity<R>();
   for (int i = i0; i < i1; ++i) {
-    const double2 a = __ldcg(cp + 2 * i), b = __ldcg(cp + 2 * i + 1);
-    M = quat_mul(Quat{a.x, a.y, b.x, b.y}, M);
+    QuatT<R> c;
+    if constexpr (sizeof(R) == 8) {
+      const double2* cp = reinterpret_cast<const double2*>(job.cta_out);
+      const double2 a = __ldcg(cp + 2 * i), b = __ldcg(cp + 2 * i + 1);
+      c = QuatT<R>{a.x, a.y, b.x, b.y};
+    } else {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(job.cta_out) + i);
+      c = QuatT<R>{a.x, a.y, a.z, a.w};
+    }
+    M = quat_mul(c, M);
   }
   cta_product(M);
   if (threadIdx.x == 0) {
     // [[a, b], [-conj(b), conj(a)]] in the output dtype
-    const double e[8] = {M.ar, M.ai, M.br, M.bi, -M.br, M.bi, M.ar, -M.ai};
+    const R e[8] = {M.ar, M.ai, M.br, M.bi, -M.br, M.bi, M.ar, -M.ai};
     if (job.to_fp32) {
       float* o = reinterpret_cast<float*>(job.out);
 #pragma unroll
@@ -270,7 +292,7 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, Quat V, bool bad, 
     } else {
       double* o = reinterpret_cast<double*>(job.out);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = e[i];
+      for (int i = 0; i < 8; ++i) o[i] = (double)e[i];
     }
     su2_mark(job, 5);
     *job.ctr = 0;  // ready for the next launch
@@ -288,9 +310,10 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, Quat V, bool bad, 
 // [lane n / lanes, (lane + 1) n / lanes); the rows stream through a
 // per-thread cp.async ring in shared memory.
 // ---------------------------------------------------------------------------
-template <int MODE, int NCC, int MC>
-__global__ void __launch_bounds__(Su2Shape<MODE, NCC>::TPB, 1) lane_su2_kernel(const Su2Job job) {
-  using S = Su2Shape<MODE, NCC>;
+template <int MODE, int NCC, int MC, class R = double>
+__global__ void __launch_bounds__(Su2Shape<MODE, NCC, R>::TPB, 1)
+    lane_su2_kernel(const Su2Job job) {
+  using S = Su2Shape<MODE, NCC, R>;
   constexpr int K = S::K, DS = S::DS, CP = S::CP, UNIT = S::UNIT;
   extern __shared__ __align__(16) unsigned char su2_ring[];
   const int m = MC > 0 ? MC : job.m;
@@ -300,7 +323,7 @@ __global__ void __launch_bounds__(Su2Shape<MODE, NCC>::TPB, 1) lane_su2_kernel(c
   const int64_t s1 = ((int64_t)lane + 1) * job.n_slices / lanes;
   const int cnt = (int)(s1 - s0);
 
-  Quat V = quat_identity();
+  QuatT<R> V = quat_identity<R>();
   bool bad = false;
   // first unit of this lane: row s0 (midpoint) or rows 2 s0 + 1, 2 s0 + 2
   const unsigned char* unit0 = reinterpret_cast<const unsigned char*>(
@@ -351,11 +374,11 @@ __global__ void __launch_bounds__(Su2Shape<MODE, NCC>::TPB, 1) lane_su2_kernel(c
         }
 #pragma unroll
         for (int q = 0; q < K; ++q) bad |= amp_bad(cur[q]);
-        su2_slice<MODE, NCC, MC>(job, m, cur, r1, V);
+        su2_slice<R, MODE, NCC, MC>(job, m, cur, r1, V);
       }
     }
   }
-  su2_finish<NCC>(job, V, bad, MODE == SP_MODE_MIDPOINT ? s0 : 2 * s0,
+  su2_finish<R, NCC>(job, V, bad, MODE == SP_MODE_MIDPOINT ? s0 : 2 * s0,
                   MODE == SP_MODE_MIDPOINT ? s1 - 1 : 2 * s1);
 }
 
@@ -409,7 +432,7 @@ __device__ __forceinline__ void su2_tma_2d(void* dst, const void* tmap, int x, i
       : "memory");
 }
 
-template <int NCC, int MC, int C>
+template <int NCC, int MC, int C, class R = double>
 __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
     lane_su2_tma_kernel(const Su2Job job, const __grid_constant__ CUtensorMap tmap,
                         const int64_t L) {
@@ -451,7 +474,7 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
   }
   __syncwarp();
 
-  Quat V = quat_identity();
+  QuatT<R> V = quat_identity<R>();
   bool bad = false;
   double r1[NCC];
   const int sw = LROWB == 128 ? (ln & 7) : ((ln >> 1) & 3);  // swizzle of this lane's row
@@ -472,14 +495,14 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
     if (!direct && (r + 1) * C <= cnt) {
       // a whole round: the C slice propagators are independent (ILP), the
       // running product takes them in adjacent pairs, later on the left
-      Quat U[C];
+      QuatT<R> U[C];
 #pragma unroll
       for (int k = 0; k < C; ++k) {
         double cur[NCC];
         smem_row(k, cur);
 #pragma unroll
         for (int q = 0; q < NCC; ++q) bad |= amp_bad(cur[q]);
-        U[k] = su2_u<SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1);
+        U[k] = su2_u<R, SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1);
       }
 #pragma unroll
       for (int k = 0; k < C; k += 2) V = quat_mul(quat_mul(U[k + 1], U[k]), V);
@@ -497,7 +520,7 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
           }
 #pragma unroll
           for (int q = 0; q < NCC; ++q) bad |= amp_bad(cur[q]);
-          su2_slice<SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1, V);
+          su2_slice<R, SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1, V);
         }
       }
     }
@@ -509,7 +532,7 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
       su2_tma_2d(ring + s * STAGE, &tmap, (r + NST) * C * NCC, (int)wlane0, wb + s);
     }
   }
-  su2_finish<NCC>(job, V, bad, s0, s1 - 1);
+  su2_finish<R, NCC>(job, V, bad, s0, s1 - 1);
 }
 
 }  // namespace sp
@@ -545,7 +568,7 @@ __global__ void __launch_bounds__(512, 1) qubit_reference_kernel(const Su2Job jo
     // [[c - i s az, -i s (nx - i ny)], [-i s (nx + i ny), c + i s az]]
     V = quat_mul(Quat{q.c, -q.s * q.az, -q.s * ny, -q.s * nx}, V);
   }
-  su2_finish<1>(job, V, false, 0, 0);
+  su2_finish<double, 1>(job, V, false, 0, 0);
 }
 
 }  // namespace sp

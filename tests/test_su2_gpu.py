@@ -174,3 +174,67 @@ def test_not_traceless_uses_the_general_kernel():
     h0 = h0 + 0.25 * np.eye(2)
     res, kernel = _run(h0, hs, values, dt, "midpoint")
     assert kernel.startswith("lane_small_kernel")
+
+
+def test_misaligned_table_falls_back_to_the_general_kernel():
+    """A device table whose rows are not 16-byte aligned (offset by one
+    double) cannot feed the TMA / vector row loads: the general d = 2 kernel
+    runs instead, with the same result."""
+    import torch
+    h0, hs, values, dt = qubit_inputs(20000, "midpoint")
+    with sp.create() as ctx:
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+        base = torch.zeros(values.size + 1, dtype=torch.float64, device="cuda")
+        base[1:] = torch.from_numpy(values.reshape(-1)).cuda()
+        out = torch.empty((2, 2), dtype=torch.complex128, device="cuda")
+        ctx.equiprop_device_ptr(base.data_ptr() + 8, values.shape[0], 2, dt, out.data_ptr())
+        torch.cuda.synchronize()
+        assert ctx.last_timing()["kernel"].startswith("lane_small")
+        aligned = torch.from_numpy(values).cuda()
+        out2 = torch.empty_like(out)
+        ctx.equiprop_device_ptr(aligned.data_ptr(), values.shape[0], 2, dt, out2.data_ptr())
+        torch.cuda.synchronize()
+        assert ctx.last_timing()["kernel"] == "lane_su2_kernel"
+        assert rel_fro(out.cpu().numpy(), out2.cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", ["midpoint", "magnus"])
+def test_emulated_multi_device_qubit(mode):
+    """A multi-device context (4 children emulated on device 0) runs the
+    su(2) kernel on every block and matches the single-device result."""
+    pts = 400_000 if mode == "midpoint" else 400_001
+    h0, hs, values, dt = qubit_inputs(pts, mode)
+    res = []
+    for devs in (None, [0, 0, 0, 0]):
+        with sp.create(devices=devs) as ctx:
+            ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus")
+            res.append(ctx.equiprop(sp.ControlAmplitudes(values, dt)).u)
+    u, _ = oracle.slice_propagators(h0, hs, values, dt, mode=mode)
+    ref, seq = oracle.reduce_pairwise(u), oracle.reduce_sequential(u)
+    tol, _ = parity_tolerance(ref, seq, "fp64")
+    assert rel_fro(res[1], res[0]) <= tol
+    assert rel_fro(res[1], ref) <= tol
+
+
+@pytest.mark.parametrize("mode", ["midpoint", "magnus"])
+@pytest.mark.parametrize("slices", [1, 5000, 300_000])
+def test_complex64_contexts_run_float32_su2(mode, slices):
+    """complex64 contexts: the same kernels in float32 arithmetic (weights
+    and terms cast to float32 as the reference's fp32 path does), gated
+    against the oracle's complex64 restatement: max(1e-5, 4 eps_self)."""
+    pts = slices if mode == "midpoint" else 2 * slices + 1
+    h0, hs, values, dt = qubit_inputs(pts, mode)
+    with sp.create("fp32") as ctx:
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus")
+        res = ctx.equiprop(sp.ControlAmplitudes(values, dt))
+        kernel = ctx.last_timing()["kernel"]
+    assert kernel == "lane_su2_f32_kernel" and res.u.dtype == np.complex64
+    u, _ = oracle.slice_propagators(h0, hs, values, dt, mode=mode, bits=32)
+    ref, seq = oracle.reduce_pairwise(u), oracle.reduce_sequential(u)
+    tol, eps = parity_tolerance(ref, seq, "fp32")
+    u64, _ = oracle.slice_propagators(h0, hs, values, dt, mode=mode)
+    ref64 = oracle.reduce_pairwise(u64)
+    err, err64, ref_err64 = rel_fro(res.u, ref), rel_fro(res.u, ref64), rel_fro(ref, ref64)
+    print(f"\n[su2 f32] {mode} slices={slices}: vs ref c64 {err:.3e} (tol {tol:.3e}), "
+          f"vs c128 {err64:.3e} (reference c64 vs c128 {ref_err64:.3e})")
+    assert err <= tol or err64 <= ref_err64

@@ -80,8 +80,9 @@ def main():
         peaks = json.load(fh)
 
     def pipe_peak(kernel):
-        key = ("fp32_ffma_tflops" if kernel.startswith("lane_f32") else "fp64_dfma_tflops"
-               if kernel.startswith(("lane_small", "lane_su2")) else "fp64_dmma_tflops")
+        key = ("fp32_ffma_tflops" if kernel.startswith(("lane_f32", "lane_su2_f32"))
+               else "fp64_dfma_tflops" if kernel.startswith(("lane_small", "lane_su2"))
+               else "fp64_dmma_tflops")
         return peaks[key] * 1e12
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
