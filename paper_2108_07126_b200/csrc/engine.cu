@@ -929,10 +929,46 @@ int f32_run(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_t 
   return SP_OK;
 }
 
+// D = 2: one thread per lane, everything in registers (lane_f32_reg2_kernel)
+int f32_run_reg2(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_t st,
+                 int* lanes_out) {
+  const size_t smem = (size_t)job.n_terms * 4 * sizeof(float2);
+  if (smem > 48 * 1024)
+    CUDA_TRY(ctx, cudaFuncSetAttribute(lane_f32_reg2_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_f32_reg2_kernel, F32_THREADS, smem);
+  occ = std::max(occ, 1);
+  // one wave of resident lanes, at least 16 slices per lane
+  const int64_t cap = (int64_t)ctx->sms * occ * F32_THREADS;
+  const int64_t want = std::max<int64_t>(1024, (job.n_slices + 15) / 16);
+  const int lanes = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(cap, want),
+                                                                 job.n_slices));
+  int rc = ensure(ctx, ctx->lanes, (size_t)lanes * 4 * sizeof(double2));
+  if (rc) return rc;
+  const int grid = (lanes + F32_THREADS - 1) / F32_THREADS;
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, st));
+  lane_f32_reg2_kernel<<<grid, F32_THREADS, smem, st>>>(job, (const double2*)ctx->terms.p, lanes,
+                                                         (double2*)ctx->lanes.p, prefix_out);
+  CUDA_TRY(ctx, cudaGetLastError());
+  if (ctx->prof) CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, st));
+  *lanes_out = lanes;
+  return SP_OK;
+}
+
 int f32_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream_t st,
                const double2** prods, int* count) {
   int lanes = 0;
-  const int rc = ctx->D == 2 ? f32_run<2>(ctx, job, prefix_out, st, &lanes)
+  // D = 2: register lanes from 2^19 slices (1e7: 309 vs 380 us); below,
+  // the two-thread lanes give twice the threads for the same lane count
+  // (1e5: 25 vs 34 us).  SP_F32_REG2=0 / 1 forces either (A/B, tests)
+  static const int reg2_env = [] {
+    const char* e = getenv("SP_F32_REG2");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  const bool reg2 = reg2_env >= 0 ? reg2_env == 1 : job.n_slices >= (1 << 19);
+  const int rc = ctx->D == 2 ? (reg2 ? f32_run_reg2(ctx, job, prefix_out, st, &lanes)
+                                     : f32_run<2>(ctx, job, prefix_out, st, &lanes))
                  : ctx->D == 4 ? f32_run<4>(ctx, job, prefix_out, st, &lanes)
                                : f32_run<8>(ctx, job, prefix_out, st, &lanes);
   if (rc) return rc;

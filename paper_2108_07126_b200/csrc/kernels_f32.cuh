@@ -251,4 +251,164 @@ __global__ void __launch_bounds__(F32_THREADS) lane_f32_kernel(SliceJob job,
   }
 }
 
+// D = 2 with one thread per lane: the same per-column arithmetic as
+// lane_f32_kernel<2> (each column of U = p(X) e_c is computed by the
+// identical operation sequence, so results are bitwise those of the two-
+// thread form), with X, the Clenshaw iterates, U and V in registers — no
+// shared-memory round trips or warp barriers per slice.
+__global__ void __launch_bounds__(F32_THREADS, 2) lane_f32_reg2_kernel(SliceJob job,
+                                                                    const double2* __restrict__ terms,
+                                                                    int lanes,
+                                                                    double2* __restrict__ lane_out,
+                                                                    double2* __restrict__ prefix_out) {
+  constexpr int D = 2;
+  const int T = job.n_terms;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* sterm = reinterpret_cast<float2*>(smem_raw);  // T x 2 x 2, cast once per CTA
+  for (int e = threadIdx.x; e < T * D * D; e += blockDim.x) {
+    const double2 v = terms[e];
+    sterm[e] = make_float2((float)v.x, (float)v.y);
+  }
+  __syncthreads();
+  const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t s0 = 0, s1 = 0;
+  if (lane < lanes) lane_range(job.n_slices, lanes, lane, s0, s1);
+  float2 V[D][D];  // V[r][c]
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int c = 0; c < D; ++c) V[r][c] = make_float2(r == c ? 1.0f : 0.0f, 0.0f);
+  const float scale = (float)job.scale;
+  const float xs = (float)job.xspan;
+  const int m = job.m;
+  const bool phase_one = job.phase[0] == 1.0 && job.phase[1] == 0.0;
+  const float2 ph = make_float2((float)job.phase[0], (float)job.phase[1]);
+  for (int64_t s = s0; s < s1; ++s) {
+    // X = float(2 / span) * (scale * (T_0 + sum_t w_t T_t)), per column as
+    // the two-thread form forms it
+    float2 X[D][D];
+    {
+      float2 ctl[D][D];
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) ctl[r][c] = make_float2(0.0f, 0.0f);
+      for (int t = 1; t < T; ++t) {
+        const float w = (float)f32_weight(job, s, t, true);
+        const float2* Ht = sterm + (size_t)t * D * D;
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            const float2 h = Ht[r * D + c];
+            ctl[r][c].x = fmaf(w, h.x, ctl[r][c].x);
+            ctl[r][c].y = fmaf(w, h.y, ctl[r][c].y);
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const float2 g = sterm[r * D + c];
+          float2 v = make_float2((g.x + ctl[r][c].x) * scale, (g.y + ctl[r][c].y) * scale);
+          v.x *= xs;
+          v.y *= xs;
+          X[r][c] = v;
+        }
+    }
+    // U[:, c] = p(X) e_c for both columns
+    float2 U[D][D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      float2 d0[D], d1[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) d0[r] = d1[r] = make_float2(0.0f, 0.0f);
+      bool first = true;
+      for (int k = m; k >= 1; k -= 2) {
+        const float2 ak = make_float2((float)job.coef[2 * k], (float)job.coef[2 * k + 1]);
+        float2 acc[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) acc[r] = make_float2(0.0f, 0.0f);
+        if (!first) {
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            const float2 b = d0[q];
+#pragma unroll
+            for (int r = 0; r < D; ++r) cfma32(acc[r], X[r][q], b);
+          }
+        }
+        first = false;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          float2 v = make_float2(-d1[r].x + 2.0f * acc[r].x, -d1[r].y + 2.0f * acc[r].y);
+          if (r == c) {
+            v.x += ak.x;
+            v.y += ak.y;
+          }
+          d1[r] = v;
+        }
+        const bool last = k == 1;
+        const float cc = last ? 2.0f : 1.0f;
+        const int k2 = last ? 0 : k - 1;
+        const float2 ap = make_float2((float)job.coef[2 * k2], (float)job.coef[2 * k2 + 1]);
+#pragma unroll
+        for (int r = 0; r < D; ++r) acc[r] = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          const float2 b = d1[q];
+#pragma unroll
+          for (int r = 0; r < D; ++r) cfma32(acc[r], X[r][q], b);
+        }
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          float2 v =
+              make_float2(-cc * d0[r].x + 2.0f * acc[r].x, -cc * d0[r].y + 2.0f * acc[r].y);
+          if (r == c) {
+            v.x += ap.x;
+            v.y += ap.y;
+          }
+          d0[r] = v;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        float2 u = d0[r];
+        if (!phase_one) u = make_float2(u.x * ph.x - u.y * ph.y, u.x * ph.y + u.y * ph.x);
+        U[r][c] = u;
+      }
+    }
+    // V[:, c] <- U V[:, c]
+    float2 nv[D][D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+#pragma unroll
+      for (int r = 0; r < D; ++r) nv[r][c] = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        const float2 b = V[q][c];
+#pragma unroll
+        for (int r = 0; r < D; ++r) cfma32(nv[r][c], U[r][q], b);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) V[r][c] = nv[r][c];
+    if (prefix_out) {
+      double2* o = prefix_out + (size_t)s * D * D;
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) o[r * D + c] = make_double2(V[r][c].x, V[r][c].y);
+    }
+  }
+  if (lane < lanes) {
+    double2* o = lane_out + (size_t)lane * D * D;
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) o[r * D + c] = make_double2(V[r][c].x, V[r][c].y);
+  }
+}
+
 }  // namespace sp

@@ -352,3 +352,29 @@ def test_more_than_2_31_slices_device_resident():
     del d_amps
     torch.cuda.empty_cache()
     ctx.close()
+
+
+def test_complex64_d2_register_lanes_match_the_two_thread_lanes():
+    """lane_f32_reg2_kernel (one thread per d = 2 lane, registers only) runs
+    the same per-column float32 operation sequence as the two-thread
+    lane_f32_kernel<2>: bitwise-identical lane products (SP_F32_REG2=0 in a
+    subprocess selects the two-thread form)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import numpy as np, sys; sys.path[:0] = ['tests/golden', '.'];"
+            "from cases import random_inputs; import paper_2108_07126_b200 as sp;"
+            "h0, hs, v, dt = random_inputs(2, 2, 40000, 9); ctx = sp.create('fp32');"
+            "ctx.set_hamiltonian(sp.ControlSystem(h0, hs));"
+            "u = ctx.equiprop(sp.ControlAmplitudes(v, dt), reduction='sequential').u;"
+            "print(ctx.last_timing()['kernel']); np.save(sys.argv[1], u)")
+    outs = []
+    for flag in ("1", "0"):
+        out = os.path.join(tempfile.mkdtemp(), "u.npy")
+        r = subprocess.run([sys.executable, "-c", code, out], cwd=root, capture_output=True,
+                           text=True, timeout=300, env=dict(os.environ, SP_F32_REG2=flag))
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
