@@ -70,6 +70,8 @@ def main():
     ap.add_argument("--dims", default=",".join(map(str, DIMS)))
     ap.add_argument("--precisions", default="fp64,fp32")
     ap.add_argument("--qubit", type=int, default=1, help="add the driven-qubit d = 2 series")
+    ap.add_argument("--modes", default="midpoint,simpson,magnus",
+                    help="slicing modes (three-point modes: fp64 rows)")
     args = ap.parse_args()
     import torch
 
@@ -89,34 +91,45 @@ def main():
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     fh = open(args.out, "w")
     nmax = max(SLICES)
-    for prec in args.precisions.split(","):
+    combos = [(p, "midpoint") for p in args.precisions.split(",")]
+    combos += [("fp64", m) for m in args.modes.split(",") if m and m != "midpoint"]
+    for prec, mode in combos:
         bits = 64 if prec == "fp64" else 32
+        three = mode != "midpoint"
         for d in map(int, args.dims.split(",")):
             rng = np.random.default_rng(SEED)
             h0 = unit_hermitian(rng, d)
             hs = [unit_hermitian(rng, d) for _ in range(N_CTRL)]
-            dt = 0.5 / (N_CTRL + 1.0)
-            values = rng.uniform(-1.0, 1.0, (nmax, N_CTRL))
+            dt = 0.5 / (N_CTRL + 1.0) / (2.0 if three else 1.0)
+            values = rng.uniform(-1.0, 1.0, ((2 * nmax + 1) if three else nmax, N_CTRL))
             ctx = sp.create(prec)
-            ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+            ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                                quadrature=None if mode == "magnus" else mode)
             ctx.set_profiling(True)
             plan = ctx.plan_for(dt)
-            F = canonical_flops(d, plan.m_max, N_CTRL + 1)
+            n_terms = 1 + 2 * N_CTRL + N_CTRL * (N_CTRL - 1) // 2 if mode == "magnus" \
+                else N_CTRL + 1
+            F = canonical_flops(d, plan.m_max, n_terms)
             d_amps = torch.from_numpy(values).to(dev)
             out = torch.empty((d, d), dtype=torch.complex128 if bits == 64 else torch.complex64,
                               device=dev)
             rate_est = None
-            cpu, cpu_n, cpu_kind = cpu_rate(h0, hs, values, dt, bits, args.cpu_s)
+            if three:  # the CPU column is the midpoint reference's
+                cpu, cpu_n, cpu_kind = None, 0, "n/a (three-point row)"
+            else:
+                cpu, cpu_n, cpu_kind = cpu_rate(h0, hs, values, dt, bits, args.cpu_s)
             for n in SLICES:
                 if rate_est is not None and n / rate_est > args.cap_s:
-                    rec = {"precision": prec, "dim": d, "slices": n, "skipped":
+                    rec = {"precision": prec, "dim": d, "slices": n, "mode": mode, "skipped":
                            f"estimated {n / rate_est:.0f} s > cap {args.cap_s} s"}
                     print(json.dumps(rec), flush=True)
                     fh.write(json.dumps(rec) + "\n")
                     continue
 
+                pts = 2 * n + 1 if three else n
+
                 def step():
-                    ctx.equiprop_device_ptr(d_amps.data_ptr(), n, N_CTRL, dt, out.data_ptr(),
+                    ctx.equiprop_device_ptr(d_amps.data_ptr(), pts, N_CTRL, dt, out.data_ptr(),
                                             stream=stream.cuda_stream, plan=plan)
                 step()
                 torch.cuda.synchronize(dev)
@@ -137,7 +150,7 @@ def main():
                 rate = n / (step_ms / 1e3)
                 rate_est = rate
                 kms = statistics.median(kern)
-                rec = {"precision": prec, "dim": d, "slices": n, "m": plan.m_max,
+                rec = {"precision": prec, "dim": d, "slices": n, "mode": mode, "m": plan.m_max,
                        "slices_per_s": rate, "ms_per_step": step_ms,
                        "kernel": t["kernel"], "kernel_ms": kms, "launches": t["launches"],
                        "canonical_tflops": n * F / (step_ms / 1e3) / 1e12,
@@ -146,7 +159,7 @@ def main():
                        "series": ctx.last_algorithm(), "lanes": ctx.last_lanes(),
                        "cpu_slices_per_s": cpu, "cpu_sample_slices": cpu_n,
                        "cpu_kind": cpu_kind,
-                       "gpu_over_cpu": rate / cpu}
+                       "gpu_over_cpu": rate / cpu if cpu else None}
                 print(json.dumps(rec), flush=True)
                 fh.write(json.dumps(rec) + "\n")
                 fh.flush()
