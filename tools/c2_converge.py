@@ -43,8 +43,15 @@ REF = {
 RUNS = {"midpoint c128": dict(magnus=False, quadrature="midpoint", precision="fp64"),
         "simpson c128": dict(magnus=False, quadrature="simpson", precision="fp64"),
         "magnus c128": dict(magnus=True, quadrature=None, precision="fp64"),
-        "magnus c64": dict(magnus=True, quadrature=None, precision="fp32")}
-BANDS = {"midpoint c128": (1.9, 2.2), "simpson c128": (1.9, 2.2), "magnus c128": (3.7, 4.3)}
+        "magnus c64": dict(magnus=True, quadrature=None, precision="fp32"),
+        # extensions (no reference rows): 4th-order Gauss-Legendre Magnus and
+        # the 2-node average, same sample counts (coerced even)
+        "gauss-legendre magnus c128": dict(magnus=True, quadrature="gauss-legendre",
+                                           precision="fp64"),
+        "gauss-legendre average c128": dict(magnus=False, quadrature="gauss-legendre",
+                                            precision="fp64")}
+BANDS = {"midpoint c128": (1.9, 2.2), "simpson c128": (1.9, 2.2), "magnus c128": (3.7, 4.3),
+         "gauss-legendre magnus c128": (3.7, 4.3), "gauss-legendre average c128": (1.9, 2.2)}
 
 
 def main():
@@ -63,11 +70,15 @@ def main():
         err = [e for _, e in rows]
         out += [f"## {name}  ({sec:.1f} s for the whole sweep)", "",
                 "| pts | B200 error | reference error | ratio |", "|---|---|---|---|"]
-        for p, e, r in zip(pts, err, REF[name]):
+        ref_rows = REF.get(name, REF["magnus c128"] if "magnus" in name else REF["midpoint c128"])
+        if name not in REF:
+            out[-1:] = ["| pts | B200 error | reference error (Simpson-Magnus / midpoint, "
+                        "nearest pts) | ratio |", "|---|---|---|---|"]
+        for p, e, r in zip(pts, err, ref_rows):
             out.append(f"| {p} | {e:.6e} | {r:.6e} | {e / r:.4f} |")
         if name in BANDS:
             order, (lo, hi) = fit_convergence_order(pts, err)
-            ref_order, _ = fit_convergence_order(pts, REF[name])
+            ref_order, _ = fit_convergence_order(pts, ref_rows)
             band = BANDS[name]
             ok = band[0] <= order <= band[1]
             out += ["", f"fitted order {order:.4f} over pts {lo}..{hi} (reference {ref_order:.4f}; "
