@@ -997,7 +997,7 @@ bool su2_applies(const sp_ctx* ctx, const SliceJob& job) {
 }
 
 int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_out,
-               const double2** prods, int* count) {
+               const double2** prods, int* count, double2* prefix_out = nullptr) {
   Su2Job sj;
   std::memset(&sj, 0, sizeof(sj));
   sj.amps = job.amps;
@@ -1014,6 +1014,7 @@ int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_ou
   }
   for (int k = 0; k <= job.m; ++k) sj.cr[k] = job.coef[2 * k + (k & 1)];
   sj.viol = job.viol;
+  sj.viol_epoch = job.viol_epoch;
   sj.out = fused_out;
   sj.to_fp32 = out32(ctx) ? 1 : 0;
   sj.arith32 = ctx->bits == 32 ? 1 : 0;
@@ -1028,12 +1029,22 @@ int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_ou
   }();
   int tpb_max = su2_max_block(sj);
   if (tpb_env >= 32) tpb_max = std::min(tpb_max, tpb_env & ~31);
-  const int64_t want = std::max<int64_t>(1, (job.n_slices + spt - 1) / spt);
+  // (lane mode: >= 16 slices per lane, the two-level scan of the lane
+  // products sizes its groups for that)
+  const int spt_eff = fused_out ? spt : std::max(spt, 16);
+  const int64_t want = std::max<int64_t>(1, (job.n_slices + spt_eff - 1) / spt_eff);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->sms, (want + 31) / 32));
   const int64_t per = (want + grid - 1) / grid;
   const int block = (int)std::min<int64_t>(tpb_max, ((per + 31) / 32) * 32);
-  int rc = ensure(ctx, ctx->lanes, (size_t)grid * 4 * sizeof(double));
+  const bool lane_mode = fused_out == nullptr;
+  int rc = ensure(ctx, ctx->lanes, lane_mode ? (size_t)grid * block * 4 * sizeof(double2)
+                                             : (size_t)grid * 4 * sizeof(double));
   if (rc) return rc;
+  if (lane_mode) {  // lane products, per-slice running products, initial products
+    sj.lane_out = ctx->lanes.p;
+    sj.prefix_out = prefix_out;
+    sj.vinit = job.vinit;
+  }
   sj.cta_out = ctx->lanes.p;
   if (!ctx->tailctr.p) {
     rc = ensure(ctx, ctx->tailctr, sizeof(unsigned));
@@ -1071,7 +1082,7 @@ int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_ou
   ctx->last_gemms = job.m;
   ctx->last_lanes = grid * block;
   *prods = (const double2*)ctx->lanes.p;
-  *count = grid;
+  *count = lane_mode ? grid * block : grid;
   return SP_OK;
 }
 
@@ -1086,6 +1097,10 @@ int run_lanes(sp_ctx* ctx, const SliceJob& job, bool cta_reduce, double2* prefix
   if (ctx->fam == FAM_S2 && fused_out && cta_reduce && !prefix_out && !job.vinit &&
       su2_applies(ctx, job))
     return su2_launch(ctx, job, st, fused_out, prods, count);
+  // lane mode (sequential reduction, the d = 2 two-pass equiprop_all): the
+  // su(2) lanes write lane products / running products in the plain layout
+  if (ctx->fam == FAM_S2 && !cta_reduce && ctx->bits == 64 && su2_applies(ctx, job))
+    return su2_launch(ctx, job, st, nullptr, prods, count, prefix_out);
   if (f32_path(ctx)) return f32_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_T8) return d8_launch(ctx, job, prefix_out, st, prods, count);
   if (ctx->fam == FAM_S2 || ctx->fam == FAM_S4) {

@@ -69,6 +69,7 @@ struct Su2Job {
   double tz[SU2_MAX_TERMS][3];      // per term: 2X factor x (H00, Re H01, Im H01)
   double cr[SP_MAX_ORDER + 1];      // nonzero component of a_k: Re (k even), Im (k odd)
   unsigned long long* viol;         // violation slots (epoch scheme of SliceJob), or null
+  int viol_epoch;                   // 1: fused call (epoch slot), 0: slot 2
   unsigned* ctr;                    // arrival counter (zero between launches)
   void* cta_out;                    // gridDim x 4 doubles: CTA products
   void* out;                        // 2 x 2 result (complex128, or complex64 if to_fp32)
@@ -77,6 +78,13 @@ struct Su2Job {
   // phase timestamps (tools only, SP_SU2_PROF=1): [2k] = min, [2k+1] = max
   // over CTAs of %globaltimer at phase k; null = off
   unsigned long long* prof;
+  // lane mode (sequential reductions, equiprop_all): no CTA tree / tail;
+  // lane_out[lane] = the lane's 2 x 2 product (complex128), prefix_out[s] =
+  // the running product after slice s, vinit[lane] = the lane's initial
+  // product (null: identity); all complex128 2 x 2 row-major
+  void* lane_out;
+  void* prefix_out;
+  const void* vinit;
 };
 // launch lane_su2_kernel (su2.cu); grid x block threads are the lanes
 cudaError_t su2_run(const Su2Job& job, int grid, int block, cudaStream_t st);

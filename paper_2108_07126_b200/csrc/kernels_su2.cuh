@@ -106,6 +106,34 @@ __device__ __forceinline__ void quat_warp_product(QuatT<R>& q) {
   for (int k = 1; k < 32; k <<= 1) q = quat_mul(quat_shfl_down(q, k), q);
 }
 
+// lane mode: the running product's initial value and per-slice output
+template <class R>
+__device__ __forceinline__ QuatT<R> su2_vinit(const Su2Job& job, int64_t lane) {
+  if (job.vinit == nullptr) return quat_identity<R>();
+  const double2* e = reinterpret_cast<const double2*>(job.vinit) + 4 * lane;
+  const double2 a = e[0], b = e[1];  // row 0: (a, b); row 1 is (-conj b, conj a)
+  return QuatT<R>{(R)a.x, (R)a.y, (R)b.x, (R)b.y};
+}
+template <class R>
+__device__ __forceinline__ void su2_store(void* base, int64_t idx, const QuatT<R>& q) {
+  // two 256-bit stores (sm_100 STG.256) per 64-byte 2 x 2 complex128 matrix
+  double* o = reinterpret_cast<double*>(base) + 8 * idx;
+  if (reinterpret_cast<uintptr_t>(o) & 31u) {  // caller's buffer not 32-byte aligned
+    double2* q2 = reinterpret_cast<double2*>(o);
+    q2[0] = make_double2(q.ar, q.ai);
+    q2[1] = make_double2(q.br, q.bi);
+    q2[2] = make_double2(-(double)q.br, q.bi);
+    q2[3] = make_double2(q.ar, -(double)q.ai);
+    return;
+  }
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o), "d"((double)q.ar),
+               "d"((double)q.ai), "d"((double)q.br), "d"((double)q.bi)
+               : "memory");
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o + 4), "d"(-(double)q.br),
+               "d"((double)q.bi), "d"((double)q.ar), "d"(-(double)q.ai)
+               : "memory");
+}
+
 // |v| <= 1 fails (also for NaN): accumulated without a branch
 __device__ __forceinline__ bool amp_bad(double v) { return !(fabs(v) <= 1.0); }
 
@@ -227,13 +255,19 @@ __device__ __forceinline__ void su2_slice(const Su2Job& job, int m, const double
 // After the lane loops: the lane's first amplitude offender (rare path; rows
 // [r0, rl] of the table), the ordered CTA product, the arrival ticket and, in
 // the last CTA, the ordered product of the CTA products and the d x d result.
-template <class R, int NCC>
+template <class R, int NCC, bool PFX = false>
 __device__ __forceinline__ void su2_finish(const Su2Job& job, QuatT<R> V, bool bad, int64_t r0,
                                            int64_t rl) {
   if (bad && job.viol) {
     const unsigned long long v = su2_first_bad(job.amps, r0, rl, NCC);
-    unsigned long long* slot = job.viol + (__ldcg(job.viol + 3) & 1ull);
+    // fused calls: the epoch slot (SliceJob::viol); multi-launch calls: slot 2
+    unsigned long long* slot =
+        job.viol_epoch ? job.viol + (__ldcg(job.viol + 3) & 1ull) : job.viol + 2;
     atomicMin(slot, v);
+  }
+  if (PFX && job.lane_out != nullptr) {  // lane mode: the lane product, no tree
+    su2_store(job.lane_out, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, V);
+    return;
   }
   // ---- ordered products: warps, then the CTA's warps (warp 0)
   __shared__ QuatT<R> wq[32];
@@ -310,7 +344,7 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, QuatT<R> V, bool b
 // [lane n / lanes, (lane + 1) n / lanes); the rows stream through a
 // per-thread cp.async ring in shared memory.
 // ---------------------------------------------------------------------------
-template <int MODE, int NCC, int MC, class R = double>
+template <int MODE, int NCC, int MC, class R = double, bool PFX = false>
 __global__ void __launch_bounds__(Su2Shape<MODE, NCC, R>::TPB, 1)
     lane_su2_kernel(const Su2Job job) {
   using S = Su2Shape<MODE, NCC, R>;
@@ -323,7 +357,9 @@ __global__ void __launch_bounds__(Su2Shape<MODE, NCC, R>::TPB, 1)
   const int64_t s1 = ((int64_t)lane + 1) * job.n_slices / lanes;
   const int cnt = (int)(s1 - s0);
 
-  QuatT<R> V = quat_identity<R>();
+  // PFX: lane mode (initial products, per-slice running products, lane
+  // products instead of the fused tail)
+  QuatT<R> V = PFX ? su2_vinit<R>(job, lane) : quat_identity<R>();
   bool bad = false;
   // first unit of this lane: row s0 (midpoint) or rows 2 s0 + 1, 2 s0 + 2
   const unsigned char* unit0 = reinterpret_cast<const unsigned char*>(
@@ -375,10 +411,11 @@ __global__ void __launch_bounds__(Su2Shape<MODE, NCC, R>::TPB, 1)
 #pragma unroll
         for (int q = 0; q < K; ++q) bad |= amp_bad(cur[q]);
         su2_slice<R, MODE, NCC, MC>(job, m, cur, r1, V);
+        if (PFX && job.prefix_out != nullptr) su2_store(job.prefix_out, s0 + k0 + j, V);
       }
     }
   }
-  su2_finish<R, NCC>(job, V, bad, MODE == SP_MODE_MIDPOINT ? s0 : 2 * s0,
+  su2_finish<R, NCC, PFX>(job, V, bad, MODE == SP_MODE_MIDPOINT ? s0 : 2 * s0,
                   MODE == SP_MODE_MIDPOINT ? s1 - 1 : 2 * s1);
 }
 
@@ -432,7 +469,7 @@ __device__ __forceinline__ void su2_tma_2d(void* dst, const void* tmap, int x, i
       : "memory");
 }
 
-template <int NCC, int MC, int C, class R = double>
+template <int NCC, int MC, int C, class R = double, bool PFX = false>
 __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
     lane_su2_tma_kernel(const Su2Job job, const __grid_constant__ CUtensorMap tmap,
                         const int64_t L) {
@@ -474,7 +511,7 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
   }
   __syncwarp();
 
-  QuatT<R> V = quat_identity<R>();
+  QuatT<R> V = PFX ? su2_vinit<R>(job, lane) : quat_identity<R>();
   bool bad = false;
   double r1[NCC];
   const int sw = LROWB == 128 ? (ln & 7) : ((ln >> 1) & 3);  // swizzle of this lane's row
@@ -504,8 +541,16 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
         for (int q = 0; q < NCC; ++q) bad |= amp_bad(cur[q]);
         U[k] = su2_u<R, SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1);
       }
+      if (!PFX || job.prefix_out == nullptr) {
 #pragma unroll
-      for (int k = 0; k < C; k += 2) V = quat_mul(quat_mul(U[k + 1], U[k]), V);
+        for (int k = 0; k < C; k += 2) V = quat_mul(quat_mul(U[k + 1], U[k]), V);
+      } else {  // every slice's running product is written: one at a time
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          V = quat_mul(U[k], V);
+          su2_store(job.prefix_out, s0 + r * C + k, V);
+        }
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < C; ++k) {
@@ -521,6 +566,7 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
 #pragma unroll
           for (int q = 0; q < NCC; ++q) bad |= amp_bad(cur[q]);
           su2_slice<R, SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1, V);
+          if (PFX && job.prefix_out != nullptr) su2_store(job.prefix_out, s0 + kk, V);
         }
       }
     }
@@ -532,7 +578,7 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
       su2_tma_2d(ring + s * STAGE, &tmap, (r + NST) * C * NCC, (int)wlane0, wb + s);
     }
   }
-  su2_finish<R, NCC>(job, V, bad, s0, s1 - 1);
+  su2_finish<R, NCC, PFX>(job, V, bad, s0, s1 - 1);
 }
 
 }  // namespace sp

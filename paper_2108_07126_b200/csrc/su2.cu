@@ -28,22 +28,22 @@ struct Su2Kernel {
   int rows = 0;       // TMA: rows per lane per round (C)
 };
 
-template <int MODE, int NCC, class R>
+template <int MODE, int NCC, class R, bool PFX>
 Su2Kernel su2_pick(int m) {
   using S = Su2Shape<MODE, NCC, R>;
   Su2Kernel k;
   k.smem = S::SMEM_PER_THREAD * S::TPB;
   k.max_block = S::TPB;
   switch (m) {
-    case 3: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 3, R>; break;
-    case 5: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 5, R>; break;
-    case 7: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 7, R>; break;
-    default: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 0, R>;
+    case 3: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 3, R, PFX>; break;
+    case 5: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 5, R, PFX>; break;
+    case 7: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 7, R, PFX>; break;
+    default: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 0, R, PFX>;
   }
   return k;
 }
 
-template <int NCC, int C, class R>
+template <int NCC, int C, class R, bool PFX>
 Su2Kernel su2_pick_tma(int m) {
   using G = Su2Tma<NCC, C>;
   Su2Kernel k;
@@ -52,21 +52,21 @@ Su2Kernel su2_pick_tma(int m) {
   k.tma = true;
   k.rows = C;
   switch (m) {
-    case 3: k.fn = (const void*)lane_su2_tma_kernel<NCC, 3, C, R>; break;
-    case 5: k.fn = (const void*)lane_su2_tma_kernel<NCC, 5, C, R>; break;
-    case 7: k.fn = (const void*)lane_su2_tma_kernel<NCC, 7, C, R>; break;
-    default: k.fn = (const void*)lane_su2_tma_kernel<NCC, 0, C, R>;
+    case 3: k.fn = (const void*)lane_su2_tma_kernel<NCC, 3, C, R, PFX>; break;
+    case 5: k.fn = (const void*)lane_su2_tma_kernel<NCC, 5, C, R, PFX>; break;
+    case 7: k.fn = (const void*)lane_su2_tma_kernel<NCC, 7, C, R, PFX>; break;
+    default: k.fn = (const void*)lane_su2_tma_kernel<NCC, 0, C, R, PFX>;
   }
   return k;
 }
 
-template <int MODE, class R>
+template <int MODE, class R, bool PFX>
 Su2Kernel su2_pick_n(int n_ctrl, int m) {
   switch (n_ctrl) {
-    case 1: return su2_pick<MODE, 1, R>(m);
-    case 2: return su2_pick<MODE, 2, R>(m);
-    case 3: return su2_pick<MODE, 3, R>(m);
-    case 4: return su2_pick<MODE, 4, R>(m);
+    case 1: return su2_pick<MODE, 1, R, PFX>(m);
+    case 2: return su2_pick<MODE, 2, R, PFX>(m);
+    case 3: return su2_pick<MODE, 3, R, PFX>(m);
+    case 4: return su2_pick<MODE, 4, R, PFX>(m);
   }
   return {};
 }
@@ -76,24 +76,27 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-template <class R>
+template <class R, bool PFX>
 Su2Kernel su2_kernel_for_t(const Su2Job& job) {
   static const int use_tma = env_int("SP_SU2_TMA", 1);
   // 128-byte lane rows per round (measured: 64-byte rounds with 1024-thread
   // CTAs 1.4x slower at 1e7 slices)
   if (use_tma && job.mode == SP_MODE_MIDPOINT && (job.n_ctrl == 2 || job.n_ctrl == 4))
-    return job.n_ctrl == 2 ? su2_pick_tma<2, 8, R>(job.m) : su2_pick_tma<4, 4, R>(job.m);
+    return job.n_ctrl == 2 ? su2_pick_tma<2, 8, R, PFX>(job.m)
+                           : su2_pick_tma<4, 4, R, PFX>(job.m);
   switch (job.mode) {
-    case SP_MODE_MIDPOINT: return su2_pick_n<SP_MODE_MIDPOINT, R>(job.n_ctrl, job.m);
-    case SP_MODE_SIMPSON: return su2_pick_n<SP_MODE_SIMPSON, R>(job.n_ctrl, job.m);
-    case SP_MODE_MAGNUS: return su2_pick_n<SP_MODE_MAGNUS, R>(job.n_ctrl, job.m);
+    case SP_MODE_MIDPOINT: return su2_pick_n<SP_MODE_MIDPOINT, R, PFX>(job.n_ctrl, job.m);
+    case SP_MODE_SIMPSON: return su2_pick_n<SP_MODE_SIMPSON, R, PFX>(job.n_ctrl, job.m);
+    case SP_MODE_MAGNUS: return su2_pick_n<SP_MODE_MAGNUS, R, PFX>(job.n_ctrl, job.m);
   }
   return {};
 }
 
-// complex64 contexts: the same kernels in float32 arithmetic
+// complex64 contexts: the same kernels in float32 arithmetic; lane mode
+// (lane_out set: sequential reduction / equiprop_all) is complex128 only
 Su2Kernel su2_kernel_for(const Su2Job& job) {
-  return job.arith32 ? su2_kernel_for_t<float>(job) : su2_kernel_for_t<double>(job);
+  if (job.lane_out) return su2_kernel_for_t<double, true>(job);
+  return job.arith32 ? su2_kernel_for_t<float, false>(job) : su2_kernel_for_t<double, false>(job);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {

@@ -238,3 +238,35 @@ def test_complex64_contexts_run_float32_su2(mode, slices):
     print(f"\n[su2 f32] {mode} slices={slices}: vs ref c64 {err:.3e} (tol {tol:.3e}), "
           f"vs c128 {err64:.3e} (reference c64 vs c128 {ref_err64:.3e})")
     assert err <= tol or err64 <= ref_err64
+
+
+@pytest.mark.parametrize("mode", ["midpoint", "simpson", "magnus"])
+@pytest.mark.parametrize("slices", [1, 37, 50_000])
+def test_lane_mode_sequential_and_cumulative(mode, slices):
+    """Lane mode of the su(2) kernels (reduction="sequential" and the d = 2
+    two-pass equiprop_all): lane products / per-slice running products in
+    the plain 2 x 2 layout, the ordered scan, pass 2 from the exclusive lane
+    prefixes.  Gates: sequential total and every cumulative entry vs the
+    oracle (max(1e-12, 4 eps_self)); the reference property u_all[-1] ==
+    sequential total, bit for bit (propagator.py:304-306)."""
+    pts = slices if mode == "midpoint" else 2 * slices + 1
+    h0, hs, values, dt = qubit_inputs(pts, mode)
+    with sp.create() as ctx:
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                            quadrature=None if mode == "magnus" else mode)
+        amps = sp.ControlAmplitudes(values, dt)
+        seq = ctx.equiprop(amps, reduction="sequential").u
+        assert ctx.last_timing()["kernel"] == "lane_su2_kernel"
+        cum = ctx.equiprop_all(amps)
+        assert ctx.last_timing()["kernel"] == "lane_su2_kernel"
+    u, _ = oracle.slice_propagators(h0, hs, values, dt, mode=mode)
+    ref, ref_seq = oracle.reduce_pairwise(u), oracle.reduce_sequential(u)
+    tol, _ = parity_tolerance(ref, ref_seq, "fp64")
+    assert rel_fro(seq, ref_seq) <= tol
+    assert np.array_equal(cum.u_all[-1], seq)
+    ref_all = oracle.cumulative(u)
+    step = max(1, slices // 200)
+    worst = max(rel_fro(cum.u_all[k], ref_all[k]) for k in range(0, slices, step))
+    print(f"\n[su2 lane mode] {mode} slices={slices}: seq {rel_fro(seq, ref_seq):.3e}, "
+          f"cumulative worst {worst:.3e} (tol {tol:.3e})")
+    assert worst <= tol

@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 
 CASES = [(2, 4_000_000), (4, 2_000_000), (8, 1_000_000), (16, 400_000), (32, 100_000),
-         (64, 20_000), (128, 4_000)]
+         (64, 20_000), (128, 4_000), ("qubit", 4_000_000)]
 
 
 def main():
@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
     cases = [c for c in CASES if not a.dims or str(c[0]) in a.dims.split(",")]
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
     import torch
 
     import paper_2108_07126_b200 as sp
@@ -41,11 +42,17 @@ def main():
     stream = torch.cuda.current_stream(dev)
     fh = open(a.out, "w")
     for d, n in cases:
-        rng = np.random.default_rng(20240911)
-        h0 = unit_hermitian(rng, d)
-        hs = [unit_hermitian(rng, d) for _ in range(2)]
-        values = rng.uniform(-1.0, 1.0, (n, 2))
-        dt = 0.5 / 3.0
+        label = d
+        if d == "qubit":  # the driven qubit: su(2) lanes in the two-pass form
+            from cases import qubit_inputs
+            h0, hs, values, dt = qubit_inputs(n, "midpoint")
+            d = 2
+        else:
+            rng = np.random.default_rng(20240911)
+            h0 = unit_hermitian(rng, d)
+            hs = [unit_hermitian(rng, d) for _ in range(2)]
+            values = rng.uniform(-1.0, 1.0, (n, 2))
+            dt = 0.5 / 3.0
         ctx = sp.create()
         ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
         plan = ctx.plan_for(dt)
@@ -68,7 +75,9 @@ def main():
         D = {2: 2, 4: 4, 8: 8}.get(d, d)
         out_b = n * d * d * 16
         est = out_b + 2 * n * D * D * 16
-        rec = {"dim": d, "slices": n, "ms": t * 1e3, "slices_per_s": n / t,
+        rec = {"dim": d, "system": "driven qubit" if label == "qubit" else "random",
+               "kernel": ctx.last_timing()["kernel"], "slices": n, "ms": t * 1e3,
+               "slices_per_s": n / t,
                "output_gb_s": out_b / t / 1e9, "traffic_est_gb_s": est / t / 1e9,
                "hbm_frac_output": out_b / t / 1e9 / hbm, "hbm_frac_traffic_est": est / t / 1e9 / hbm,
                "output_bytes": out_b, "hbm_gbs_peak": hbm}
