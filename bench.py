@@ -394,12 +394,13 @@ def roofline_for(t, local_slices, wl, m, kern_ms, peaks):
                            + " peak (tools/fp64_peak.cu, profiles/fp64_peak.json; "
                              "MEASURED_PEAKS.json has no FP64 entry)",
             "amplitude_bytes_per_launch": amp_bytes, "hbm_achieved_gbs": hbm_gbs,
-            "hbm_peak_gbs": hbm_peak, "hbm_frac": hbm_gbs / hbm_peak if hbm_peak else None}
+            "hbm_peak_gbs": hbm_peak, "hbm_frac": hbm_gbs / hbm_peak if hbm_peak else None,
+            "pipe_frac": executed / peak}
     if hbm_peak and hbm_gbs / hbm_peak > executed / peak:
         # the su(2) quaternion kernel executes ~34 FP64 instructions per 16-byte
         # amplitude row: its bound is the amplitude stream, not the FP64 pipe
         line.update({"bound": "hbm", "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": hbm_gbs / hbm_peak, "fp64_frac": executed / peak,
+                     "frac": hbm_gbs / hbm_peak,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy "
                                     "bandwidth)"})
     return line
@@ -636,10 +637,14 @@ def main():
         r = measure_gpu(args, name, rank, world, local_rank, dist, False)
         per_dim[name] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
                          "steps": r["steps"], "e2e": r["e2e"],
+                         "roofline_bound": r["roofline"]["bound"],
                          "roofline_frac": r["roofline"]["frac"],
+                         "roofline_achieved": r["roofline"]["achieved"],
+                         "roofline_peak": r["roofline"]["peak"],
+                         "roofline_unit": r["roofline"]["unit"],
+                         "pipe_frac": r["roofline"]["pipe_frac"],
                          "canonical_frac": r["roofline"]["canonical_frac"],
-                         "achieved_tflops": r["roofline"]["achieved"],
-                         "peak_tflops": r["roofline"]["peak"], "pipe": r["roofline"]["pipe"],
+                         "pipe": r["roofline"]["pipe"],
                          "kernel": r["roofline"]["kernel"], "workload": r["config"]["workload"],
                          "m": r["m"], "lanes": r["lanes"], "cuda_graph": r["config"]["cuda_graph"],
                          "cpu_baseline": r["cpu_sample"], "parity": r["parity"]}
