@@ -31,6 +31,7 @@ reference's own pairwise-vs-sequential noise eps_self beside it).
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -499,7 +500,10 @@ def measure_gpu(args, name, rank, world, local_rank, dist, headline):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(steps)]
     kernel_ms, launches = [], 0
-    with Clocks(local_rank) as clk:
+    # clocks are sampled (nvidia-smi every 200 ms) during the headline's
+    # timed region; the microsecond secondaries run without the poller
+    clk = Clocks(local_rank) if headline else None
+    with (clk if clk is not None else contextlib.nullcontext()):
         for k in range(steps):
             l2_flush(k)
             evs[k][0].record(stream)
@@ -566,7 +570,7 @@ def measure_gpu(args, name, rank, world, local_rank, dist, headline):
     assert np.all(np.isfinite(u))
     res = {"value": value, "ms_per_step": total_ms / steps, "steps": steps,
            "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
-           "clocks": clk.summary(), "m": plan.m_max, "lanes": lanes,
+           "clocks": clk.summary() if clk is not None else None, "m": plan.m_max, "lanes": lanes,
            "config": {"workload": wl["label"], "dim": d, "n_ctrl": wl["n_ctrl"],
                       "slices": n, "mode": mode, "m": plan.m_max,
                       "n_terms": n_terms_for(wl), "lanes": lanes,
