@@ -165,7 +165,7 @@ def main():
                 fh.flush()
             ctx.close()
             del d_amps
-        if args.qubit:
+        if args.qubit and mode == "midpoint":
             qubit_series(args, prec, sp, torch, dev, stream, fh, pipe_peak)
     fh.close()
 
