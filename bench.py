@@ -605,7 +605,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
-    ap.add_argument("--secondary", default="c4m,c3,c3s,c1,c1m",
+    # (the microsecond-scale qubit lines first, the seconds-long C4 magnus
+    # line last: each secondary measured before the next heats the board)
+    ap.add_argument("--secondary", default="c1,c1m,c3s,c3,c4m",
                     help="extra workloads reported under per_dim ('' for none)")
     ap.add_argument("--cpu-seconds", type=float, default=9.0)
     ap.add_argument("--no-cpu", action="store_true")
