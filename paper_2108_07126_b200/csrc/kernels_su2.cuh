@@ -105,6 +105,12 @@ __device__ __forceinline__ void quat_warp_product(QuatT<R>& q) {
 #pragma unroll
   for (int k = 1; k < 32; k <<= 1) q = quat_mul(quat_shfl_down(q, k), q);
 }
+// the same over the first `width` lanes only (lanes >= width hold identity):
+// log2(width) levels
+template <class R>
+__device__ __forceinline__ void quat_warp_product(QuatT<R>& q, int width) {
+  for (int k = 1; k < width; k <<= 1) q = quat_mul(quat_shfl_down(q, k), q);
+}
 
 // lane mode: the running product's initial value and per-slice output
 template <class R>
@@ -279,7 +285,7 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, QuatT<R> V, bool b
     __syncthreads();
     if (wp == 0) {
       q = ln < nw ? wq[ln] : quat_identity<R>();
-      quat_warp_product(q);
+      quat_warp_product(q, nw);  // only the levels the nw warp products need
     }
     __syncthreads();
   };
