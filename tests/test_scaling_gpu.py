@@ -124,3 +124,33 @@ def test_default_context_still_raises_and_within_capability_is_unchanged():
         bad[7, 0] = 1.5
         with pytest.raises(sp.AmplitudeBoundError, match="sample 7, control 0"):
             ctx.equiprop(sp.ControlAmplitudes(bad, 10.0))
+
+
+def test_cli_and_binding_expose_scaling(tmp_path):
+    """`propagate --scaling` and pysliceprop.Session(scaling=True) reach the
+    extension; without them the reference's StepTooLargeError (CLI exit 3)."""
+    import json
+    import subprocess
+    import sys
+    from paper_2108_07126_b200 import pysliceprop
+    rng = np.random.default_rng(8)
+    h0, h1 = unit_hermitian(rng, 4), unit_hermitian(rng, 4)
+    values = rng.uniform(-1, 1, (50, 1))
+    pairs = lambda m: np.stack([m.real, m.imag], axis=-1).tolist()
+    manifest = {"dim": 4, "drift": pairs(h0), "controls": [pairs(h1)], "dt": 6.0,
+                "amplitudes": {"pts": 50, "data": values.tolist()}}
+    path = tmp_path / "m.json"
+    path.write_text(json.dumps(manifest))
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__file__))
+    base = [sys.executable, "-m", "paper_2108_07126_b200", "propagate", str(path)]
+    r = subprocess.run(base, cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 3, r.stderr
+    r = subprocess.run(base + ["--scaling"], cwd=root, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert "squarings" in r.stderr
+    u_cli = np.array(json.loads(r.stdout)["u"])
+    with pysliceprop.Session(scaling=True) as s:
+        s.set_hamiltonian(h0, [h1])
+        u = s.equiprop(values, 6.0)
+    assert np.allclose(u_cli[..., 0] + 1j * u_cli[..., 1], u, rtol=0, atol=1e-12)
