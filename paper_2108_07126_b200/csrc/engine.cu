@@ -86,7 +86,13 @@ int ps_cost(int m, int s) {
 
 int ps_choose(int m) {
   // s <= 4: the power blocks T_1..T_{s-1} live in TMEM (4 blocks per
-  // thread); larger s never lowers the cost for m <= 25
+  // thread); larger s never lowers the cost for m <= 25.  SP_PS_S=<s>
+  // forces the split (A/B timing)
+  static const int s_env = [] {
+    const char* e = getenv("SP_PS_S");
+    return e ? atoi(e) : 0;
+  }();
+  if (s_env >= 2 && s_env <= 4 && (m + 1 + s_env - 1) / s_env >= 2) return s_env;
   int best = 0, cost = m;
   for (int s = 2; s <= 4; ++s) {
     const int r = (m + 1 + s - 1) / s;
