@@ -23,6 +23,12 @@
 
 namespace sp {
 
+__device__ __forceinline__ void st_global_v4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d)
+               : "memory");
+}
+
 
 // tile_mma3 with cross-step prefetch: a holds the kb = 0 fragments on entry;
 // on exit it holds the kb = 0 fragments of An (if An != nullptr)
@@ -91,7 +97,6 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   constexpr int D = C::D, WC = C::WC, MT = C::MT, NT = C::NT, NE = MT * NT * 4;
   constexpr int KB = C::KB;
   constexpr int KBC = WC / 4;                 // k-blocks of one column block
-  constexpr int CHUNK = C::S * KBC * 3 * 64;  // doubles of one column block (A layout)
   const SliceJob& job = pj.base;
   extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -114,18 +119,6 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int s = pj.s, r = pj.r;
   auto row_of = [&](int idx) { return 16 * (ms0 + idx / (NT * 4)) + g + 8 * ((idx & 3) >> 1); };
   auto col_of = [&](int idx) { return 8 * (nt0 + (idx / 4) % NT) + 2 * t4 + (idx & 1); };
-  // A-layout index of the q-th double of this CTA's column chunk
-  auto chunk_index = [&](int q) {
-    const int strip = q / (KBC * 192), rem = q % (KBC * 192);
-    const int kbl = rem / 192, rr = rem % 192;
-    return ((strip * KB + cb * KBC + kbl) * 3) * 64 + rr;
-  };
-  // position of own element e (plane p) inside the column chunk
-  auto chunk_pos = [&](int e, int p) {
-    const int rr = row_of(e), c = col_of(e);  // c: column within the block
-    return ((rr >> 4) * KBC + (c >> 2)) * 192 + p * 64 + (((rr & 7) << 2) | (c & 3)) * 2 +
-           ((rr >> 3) & 1);
-  };
 
   __shared__ uint32_t tmem_slot;
   if (warp == 0) tmem_alloc(&tmem_slot, C::TMEM_COLS);
@@ -252,20 +245,30 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
     }
   };
-  // stage own elements in chunk order (smem at off), then coalesced copy
-  auto publish = [&](double* dst, int off, const double(&vr)[NE], const double(&vi)[NE],
-                     double fr, double fi) {
+  // own elements straight from the accumulator fragments into the 3-plane A
+  // layout: a lane's (g, c), (g+8, c), (g, c+1), (g+8, c+1) for c = 2 t4
+  // are 4 consecutive doubles of one A block (one full 32-byte sector), so
+  // every store is a 256-bit st.global.v4.f64 and a warp instruction writes
+  // two whole 512-byte blocks — no staging buffer, no CTA barrier
+  auto publish = [&](double* dst, const double(&vr)[NE], const double(&vi)[NE], double fr,
+                     double fi) {
 #pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const double xr = fr * vr[e] - fi * vi[e], xi = fr * vi[e] + fi * vr[e];
-      smem[off + chunk_pos(e, 0)] = xr;
-      smem[off + chunk_pos(e, 1)] = xi;
-      smem[off + chunk_pos(e, 2)] = xr + xi;
-    }
-    __syncthreads();
-    for (int q = 2 * threadIdx.x; q < CHUNK; q += 2 * C::THREADS)
-      *reinterpret_cast<double2*>(dst + chunk_index(q)) =
-          *reinterpret_cast<const double2*>(&smem[off + q]);
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn) {
+        const int e0 = (i * NT + jn) * 4;
+        double xr[4], xi[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          xr[q] = fr * vr[e0 + q] - fi * vi[e0 + q];
+          xi[q] = fr * vi[e0 + q] + fi * vr[e0 + q];
+        }
+        const int c = col0 + 8 * (nt0 + jn) + 2 * t4;
+        double* o = dst + ((((ms0 + i) * KB + (c >> 2)) * 3) * 64 + (g * 4 + (c & 3)) * 2);
+        st_global_v4(o, xr[0], xr[2], xr[1], xr[3]);
+        st_global_v4(o + 64, xi[0], xi[2], xi[1], xi[3]);
+        st_global_v4(o + 128, xr[0] + xi[0], xr[2] + xi[2], xr[1] + xi[1], xr[3] + xi[3]);
+      }
   };
   auto write_B = [&](int off, const double(&vr)[NE], const double(&vi)[NE], double f) {
 #pragma unroll
@@ -366,14 +369,13 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         __syncthreads();
       }
     }
-    // 2y = 2 T_s: stage in the free buffer bo(pb^1) (T_{s-2}, already in
-    // TMEM; nobody reads it in the last power step)
+    // 2y = 2 T_s
     PH(1);
-    publish(gy, bo(pb ^ 1), accR, accI, 2.0, 0.0);
+    publish(gy, accR, accI, 2.0, 0.0);
     PH(2);
     // 2y published; the first Clenshaw B operand (own TMEM -> own smem) is
     // staged while the group's other CTAs arrive (the arrival's CTA barrier
-    // also ends every read of the publication staging buffer)
+    // also ends every warp's last power GEMM, which read bo(pb))
     garrive();
     int pc = 0;
     {
@@ -407,12 +409,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       }
     }
     PH(4);
-    // U (times the plan phase): stage in bo(pc^1) (b_2, consumed) and publish
-    __syncthreads();
-    publish(gu, bo(pc ^ 1), accR, accI, phase_one ? 1.0 : job.phase[0],
-            phase_one ? 0.0 : job.phase[1]);
-    // next slice's 2X (its buffer is dead since the powers phase) and T_1,
-    // into the U staging buffer once the copy-out has finished
+    // U (times the plan phase), straight from the accumulators
+    publish(gu, accR, accI, phase_one ? 1.0 : job.phase[0], phase_one ? 0.0 : job.phase[1]);
+    // next slice's 2X (its buffer is dead since the powers phase) and T_1
+    // into bo(pc^1) (b_2: assemble's barrier ends the owners' reads of it)
     PH(5);
     if (more) assemble(sl + 1, bo(pc ^ 1));
     tb = pc ^ 1;
