@@ -46,9 +46,16 @@ __host__ __device__ constexpr int xfrag3_index(int D, int r, int c, int plane) {
          ((r >> 3) & 1);
 }
 
+// 3-plane B-native layout: per 4-row k block, 8-column n tile and plane, 32
+// doubles in mma.sync B-fragment order (lane n*4 + k), with bit 2 of the
+// position flipped in its upper half (XOR swizzle: a warp's accumulator
+// scatter — rows g, columns 2 t4 + par — then spans all 16 bank pairs of a
+// block, 2 wavefronts instead of 4; the fragment loads read lane bswz(ln))
+__host__ __device__ constexpr int bswz(int x) { return x ^ (((x >> 4) & 1) << 2); }
+
 template <class C>
 __device__ __forceinline__ int bfrag3_index(int r, int n, int plane) {
-  return (((r >> 2) * C::NTC + (n >> 3)) * 3 + plane) * 32 + ((n & 7) << 2) + (r & 3);
+  return (((r >> 2) * C::NTC + (n >> 3)) * 3 + plane) * 32 + bswz(((n & 7) << 2) + (r & 3));
 }
 
 template <class C, bool AG>
@@ -81,7 +88,7 @@ __device__ __forceinline__ void tile_mma3(const double* __restrict__ Ag, int a_o
     double b[NT][3];
 #pragma unroll
     for (int jn = 0; jn < NT; ++jn) {
-      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 3) * 32 + ln;
+      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 3) * 32 + bswz(ln);
 #pragma unroll
       for (int p = 0; p < 3; ++p) b[jn][p] = smem[bi + 32 * p];
     }

@@ -60,7 +60,7 @@ __device__ __forceinline__ void tile_mma3_pf(const double* __restrict__ Ag,
     double b[NT][3];
 #pragma unroll
     for (int jn = 0; jn < NT; ++jn) {
-      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 3) * 32 + ln;
+      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 3) * 32 + bswz(ln);
 #pragma unroll
       for (int p = 0; p < 3; ++p) b[jn][p] = smem[bi + 32 * p];
     }
