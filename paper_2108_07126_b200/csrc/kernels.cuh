@@ -1149,9 +1149,16 @@ __device__ __forceinline__ void store_prefix(double2* base, int D, int64_t slice
   o[xfrag_index(D, r, c, 1)] = im;
 }
 
+// B-native layout: per 4-row k block, 8-column n tile and plane, 32 doubles
+// in mma.sync B-fragment order (lane n*4 + k), with bit 2 of the position
+// flipped in its upper half (XOR swizzle: a warp's accumulator scatter —
+// rows g, columns 2 t4 + par — then spans all 16 bank pairs of a block, 2
+// wavefronts instead of 4; the fragment loads read position bswz(ln))
+__host__ __device__ constexpr int bswz(int x) { return x ^ (((x >> 4) & 1) << 2); }
+
 template <class C>
 __device__ __forceinline__ int bfrag_index(int r, int n, int plane) {
-  return (((r >> 2) * C::NTC + (n >> 3)) * 2 + plane) * 32 + ((n & 7) << 2) + (r & 3);
+  return (((r >> 2) * C::NTC + (n >> 3)) * 2 + plane) * 32 + bswz(((n & 7) << 2) + (r & 3));
 }
 
 template <class C>

@@ -46,13 +46,7 @@ __host__ __device__ constexpr int xfrag3_index(int D, int r, int c, int plane) {
          ((r >> 3) & 1);
 }
 
-// 3-plane B-native layout: per 4-row k block, 8-column n tile and plane, 32
-// doubles in mma.sync B-fragment order (lane n*4 + k), with bit 2 of the
-// position flipped in its upper half (XOR swizzle: a warp's accumulator
-// scatter — rows g, columns 2 t4 + par — then spans all 16 bank pairs of a
-// block, 2 wavefronts instead of 4; the fragment loads read lane bswz(ln))
-__host__ __device__ constexpr int bswz(int x) { return x ^ (((x >> 4) & 1) << 2); }
-
+// 3-plane B-native layout (swizzled as bfrag_index, kernels.cuh)
 template <class C>
 __device__ __forceinline__ int bfrag3_index(int r, int n, int plane) {
   return (((r >> 2) * C::NTC + (n >> 3)) * 3 + plane) * 32 + bswz(((n & 7) << 2) + (r & 3));

@@ -39,7 +39,7 @@ __device__ __forceinline__ void tile_mma(const double* __restrict__ Ag, int a_of
     double bR[NT], bI[NT];
 #pragma unroll
     for (int jn = 0; jn < NT; ++jn) {
-      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 2) * 32 + ln;
+      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 2) * 32 + bswz(ln);
       bR[jn] = smem[bi];
       bI[jn] = smem[bi + 32];
     }
@@ -101,7 +101,7 @@ __device__ __forceinline__ void tile_mma_ra(const double2 (&aR)[C::KB],
     double bR[NT], bI[NT];
 #pragma unroll
     for (int jn = 0; jn < NT; ++jn) {
-      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 2) * 32 + ln;
+      const int bi = b_off + ((kb * C::NTC + nt0 + jn) * 2) * 32 + bswz(ln);
       bR[jn] = smem[bi];
       bI[jn] = smem[bi + 32];
     }
