@@ -1128,10 +1128,25 @@ struct TCCfg {
   static constexpr int THREADS = 32 * WPL * LPC;
   static constexpr int LANE_DBL = 2 * BDBL + (XS ? XDBL : 0) + WMAX;
   static constexpr size_t SMEM = (size_t)LANE_DBL * LPC * sizeof(double);
+  static constexpr bool ASW = false;  // smem A operands swizzled (aswz)
   static_assert(D == WC * GPL, "column blocks must tile D");
   static_assert((S / MT) * (NTC / NT) == WPL, "warp tiling must cover the block");
   static_assert(GPL == 1 || LPC == 1, "groups own one lane per CTA");
 };
+
+// 256-bit global store (sm_100: STG.E.ENL2.256); p 32-byte aligned
+__device__ __forceinline__ void st_global_v4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d)
+               : "memory");
+}
+
+// swizzled shared-memory copy of the A-native layout (lane_ps_kernel): the
+// 16-byte units of odd k blocks swap pairwise (bit 1 of the double offset),
+// so a warp's 16-byte accumulator stores — rows g / g+8 of columns 2 t4,
+// t4 = 0..3, spanning two k blocks — hit 8 distinct bank quads per phase;
+// the fragment loads stay one unit per lane.  Valid for an even k-block count.
+__host__ __device__ constexpr int aswz(int idx) { return idx ^ (((idx >> 7) & 1) << 1); }
 
 __host__ __device__ constexpr int xfrag_index(int D, int r, int c, int plane) {
   // element (r, c) of a D x D matrix in the A-native layout

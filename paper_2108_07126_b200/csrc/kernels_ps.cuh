@@ -47,6 +47,8 @@ struct PSCfg : TCCfg<D_, WC_, MT_, NT_, WPL_, LPC_, GPL_, XS_> {
                                                                    : 0;
   static constexpr int LANE_DBL = BASE_DBL + TSB * TBLK;
   static constexpr size_t SMEM = (size_t)LANE_DBL * LPC_ * sizeof(double);
+  static constexpr bool ASW = XS_;
+  static_assert(!ASW || B::KB % 2 == 0, "aswz needs an even k-block count");
 };
 
 struct PSJob {
@@ -148,21 +150,35 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       smem[off + bfrag_index<C>(rr, n, 1)] = f * vi[e];
     }
   };
-  // A-native write of own positions: smem (XS) or global (group families)
+  // A-native write of own positions: smem (XS) or global (group families).
+  // A lane's (g, c), (g+8, c), (g, c+1), (g+8, c+1), c = 2 t4, are 4
+  // consecutive doubles of one A block: two 16-byte stores per plane (smem,
+  // swizzled: conflict-free) or one 32-byte store (global)
   auto write_A = [&](double* gptr, int off, const double(&vr)[NE], const double(&vi)[NE],
                      double fr, double fi) {
 #pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const int rr = row_of(e), c = col0 + col_of(e);
-      const double xr = fr * vr[e] - fi * vi[e], xi = fr * vi[e] + fi * vr[e];
-      if constexpr (AG) {
-        gptr[xfrag_index(D, rr, c, 0)] = xr;
-        gptr[xfrag_index(D, rr, c, 1)] = xi;
-      } else {
-        smem[off + xfrag_index(D, rr, c, 0)] = xr;
-        smem[off + xfrag_index(D, rr, c, 1)] = xi;
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn) {
+        const int e0 = (i * NT + jn) * 4;
+        double xr[4], xi[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          xr[q] = fr * vr[e0 + q] - fi * vi[e0 + q];
+          xi[q] = fr * vi[e0 + q] + fi * vr[e0 + q];
+        }
+        const int c = col0 + 8 * (nt0 + jn) + 2 * t4;
+        const int base = (((ms0 + i) * (D >> 2) + (c >> 2)) * 2) * 64 + (g * 4 + (c & 3)) * 2;
+        if constexpr (AG) {
+          st_global_v4(gptr + base, xr[0], xr[2], xr[1], xr[3]);
+          st_global_v4(gptr + base + 64, xi[0], xi[2], xi[1], xi[3]);
+        } else {
+          *reinterpret_cast<double2*>(&smem[off + aswz(base)]) = make_double2(xr[0], xr[2]);
+          *reinterpret_cast<double2*>(&smem[off + aswz(base + 2)]) = make_double2(xr[1], xr[3]);
+          *reinterpret_cast<double2*>(&smem[off + aswz(base + 64)]) = make_double2(xi[0], xi[2]);
+          *reinterpret_cast<double2*>(&smem[off + aswz(base + 66)]) = make_double2(xi[1], xi[3]);
+        }
       }
-    }
   };
   // Q_j at own positions: alpha_{j,0} I + sum_{i>=1} alpha_{j,i} T_i
   auto load_Q = [&](int j, double(&qr)[NE], double(&qi)[NE]) {
@@ -267,7 +283,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           if constexpr (AG)
             *reinterpret_cast<double2*>(gx + idx[u]) = x[u];
           else
-            *reinterpret_cast<double2*>(&smem[ax_off + idx[u]]) = x[u];
+            *reinterpret_cast<double2*>(&smem[ax_off + aswz(idx[u])]) = x[u];
         }
       }
     }
@@ -281,8 +297,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       for (int e = 0; e < NE; ++e) {
         const int rr = row_of(e), c = col0 + col_of(e);
         const int i0 = xfrag_index(D, rr, c, 0), i1 = xfrag_index(D, rr, c, 1);
-        t1r[e] = 0.5 * (AG ? __ldcg(gx + i0) : smem[ax_off + i0]);
-        t1i[e] = 0.5 * (AG ? __ldcg(gx + i1) : smem[ax_off + i1]);
+        t1r[e] = 0.5 * (AG ? __ldcg(gx + i0) : smem[ax_off + aswz(i0)]);
+        t1i[e] = 0.5 * (AG ? __ldcg(gx + i1) : smem[ax_off + aswz(i1)]);
         tp_store(0, e, make_double2(t1r[e], t1i[e]));
       }
       write_B(bofs0, t1r, t1i, 1.0);

@@ -23,12 +23,6 @@
 
 namespace sp {
 
-__device__ __forceinline__ void st_global_v4(double* p, double a, double b, double c, double d) {
-  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
-               "d"(d)
-               : "memory");
-}
-
 
 // tile_mma3 with cross-step prefetch: a holds the kb = 0 fragments on entry;
 // on exit it holds the kb = 0 fragments of An (if An != nullptr)

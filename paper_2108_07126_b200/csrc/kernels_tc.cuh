@@ -23,8 +23,9 @@ __device__ __forceinline__ void tile_mma(const double* __restrict__ Ag, int a_of
       re = __ldcg(reinterpret_cast<const double2*>(Ag + idx));
       im = __ldcg(reinterpret_cast<const double2*>(Ag + idx + 64));
     } else {
-      re = *reinterpret_cast<const double2*>(&smem[a_off + idx]);
-      im = *reinterpret_cast<const double2*>(&smem[a_off + idx + 64]);
+      const int pi = C::ASW ? aswz(idx) : idx;
+      re = *reinterpret_cast<const double2*>(&smem[a_off + pi]);
+      im = *reinterpret_cast<const double2*>(&smem[a_off + pi + 64]);
     }
   };
   double2 aR[MT], aI[MT], nR[MT], nI[MT];
@@ -82,7 +83,8 @@ __device__ __forceinline__ void load_afrag_strip(int a_off, double2 (&aR)[C::KB]
   extern __shared__ __align__(16) double smem[];
 #pragma unroll
   for (int kb = 0; kb < C::KB; ++kb) {
-    const int idx = ((ms0 * C::KB + kb) * 2) * 64 + 2 * ln;
+    const int idx0 = ((ms0 * C::KB + kb) * 2) * 64 + 2 * ln;
+    const int idx = C::ASW ? aswz(idx0) : idx0;
     aR[kb] = *reinterpret_cast<const double2*>(&smem[a_off + idx]);
     aI[kb] = *reinterpret_cast<const double2*>(&smem[a_off + idx + 64]);
   }
