@@ -12,4 +12,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:lane_ps3g -c 1 -o gpurun_out/${P}_c4_full python tools/ncu_target.py --workload c4 --slices 2000 --repeat 1 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:lane_su2 -c 1 -o gpurun_out/${P}_c1m_full python tools/ncu_target.py --workload c1m --slices 1000000 --repeat 1 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:lane_ps3g -c 1 -o gpurun_out/${P}_d64_full python tools/env_ab_target.py 64 2 20000 > /dev/null 2>&1
+# summaries on the box; the .ncu-rep files stay there (gpurun copies back <= 64 MiB)
+python tools/ncu_summary.py full gpurun_out/${P}_c4_full.ncu-rep "# ncu --set full -k regex:lane_ps3g -c 1 tools/ncu_target.py --workload c4 --slices 2000" > gpurun_out/${P}_ncu_c4.txt 2>&1
+python tools/ncu_summary.py full gpurun_out/${P}_c1m_full.ncu-rep "# ncu --set full -k regex:lane_su2 -c 1 tools/ncu_target.py --workload c1m --slices 1000000" > gpurun_out/${P}_ncu_c1m.txt 2>&1
+python tools/ncu_summary.py full gpurun_out/${P}_d64_full.ncu-rep "# ncu --set full -k regex:lane_ps3g -c 1 tools/env_ab_target.py 64 2 20000" > gpurun_out/${P}_ncu_d64.txt 2>&1
+python tools/ncu_summary.py launches gpurun_out/${P}_launches_c4.csv "# ncu --metrics gpu__time_duration.sum bench.py --steps 1 --warmup 3 (C4 headline)" > gpurun_out/${P}_launches_c4.txt 2>&1
+rm -f gpurun_out/${P}_*.ncu-rep
 tail -3 gpurun_out/${P}_tests.log
