@@ -1141,6 +1141,20 @@ __device__ __forceinline__ void st_global_v4(double* p, double a, double b, doub
                : "memory");
 }
 
+// the same with an L2 cache-policy hint (createpolicy, e.g. evict_last for
+// exchange buffers that are rewritten every slice and must stay L2-resident)
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_global_v4_hint(double* p, double a, double b, double c,
+                                                  double d, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "d"(a),
+               "d"(b), "d"(c), "d"(d), "l"(pol)
+               : "memory");
+}
+
 // swizzled shared-memory copy of the A-native layout (lane_ps_kernel): the
 // 16-byte units of odd k blocks swap pairwise (bit 1 of the double offset),
 // so a warp's 16-byte accumulator stores — rows g / g+8 of columns 2 t4,

@@ -259,9 +259,11 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         }
         const int c = col0 + 8 * (nt0 + jn) + 2 * t4;
         double* o = dst + ((((ms0 + i) * KB + (c >> 2)) * 3) * 64 + (g * 4 + (c & 3)) * 2);
-        st_global_v4(o, xr[0], xr[2], xr[1], xr[3]);
-        st_global_v4(o + 64, xi[0], xi[2], xi[1], xi[3]);
-        st_global_v4(o + 128, xr[0] + xi[0], xr[2] + xi[2], xr[1] + xi[1], xr[3] + xi[3]);
+        const uint64_t pol = l2_policy_evict_last();
+        st_global_v4_hint(o, xr[0], xr[2], xr[1], xr[3], pol);
+        st_global_v4_hint(o + 64, xi[0], xi[2], xi[1], xi[3], pol);
+        st_global_v4_hint(o + 128, xr[0] + xi[0], xr[2] + xi[2], xr[1] + xi[1], xr[3] + xi[3],
+                          pol);
       }
   };
   auto write_B = [&](int off, const double(&vr)[NE], const double(&vi)[NE], double f) {
