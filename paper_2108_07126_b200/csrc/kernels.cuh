@@ -1202,13 +1202,19 @@ __device__ __forceinline__ void lane_sync() {
   }
 }
 
+// Release / acquire at gpu scope, cumulative through the CTA barriers: the
+// CTA's stores -> bar.sync -> red.release by thread 0 ... ld.acquire by the
+// waiting CTA's thread 0 -> bar.sync -> its loads (no full fences).
+__device__ __forceinline__ void red_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void group_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    while (ld_acquire_gpu(ctr) < target) __nanosleep(32);
-    __threadfence();
+    red_release_gpu(ctr, 1u);
+    while (ld_acquire_gpu(ctr) < target) {
+    }
   }
   __syncthreads();
 }
@@ -1218,15 +1224,12 @@ __device__ __forceinline__ void group_barrier(unsigned* ctr, unsigned target) {
 // reading theirs
 __device__ __forceinline__ void group_arrive(unsigned* ctr) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-  }
+  if (threadIdx.x == 0) red_release_gpu(ctr, 1u);
 }
 __device__ __forceinline__ void group_wait(unsigned* ctr, unsigned target) {
   if (threadIdx.x == 0) {
-    while (ld_acquire_gpu(ctr) < target) __nanosleep(32);
-    __threadfence();
+    while (ld_acquire_gpu(ctr) < target) {
+    }
   }
   __syncthreads();
 }
