@@ -73,4 +73,22 @@ ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
 res = ctx.equiprop(sp.ControlAmplitudes(v, 40 * dt))
 print("scaling squarings", res.plan["squarings"], flush=True)
 ctx.close()
+# late round 2: multi-slice lanes (>= 3 slices per lane on the production
+# grids) through the swizzled B / A layouts, the direct 256-bit publication
+# and the release / acquire group barriers — the cross-slice reuse of the
+# shared buffers and exchange buffers is what racecheck has to see
+for d, n, algos in ((16, 3600, ("ps", "clenshaw")), (32, 900, ("ps", "clenshaw")),
+                    (64, 444, ("ps3m", "ps")), (128, 111, ("ps3m",)), (256, 27, ("ps3m",))):
+    for algo in algos:
+        if NO_TMEM and algo == "ps3m":
+            continue
+        h0, hs, v, dt = random_inputs(d, 2, n, 11)
+        ctx = sp.create()
+        ctx.set_algorithm(algo)
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs))
+        u = ctx.equiprop(sp.ControlAmplitudes(v, dt)).u
+        print(f"multi-slice d={d} n={n} {algo}: {ctx.last_timing()['kernel']} lanes "
+              f"{ctx.last_lanes()} unitarity {np.abs(u.conj().T @ u - np.eye(d)).max():.2e}",
+              flush=True)
+        ctx.close()
 print("sanitize target done")
