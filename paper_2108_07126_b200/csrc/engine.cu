@@ -76,7 +76,9 @@ using P3_512 = PS3Cfg<512, 8, 4, 1, 8, 1, 64, false>;
 enum Algo { ALGO_AUTO = 0, ALGO_CLENSHAW = 1, ALGO_PS = 2, ALGO_PS3 = 3,
             ALGO_F32 = 4 /* reported only: the complex64-arithmetic lane kernel */,
             ALGO_SU2 = 5 /* reported only: the su(2) quaternion lane kernel */,
-            ALGO_SU2_F32 = 6 /* reported only: the same in float32 arithmetic */ };
+            ALGO_SU2_F32 = 6 /* reported only: the same in float32 arithmetic */,
+            ALGO_U2 = 7 /* reported only: the same lanes for u(2) systems */,
+            ALGO_U2_F32 = 8 /* reported only: u(2) lanes in float32 arithmetic */ };
 
 // GEMMs per slice: Clenshaw m; PS (s-1) + (r-1) + 1, r = ceil((m+1)/s)
 int ps_cost(int m, int s) {
@@ -170,6 +172,8 @@ bool d64_single();
 const char* family_kernel_name(int fam, int algo) {
   if (algo == 5) return "lane_su2_kernel";
   if (algo == 6) return "lane_su2_f32_kernel";
+  if (algo == 7) return "lane_u2_kernel";
+  if (algo == 8) return "lane_u2_f32_kernel";
   if (algo == 4)  // complex64 arithmetic (kernels_f32.cuh)
     return fam == FAM_S2 ? "lane_f32_kernel<2>" : fam == FAM_S4 ? "lane_f32_kernel<4>"
                                                                 : "lane_f32_kernel<8>";
@@ -227,6 +231,7 @@ struct sp_ctx {
   std::vector<double> terms_host;  // T x d x d complex128 interleaved
   bool herm_exact = false;         // every term bitwise Hermitian
   bool su2_terms = false;          // d = 2, every term bitwise Hermitian and traceless
+  bool u2_terms = false;           // d = 2, every term bitwise Hermitian, some with a trace
   // device-side
   bool dev_ready = false;
   bool terms_uploaded = false;
@@ -989,13 +994,29 @@ int f32_launch(sp_ctx* ctx, const SliceJob& job, double2* prefix_out, cudaStream
 
 // su(2) family: d = 2 traceless Hermitian terms, symmetric plan with
 // alternating coefficients (phase 1), fp64, pairwise, one fused launch
-// (kernels_su2.cuh).  SP_SU2=0 in the environment disables it (A/B timing).
+// (kernels_su2.cuh); u(2) systems (Hermitian terms with a trace part) on the
+// same lanes with complex Clenshaw pairs and 2 x 2 complex products (any
+// coefficients, phase 1).  SP_SU2=0 / SP_U2=0 in the environment disable
+// them (A/B timing).
 bool su2_applies(const sp_ctx* ctx, const SliceJob& job) {
   static const int enabled = [] {
     const char* e = getenv("SP_SU2");
     return (e && e[0] == '0') ? 0 : 1;
   }();
-  if (!enabled || !ctx->su2_terms || !job.coef_alt) return false;
+  static const int u2_enabled = [] {
+    const char* e = getenv("SP_U2");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  if (!enabled) return false;
+  const bool su2 = ctx->su2_terms && job.coef_alt;
+  // u(2): complex128, midpoint with 2 or 4 controls (the TMA lanes; the
+  // cp.async forms measured slower than lane_small_kernel<2,1>, and complex64
+  // keeps the reference's float32 sequence of lane_f32_kernel<2>: the u(2)
+  // float32 pairs land 1-3x outside the complex64 gate)
+  const bool u2 = u2_enabled && ctx->u2_terms && ctx->bits == 64 &&
+                  job.mode == SP_MODE_MIDPOINT && (job.n_ctrl == 2 || job.n_ctrl == 4) &&
+                  job.m <= SP_MAX_ORDER;
+  if (!su2 && !u2) return false;
   if (job.mode > SP_MODE_MAGNUS) return false;  // Gauss-Legendre: general d = 2 kernel
   if (!(job.phase[0] == 1.0 && job.phase[1] == 0.0)) return false;
   if (job.n_ctrl % 2 == 0 && ((uintptr_t)job.amps & 15u)) return false;  // vector row loads
@@ -1012,13 +1033,21 @@ int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_ou
   sj.mode = job.mode;
   sj.m = job.m;
   sj.dt6 = job.dt / 6.0;
+  // u(2): the terms carry a trace part (su(2) terms are traceless, and then
+  // (H00 - H11) / 2 is H00 exactly)
+  sj.u2 = ctx->su2_terms ? 0 : 1;
   for (int t = 0; t < ctx->n_terms; ++t) {
     const double* h = &ctx->terms_host[(size_t)t * 8];  // 2 x 2 complex128, row-major
-    sj.tz[t][0] = job.xs * h[0];                        // H00 (= -H11)
+    sj.ta[t] = job.xs * (0.5 * (h[0] + h[6]));          // (H00 + H11) / 2
+    sj.tz[t][0] = job.xs * (0.5 * (h[0] - h[6]));       // (H00 - H11) / 2
     sj.tz[t][1] = job.xs * h[2];                        // Re H01
     sj.tz[t][2] = job.xs * h[3];                        // Im H01
   }
-  for (int k = 0; k <= job.m; ++k) sj.cr[k] = job.coef[2 * k + (k & 1)];
+  for (int k = 0; k <= job.m; ++k) {
+    sj.cr[k] = job.coef[2 * k + (k & 1)];
+    sj.cz[2 * k] = job.coef[2 * k];
+    sj.cz[2 * k + 1] = job.coef[2 * k + 1];
+  }
   sj.viol = job.viol;
   sj.viol_epoch = job.viol_epoch;
   sj.out = fused_out;
@@ -1044,7 +1073,7 @@ int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_ou
   const int block = (int)std::min<int64_t>(tpb_max, ((per + 31) / 32) * 32);
   const bool lane_mode = fused_out == nullptr;
   int rc = ensure(ctx, ctx->lanes, lane_mode ? (size_t)grid * block * 4 * sizeof(double2)
-                                             : (size_t)grid * 4 * sizeof(double));
+                                             : (size_t)grid * 8 * sizeof(double));
   if (rc) return rc;
   if (lane_mode) {  // lane products, per-slice running products, initial products
     sj.lane_out = ctx->lanes.p;
@@ -1084,7 +1113,8 @@ int su2_launch(sp_ctx* ctx, const SliceJob& job, cudaStream_t st, void* fused_ou
     fprintf(stderr, "\n");
   }
   ++ctx->launches;
-  ctx->last_algo = ctx->bits == 32 ? ALGO_SU2_F32 : ALGO_SU2;
+  ctx->last_algo = sj.u2 ? (ctx->bits == 32 ? ALGO_U2_F32 : ALGO_U2)
+                         : (ctx->bits == 32 ? ALGO_SU2_F32 : ALGO_SU2);
   ctx->last_gemms = job.m;
   ctx->last_lanes = grid * block;
   *prods = (const double2*)ctx->lanes.p;
@@ -1460,6 +1490,17 @@ double executed_flops(const sp_ctx* ctx, int64_t n, int m) {
     if (ctx->mode != SP_MODE_MIDPOINT) w += 4.0 * N;
     if (ctx->mode == SP_MODE_MAGNUS) w += 2.0 * N + 4.0 * (N * (N - 1) / 2);
     const double f = 6.0 * (T - 1) + 5.0 + 4.0 * (m - 1) + 2.0 + 3.0 + 28.0 + w;
+    return (double)n * f;
+  }
+  if (ctx->last_algo == ALGO_U2 || ctx->last_algo == ALGO_U2_F32) {
+    // u(2) lanes (flops): 4 FMA per control term (assembly), 5 for zeta2,
+    // 20 per complex Clenshaw step after the peeled one (4), 20 for U, 56
+    // for the 2 x 2 complex product; three-point weights as su(2)
+    const int N = ctx->n_ctrl, T = ctx->n_terms;
+    double w = 0.0;
+    if (ctx->mode != SP_MODE_MIDPOINT) w += 4.0 * N;
+    if (ctx->mode == SP_MODE_MAGNUS) w += 2.0 * N + 4.0 * (N * (N - 1) / 2);
+    const double f = 8.0 * (T - 1) + 5.0 + 20.0 * (m - 1) + 4.0 + 20.0 + 56.0 + w;
     return (double)n * f;
   }
   if (ctx->fam == FAM_S2) {
@@ -2019,11 +2060,14 @@ int sp_set_hamiltonian(sp_ctx* ctx, int dim, int n_ctrl, int n_terms, int mode,
       }
   // su(2) family (kernels_su2.cuh): 2 x 2 terms that are bitwise Hermitian
   // and traceless, at most SU2_MAX_CTRL controls
-  ctx->su2_terms = dim == 2 && ctx->herm_exact && n_ctrl >= 1 && n_ctrl <= SU2_MAX_CTRL &&
+  const bool two = dim == 2 && ctx->herm_exact && n_ctrl >= 1 && n_ctrl <= SU2_MAX_CTRL &&
                    n_terms <= SU2_MAX_TERMS;
+  ctx->su2_terms = two;
   for (int t = 0; t < n_terms && ctx->su2_terms; ++t)
     if (!(ctx->terms_host[(size_t)t * 8 + 0] == -ctx->terms_host[(size_t)t * 8 + 6]))
       ctx->su2_terms = false;
+  // u(2) lanes (kernels_su2.cuh, 2 x 2 complex algebra) for the rest
+  ctx->u2_terms = two && !ctx->su2_terms;
   ctx->fam = fam;
   ctx->D = D;
   ctx->terms_uploaded = false;

@@ -66,12 +66,17 @@ struct Su2Job {
   int mode;
   int m;
   double dt6;                       // dt / 6 (magnus commutator weights)
-  double tz[SU2_MAX_TERMS][3];      // per term: 2X factor x (H00, Re H01, Im H01)
+  double tz[SU2_MAX_TERMS][3];      // per term: 2X factor x ((H00 - H11) / 2, Re H01, Im H01)
   double cr[SP_MAX_ORDER + 1];      // nonzero component of a_k: Re (k even), Im (k odd)
+  // u(2) systems (terms with a trace part): u2 = 1, the per-term trace part
+  // 2X factor x (H00 + H11) / 2, and the full complex coefficients a_k
+  int u2;
+  double ta[SU2_MAX_TERMS];
+  double cz[2 * (SP_MAX_ORDER + 1)];
   unsigned long long* viol;         // violation slots (epoch scheme of SliceJob), or null
   int viol_epoch;                   // 1: fused call (epoch slot), 0: slot 2
   unsigned* ctr;                    // arrival counter (zero between launches)
-  void* cta_out;                    // gridDim x 4 doubles: CTA products
+  void* cta_out;                    // gridDim x 8 doubles: CTA products
   void* out;                        // 2 x 2 result (complex128, or complex64 if to_fp32)
   int to_fp32;
   int arith32;                      // complex64 context: float32 arithmetic

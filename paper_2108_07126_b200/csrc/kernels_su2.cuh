@@ -40,6 +40,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "internal.h"
 
 namespace sp {
@@ -140,10 +142,46 @@ __device__ __forceinline__ void su2_store(void* base, int64_t idx, const QuatT<R
                : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// u(2) systems (terms with a trace part, lane_u2 kernels): the slice
+// propagators are general 2 x 2 complex matrices (no quaternion closure), the
+// running products too: 8 values, 32 FP64 operations per product.
+// ---------------------------------------------------------------------------
+template <class R>
+struct M2T {  // row-major: m[0..1] U00, m[2..3] U01, m[4..5] U10, m[6..7] U11 (re, im)
+  R m[8];
+};
+
+// P Q (P later in time, on the left), in lane_small_kernel's summation order
+template <class R>
+__device__ __forceinline__ M2T<R> m2_mul(const M2T<R>& P, const M2T<R>& Q) {
+  M2T<R> o;
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const R* p0 = &P.m[4 * r];
+      const R* p1 = &P.m[4 * r + 2];
+      const R* q0 = &Q.m[2 * c];
+      const R* q1 = &Q.m[4 + 2 * c];
+      R re = p0[0] * q0[0];
+      re = fma(-p0[1], q0[1], re);
+      re = fma(p1[0], q1[0], re);
+      re = fma(-p1[1], q1[1], re);
+      R im = p0[0] * q0[1];
+      im = fma(p0[1], q0[0], im);
+      im = fma(p1[0], q1[1], im);
+      im = fma(p1[1], q1[0], im);
+      o.m[4 * r + 2 * c] = re;
+      o.m[4 * r + 2 * c + 1] = im;
+    }
+  return o;
+}
+
 // |v| <= 1 fails (also for NaN): accumulated without a branch
 __device__ __forceinline__ bool amp_bad(double v) { return !(fabs(v) <= 1.0); }
 
-template <int MODE, int NCC, class R = double>
+template <int MODE, int NCC, class R = double, bool U2 = false>
 struct Su2Shape {
   // doubles read per slice: midpoint one row; three-point the rows 2s+1, 2s+2
   // (row 2s is the previous slice's last row)
@@ -153,9 +191,11 @@ struct Su2Shape {
   static constexpr int CP = K * 8 / UNIT;      // cp.async per slice
   // threads per CTA: 1024 (64 registers) except the three-point forms, whose
   // float64 weights need more registers (with >= 3 controls, or next to the
-  // float32 working set of complex64 contexts)
+  // float32 working set of complex64 contexts), and the u(2) forms (complex
+  // Clenshaw pairs, 2 x 2 complex products: 128 registers)
   static constexpr bool F32 = sizeof(R) == 4;
-  static constexpr int TPB = MODE == SP_MODE_MIDPOINT ? 1024
+  static constexpr int TPB = U2 ? (MODE != SP_MODE_MIDPOINT && NCC >= 3 ? 256 : 512)
+                             : MODE == SP_MODE_MIDPOINT ? 1024
                              : NCC >= 3 ? (F32 ? 256 : 512)
                                         : (F32 ? 512 : 1024);
   // shared-memory ring: DS slices per thread in flight (<= 192 KB per CTA:
@@ -195,21 +235,24 @@ __device__ __noinline__ unsigned long long su2_first_bad(const double* amps, int
   return ~0ull;
 }
 
-// One slice's propagator: weights from the slice's amplitude samples `cur`
-// (and, for the three-point modes, the carried row 2s in r1),
-// Z' = sum_t w_t tz_t, the real Clenshaw pairs, U = A I + i B Z'.
-template <class R, int MODE, int NCC, int MC>
-__device__ __forceinline__ QuatT<R> su2_u(const Su2Job& job, int m, const double* cur,
-                                          double (&r1)[NCC]) {
+// Slice weights (hamiltonian.py:199-205, magnus.py:88-106) from the slice's
+// amplitude samples `cur` (and, for the three-point modes, the carried row
+// 2s in r1), and Z = sum_t w_t z_t (2X factor folded into the per-term
+// components on the host): dz, zx, zy the traceless part, z0 (TR) the trace
+// part.  (complex64 contexts: the float64 weights and the terms cast to the
+// working precision, linalg.py:273-274, everything after in float32.)
+template <class R, int MODE, int NCC, bool TR>
+__device__ __forceinline__ void su2_weights(const Su2Job& job, const double* cur,
+                                            double (&r1)[NCC], R& z0, R& dz, R& zx, R& zy) {
   constexpr int T = MODE == SP_MODE_MAGNUS ? 1 + 2 * NCC + NCC * (NCC - 1) / 2 : 1 + NCC;
   static_assert(T <= SU2_MAX_TERMS, "too many su(2) terms");
-  // ---- slice weights (hamiltonian.py:199-205, magnus.py:88-106) and
-  // Z' = sum_t w_t tz_t (2X factor folded into tz on the host)
-  // (complex64 contexts: the float64 weights and the terms cast to the
-  // working precision, linalg.py:273-274, everything after in float32)
-  R dz = (R)job.tz[0][0], zx = (R)job.tz[0][1], zy = (R)job.tz[0][2];
+  z0 = TR ? (R)job.ta[0] : R(0);
+  dz = (R)job.tz[0][0];
+  zx = (R)job.tz[0][1];
+  zy = (R)job.tz[0][2];
   auto add = [&](int t, double w64) {
     const R w = (R)w64;
+    if constexpr (TR) z0 = fma(w, (R)job.ta[t], z0);
     dz = fma(w, (R)job.tz[t][0], dz);
     zx = fma(w, (R)job.tz[t][1], zx);
     zy = fma(w, (R)job.tz[t][2], zy);
@@ -234,6 +277,15 @@ __device__ __forceinline__ QuatT<R> su2_u(const Su2Job& job, int m, const double
 #pragma unroll
     for (int q = 0; q < NCC; ++q) r1[q] = c3[q];
   }
+}
+
+// One su(2) slice's propagator: Z' = sum_t w_t tz_t, the real Clenshaw
+// pairs, U = A I + i B Z'.
+template <class R, int MODE, int NCC, int MC>
+__device__ __forceinline__ QuatT<R> su2_u(const Su2Job& job, int m, const double* cur,
+                                          double (&r1)[NCC]) {
+  R z0, dz, zx, zy;
+  su2_weights<R, MODE, NCC, false>(job, cur, r1, z0, dz, zx, zy);
   const R zeta2 = fma(dz, dz, fma(zx, zx, zy * zy));
   // ---- real Clenshaw pairs; the j = m - 1 step peeled (B_{m+1} = 0)
   R A = (R)job.cr[m - 1], B = (R)job.cr[m], oA = (R)job.cr[m], oB = R(0);
@@ -251,19 +303,216 @@ __device__ __forceinline__ QuatT<R> su2_u(const Su2Job& job, int m, const double
   return QuatT<R>{A, B * dz, -(B * zy), B * zx};
 }
 
-// V <- U(slice) V
+// u(2) slice propagators, K slices in lockstep (independent dependency
+// chains for the in-order issue: one Clenshaw loop advances all K): Z = z0 I
+// + Z' (Z'^2 = zeta2 I), the complex Clenshaw pairs b_j = a_j I + b_j' Z' of
+// lane_small_kernel<2,1>'s d = 2 path (chebyshev.py:298-303 on the
+// 2-dimensional algebra; first step peeled), U = a I + b Z' entry by entry.
+template <class R, int MODE, int NCC, int MC, int K>
+__device__ __forceinline__ void u2_u_multi(const Su2Job& job, int m, const double* const (&cur)[K],
+                                           double (&r1)[NCC], M2T<R> (&U)[K]) {
+  R z0[K], dz[K], zx[K], zy[K], zeta2[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    su2_weights<R, MODE, NCC, true>(job, cur[k], r1, z0[k], dz[k], zx[k], zy[k]);
+    zeta2[k] = fma(dz[k], dz[k], fma(zx[k], zx[k], zy[k] * zy[k]));
+  }
+  auto cre = [&](int j) { return (R)job.cz[2 * j]; };
+  auto cim = [&](int j) { return (R)job.cz[2 * j + 1]; };
+  R car[K], cai[K], cbr[K], cbi[K], oar[K], oai[K], obr[K], obi[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    car[k] = cre(m);
+    cai[k] = cim(m);
+    cbr[k] = cbi[k] = oar[k] = oai[k] = obr[k] = obi[k] = R(0);
+    if (m >= 1) {
+      oar[k] = car[k];
+      oai[k] = cai[k];
+      cbr[k] = car[k];
+      cbi[k] = cai[k];
+      car[k] = cre(m - 1) + z0[k] * oar[k];
+      cai[k] = cim(m - 1) + z0[k] * oai[k];
+    }
+  }
+  constexpr int MU = MC > 0 ? MC : 1;
+#pragma unroll MU
+  for (int jj = m - 2; jj >= 0; --jj) {
+    const R beta = (jj == 0) ? R(2) : R(1);
+    const R ar = cre(jj), ai = cim(jj);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const R nar = ar + fma(z0[k], car[k], fma(zeta2[k], cbr[k], -beta * oar[k]));
+      const R nai = ai + fma(z0[k], cai[k], fma(zeta2[k], cbi[k], -beta * oai[k]));
+      const R nbr = car[k] + fma(z0[k], cbr[k], -beta * obr[k]);
+      const R nbi = cai[k] + fma(z0[k], cbi[k], -beta * obi[k]);
+      oar[k] = car[k];
+      oai[k] = cai[k];
+      obr[k] = cbr[k];
+      obi[k] = cbi[k];
+      car[k] = nar;
+      cai[k] = nai;
+      cbr[k] = nbr;
+      cbi[k] = nbi;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    U[k].m[0] = fma(cbr[k], dz[k], car[k]);
+    U[k].m[1] = fma(cbi[k], dz[k], cai[k]);
+    U[k].m[2] = cbr[k] * zx[k] - cbi[k] * zy[k];
+    U[k].m[3] = cbr[k] * zy[k] + cbi[k] * zx[k];
+    U[k].m[4] = cbr[k] * zx[k] + cbi[k] * zy[k];
+    U[k].m[5] = cbi[k] * zx[k] - cbr[k] * zy[k];
+    U[k].m[6] = fma(-cbr[k], dz[k], car[k]);
+    U[k].m[7] = fma(-cbi[k], dz[k], cai[k]);
+  }
+}
 template <class R, int MODE, int NCC, int MC>
-__device__ __forceinline__ void su2_slice(const Su2Job& job, int m, const double* cur,
-                                          double (&r1)[NCC], QuatT<R>& V) {
-  V = quat_mul(su2_u<R, MODE, NCC, MC>(job, m, cur, r1), V);
+__device__ __forceinline__ M2T<R> u2_u(const Su2Job& job, int m, const double* cur,
+                                       double (&r1)[NCC]) {
+  const double* const c[1] = {cur};
+  M2T<R> U[1];
+  u2_u_multi<R, MODE, NCC, MC, 1>(job, m, c, r1, U);
+  return U[0];
+}
+
+// The two algebras behind one set of lane kernels: the element type, the
+// product (later on the left), shuffles, the per-slice propagator, the
+// complex128 2 x 2 stores / loads of lane mode, the CTA-product slots.
+template <class R_>
+struct QuatAlg {
+  using R = R_;
+  using E = QuatT<R>;
+  static constexpr bool PAIRS = false;  // TMA round: all C propagators first (ILP)
+  __device__ static E one() { return quat_identity<R>(); }
+  __device__ static E mul(const E& a, const E& b) { return quat_mul(a, b); }
+  __device__ static E shfl(const E& q, int k) { return quat_shfl_down(q, k); }
+  template <int MODE, int NCC, int MC>
+  __device__ static E slice(const Su2Job& job, int m, const double* cur, double (&r1)[NCC]) {
+    return su2_u<R, MODE, NCC, MC>(job, m, cur, r1);
+  }
+  __device__ static void store(void* base, int64_t idx, const E& q) { su2_store(base, idx, q); }
+  __device__ static E vinit(const Su2Job& job, int64_t lane) { return su2_vinit<R>(job, lane); }
+  __device__ static void cta_put(void* p, int i, const E& q) { reinterpret_cast<E*>(p)[i] = q; }
+  __device__ static E cta_get(const void* p, int i) {
+    if constexpr (sizeof(R) == 8) {
+      const double2* cp = reinterpret_cast<const double2*>(p);
+      const double2 a = __ldcg(cp + 2 * i), b = __ldcg(cp + 2 * i + 1);
+      return E{a.x, a.y, b.x, b.y};
+    } else {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(p) + i);
+      return E{a.x, a.y, a.z, a.w};
+    }
+  }
+  // [[a, b], [-conj(b), conj(a)]] row-major
+  __device__ static void entries(const E& M, R (&e)[8]) {
+    e[0] = M.ar; e[1] = M.ai; e[2] = M.br; e[3] = M.bi;
+    e[4] = -M.br; e[5] = M.bi; e[6] = M.ar; e[7] = -M.ai;
+  }
+};
+
+template <class R_>
+struct U2Alg {
+  using R = R_;
+  using E = M2T<R>;
+  static constexpr bool PAIRS = true;  // TMA round: propagators two at a time (registers)
+  __device__ static E one() { return E{{R(1), R(0), R(0), R(0), R(0), R(0), R(1), R(0)}}; }
+  __device__ static E mul(const E& a, const E& b) { return m2_mul(a, b); }
+  __device__ static E shfl(const E& q, int k) {
+    E o;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o.m[i] = __shfl_down_sync(0xffffffffu, q.m[i], k);
+    return o;
+  }
+  template <int MODE, int NCC, int MC>
+  __device__ static E slice(const Su2Job& job, int m, const double* cur, double (&r1)[NCC]) {
+    return u2_u<R, MODE, NCC, MC>(job, m, cur, r1);
+  }
+  // two midpoint slices in lockstep (TMA rounds)
+  template <int NCC, int MC>
+  __device__ static void slice2(const Su2Job& job, int m, const double* c0, const double* c1,
+                                double (&r1)[NCC], E& u0, E& u1) {
+    const double* const c[2] = {c0, c1};
+    E U[2];
+    u2_u_multi<R, SP_MODE_MIDPOINT, NCC, MC, 2>(job, m, c, r1, U);
+    u0 = U[0];
+    u1 = U[1];
+  }
+  __device__ static void store(void* base, int64_t idx, const E& q) {
+    double* o = reinterpret_cast<double*>(base) + 8 * idx;
+    if (reinterpret_cast<uintptr_t>(o) & 31u) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (double)q.m[i];
+      return;
+    }
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o), "d"((double)q.m[0]),
+                 "d"((double)q.m[1]), "d"((double)q.m[2]), "d"((double)q.m[3])
+                 : "memory");
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o + 4), "d"((double)q.m[4]),
+                 "d"((double)q.m[5]), "d"((double)q.m[6]), "d"((double)q.m[7])
+                 : "memory");
+  }
+  __device__ static E vinit(const Su2Job& job, int64_t lane) {
+    if (job.vinit == nullptr) return one();
+    const double* e = reinterpret_cast<const double*>(job.vinit) + 8 * lane;
+    E o;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o.m[i] = (R)e[i];
+    return o;
+  }
+  __device__ static void cta_put(void* p, int i, const E& q) { reinterpret_cast<E*>(p)[i] = q; }
+  __device__ static E cta_get(const void* p, int i) {
+    E o;
+    if constexpr (sizeof(R) == 8) {
+      const double2* cp = reinterpret_cast<const double2*>(p) + 4 * i;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double2 a = __ldcg(cp + k);
+        o.m[2 * k] = a.x;
+        o.m[2 * k + 1] = a.y;
+      }
+    } else {
+      const float4* cp = reinterpret_cast<const float4*>(p) + 2 * i;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float4 a = __ldcg(cp + k);
+        o.m[4 * k] = a.x;
+        o.m[4 * k + 1] = a.y;
+        o.m[4 * k + 2] = a.z;
+        o.m[4 * k + 3] = a.w;
+      }
+    }
+    return o;
+  }
+  __device__ static void entries(const E& M, R (&e)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) e[i] = M.m[i];
+  }
+};
+
+template <class R, bool U2>
+using Su2AlgT = typename std::conditional<U2, U2Alg<R>, QuatAlg<R>>::type;
+
+// lane 0 ends with M_{31} ... M_1 M_0 (later lanes on the left); the width
+// form over the first `width` lanes only (the others hold identity)
+template <class A>
+__device__ __forceinline__ void alg_warp_product(typename A::E& q) {
+#pragma unroll
+  for (int k = 1; k < 32; k <<= 1) q = A::mul(A::shfl(q, k), q);
+}
+template <class A>
+__device__ __forceinline__ void alg_warp_product(typename A::E& q, int width) {
+  for (int k = 1; k < width; k <<= 1) q = A::mul(A::shfl(q, k), q);
 }
 
 // After the lane loops: the lane's first amplitude offender (rare path; rows
 // [r0, rl] of the table), the ordered CTA product, the arrival ticket and, in
 // the last CTA, the ordered product of the CTA products and the d x d result.
-template <class R, int NCC, bool PFX = false>
-__device__ __forceinline__ void su2_finish(const Su2Job& job, QuatT<R> V, bool bad, int64_t r0,
-                                           int64_t rl) {
+template <class A, int NCC, bool PFX = false>
+__device__ __forceinline__ void su2_finish(const Su2Job& job, typename A::E V, bool bad,
+                                           int64_t r0, int64_t rl) {
+  using R = typename A::R;
+  using E = typename A::E;
   if (bad && job.viol) {
     const unsigned long long v = su2_first_bad(job.amps, r0, rl, NCC);
     // fused calls: the epoch slot (SliceJob::viol); multi-launch calls: slot 2
@@ -272,20 +521,20 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, QuatT<R> V, bool b
     atomicMin(slot, v);
   }
   if (PFX && job.lane_out != nullptr) {  // lane mode: the lane product, no tree
-    su2_store(job.lane_out, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, V);
+    A::store(job.lane_out, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, V);
     return;
   }
   // ---- ordered products: warps, then the CTA's warps (warp 0)
-  __shared__ QuatT<R> wq[32];
+  __shared__ E wq[32];
   __shared__ bool last;
   const int ln = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  auto cta_product = [&](QuatT<R>& q) {  // result in thread 0
-    quat_warp_product(q);
+  auto cta_product = [&](E& q) {  // result in thread 0
+    alg_warp_product<A>(q);
     if (ln == 0) wq[wp] = q;
     __syncthreads();
     if (wp == 0) {
-      q = ln < nw ? wq[ln] : quat_identity<R>();
-      quat_warp_product(q, nw);  // only the levels the nw warp products need
+      q = ln < nw ? wq[ln] : A::one();
+      alg_warp_product<A>(q, nw);  // only the levels the nw warp products need
     }
     __syncthreads();
   };
@@ -293,7 +542,7 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, QuatT<R> V, bool b
   cta_product(V);
   su2_mark(job, 3);
   if (threadIdx.x == 0) {
-    reinterpret_cast<QuatT<R>*>(job.cta_out)[blockIdx.x] = V;
+    A::cta_put(job.cta_out, blockIdx.x, V);
     unsigned old;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
                  : "=r"(old)
@@ -308,23 +557,13 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, QuatT<R> V, bool b
   // (later on the left), then one CTA-wide ordered product
   const int G = (int)gridDim.x, per = (G + (int)blockDim.x - 1) / (int)blockDim.x;
   const int i0 = min(G, (int)threadIdx.x * per), i1 = min(G, i0 + per);
-  QuatT<R> M = quat_identity<R>();
-  for (int i = i0; i < i1; ++i) {
-    QuatT<R> c;
-    if constexpr (sizeof(R) == 8) {
-      const double2* cp = reinterpret_cast<const double2*>(job.cta_out);
-      const double2 a = __ldcg(cp + 2 * i), b = __ldcg(cp + 2 * i + 1);
-      c = QuatT<R>{a.x, a.y, b.x, b.y};
-    } else {
-      const float4 a = __ldcg(reinterpret_cast<const float4*>(job.cta_out) + i);
-      c = QuatT<R>{a.x, a.y, a.z, a.w};
-    }
-    M = quat_mul(c, M);
-  }
+  E M = A::one();
+  for (int i = i0; i < i1; ++i) M = A::mul(A::cta_get(job.cta_out, i), M);
   cta_product(M);
   if (threadIdx.x == 0) {
-    // [[a, b], [-conj(b), conj(a)]] in the output dtype
-    const R e[8] = {M.ar, M.ai, M.br, M.bi, -M.br, M.bi, M.ar, -M.ai};
+    // the 2 x 2 result, row-major, in the output dtype
+    R e[8];
+    A::entries(M, e);
     if (job.to_fp32) {
       float* o = reinterpret_cast<float*>(job.out);
 #pragma unroll
@@ -350,10 +589,11 @@ __device__ __forceinline__ void su2_finish(const Su2Job& job, QuatT<R> V, bool b
 // [lane n / lanes, (lane + 1) n / lanes); the rows stream through a
 // per-thread cp.async ring in shared memory.
 // ---------------------------------------------------------------------------
-template <int MODE, int NCC, int MC, class R = double, bool PFX = false>
-__global__ void __launch_bounds__(Su2Shape<MODE, NCC, R>::TPB, 1)
+template <int MODE, int NCC, int MC, class R = double, bool PFX = false, bool U2 = false>
+__global__ void __launch_bounds__(Su2Shape<MODE, NCC, R, U2>::TPB, 1)
     lane_su2_kernel(const Su2Job job) {
-  using S = Su2Shape<MODE, NCC, R>;
+  using S = Su2Shape<MODE, NCC, R, U2>;
+  using A = Su2AlgT<R, U2>;
   constexpr int K = S::K, DS = S::DS, CP = S::CP, UNIT = S::UNIT;
   extern __shared__ __align__(16) unsigned char su2_ring[];
   const int m = MC > 0 ? MC : job.m;
@@ -365,7 +605,7 @@ __global__ void __launch_bounds__(Su2Shape<MODE, NCC, R>::TPB, 1)
 
   // PFX: lane mode (initial products, per-slice running products, lane
   // products instead of the fused tail)
-  QuatT<R> V = PFX ? su2_vinit<R>(job, lane) : quat_identity<R>();
+  typename A::E V = PFX ? A::vinit(job, lane) : A::one();
   bool bad = false;
   // first unit of this lane: row s0 (midpoint) or rows 2 s0 + 1, 2 s0 + 2
   const unsigned char* unit0 = reinterpret_cast<const unsigned char*>(
@@ -416,13 +656,13 @@ __global__ void __launch_bounds__(Su2Shape<MODE, NCC, R>::TPB, 1)
         }
 #pragma unroll
         for (int q = 0; q < K; ++q) bad |= amp_bad(cur[q]);
-        su2_slice<R, MODE, NCC, MC>(job, m, cur, r1, V);
-        if (PFX && job.prefix_out != nullptr) su2_store(job.prefix_out, s0 + k0 + j, V);
+        V = A::mul(A::template slice<MODE, NCC, MC>(job, m, cur, r1), V);
+        if (PFX && job.prefix_out != nullptr) A::store(job.prefix_out, s0 + k0 + j, V);
       }
     }
   }
-  su2_finish<R, NCC, PFX>(job, V, bad, MODE == SP_MODE_MIDPOINT ? s0 : 2 * s0,
-                  MODE == SP_MODE_MIDPOINT ? s1 - 1 : 2 * s1);
+  su2_finish<A, NCC, PFX>(job, V, bad, MODE == SP_MODE_MIDPOINT ? s0 : 2 * s0,
+                          MODE == SP_MODE_MIDPOINT ? s1 - 1 : 2 * s1);
 }
 
 // ---------------------------------------------------------------------------
@@ -475,11 +715,13 @@ __device__ __forceinline__ void su2_tma_2d(void* dst, const void* tmap, int x, i
       : "memory");
 }
 
-template <int NCC, int MC, int C, class R = double, bool PFX = false>
+template <int NCC, int MC, int C, class R = double, bool PFX = false, bool U2 = false>
 __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
     lane_su2_tma_kernel(const Su2Job job, const __grid_constant__ CUtensorMap tmap,
                         const int64_t L) {
   using G = Su2Tma<NCC, C>;
+  using A = Su2AlgT<R, U2>;
+  using E = typename A::E;
   constexpr int NST = G::NST, STAGE = G::STAGE, LROWB = G::LROWB, ROWB = G::ROWB;
   extern __shared__ unsigned char su2_tma_raw[];
   __shared__ __align__(8) uint64_t bars[(G::TPB / 32) * NST];
@@ -517,7 +759,7 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
   }
   __syncwarp();
 
-  QuatT<R> V = PFX ? su2_vinit<R>(job, lane) : quat_identity<R>();
+  E V = PFX ? A::vinit(job, lane) : A::one();
   bool bad = false;
   double r1[NCC];
   const int sw = LROWB == 128 ? (ln & 7) : ((ln >> 1) & 3);  // swizzle of this lane's row
@@ -536,26 +778,40 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
       }
     };
     if (!direct && (r + 1) * C <= cnt) {
-      // a whole round: the C slice propagators are independent (ILP), the
-      // running product takes them in adjacent pairs, later on the left
-      QuatT<R> U[C];
-#pragma unroll
-      for (int k = 0; k < C; ++k) {
+      // a whole round: the slice propagators are independent (ILP), the
+      // running product takes them in adjacent pairs, later on the left —
+      // all C first (quaternions) or two at a time (u(2): registers)
+      auto u_of = [&](int k) {
         double cur[NCC];
         smem_row(k, cur);
 #pragma unroll
         for (int q = 0; q < NCC; ++q) bad |= amp_bad(cur[q]);
-        U[k] = su2_u<R, SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1);
-      }
-      if (!PFX || job.prefix_out == nullptr) {
-#pragma unroll
-        for (int k = 0; k < C; k += 2) V = quat_mul(quat_mul(U[k + 1], U[k]), V);
-      } else {  // every slice's running product is written: one at a time
+        return A::template slice<SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1);
+      };
+      if (PFX && job.prefix_out != nullptr) {  // every slice's running product is written
 #pragma unroll
         for (int k = 0; k < C; ++k) {
-          V = quat_mul(U[k], V);
-          su2_store(job.prefix_out, s0 + r * C + k, V);
+          V = A::mul(u_of(k), V);
+          A::store(job.prefix_out, s0 + r * C + k, V);
         }
+      } else if constexpr (A::PAIRS) {
+#pragma unroll
+        for (int k = 0; k < C; k += 2) {
+          double c0[NCC], c1[NCC];
+          smem_row(k, c0);
+          smem_row(k + 1, c1);
+#pragma unroll
+          for (int q = 0; q < NCC; ++q) bad |= amp_bad(c0[q]) | amp_bad(c1[q]);
+          E u0, u1;
+          A::template slice2<NCC, MC>(job, m, c0, c1, r1, u0, u1);
+          V = A::mul(A::mul(u1, u0), V);
+        }
+      } else {
+        E U[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) U[k] = u_of(k);
+#pragma unroll
+        for (int k = 0; k < C; k += 2) V = A::mul(A::mul(U[k + 1], U[k]), V);
       }
     } else {
 #pragma unroll
@@ -571,8 +827,8 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
           }
 #pragma unroll
           for (int q = 0; q < NCC; ++q) bad |= amp_bad(cur[q]);
-          su2_slice<R, SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1, V);
-          if (PFX && job.prefix_out != nullptr) su2_store(job.prefix_out, s0 + kk, V);
+          V = A::mul(A::template slice<SP_MODE_MIDPOINT, NCC, MC>(job, m, cur, r1), V);
+          if (PFX && job.prefix_out != nullptr) A::store(job.prefix_out, s0 + kk, V);
         }
       }
     }
@@ -584,7 +840,7 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
       su2_tma_2d(ring + s * STAGE, &tmap, (r + NST) * C * NCC, (int)wlane0, wb + s);
     }
   }
-  su2_finish<R, NCC, PFX>(job, V, bad, s0, s1 - 1);
+  su2_finish<A, NCC, PFX>(job, V, bad, s0, s1 - 1);
 }
 
 }  // namespace sp
@@ -620,7 +876,7 @@ __global__ void __launch_bounds__(512, 1) qubit_reference_kernel(const Su2Job jo
     // [[c - i s az, -i s (nx - i ny)], [-i s (nx + i ny), c + i s az]]
     V = quat_mul(Quat{q.c, -q.s * q.az, -q.s * ny, -q.s * nx}, V);
   }
-  su2_finish<double, 1>(job, V, false, 0, 0);
+  su2_finish<QuatAlg<double>, 1>(job, V, false, 0, 0);
 }
 
 }  // namespace sp

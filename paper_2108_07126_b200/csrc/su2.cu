@@ -1,4 +1,5 @@
-// Launchers of the su(2) family (kernels_su2.cuh).
+// Launchers of the su(2) family (kernels_su2.cuh), and of the same lanes on
+// the 2 x 2 complex algebra for u(2) systems (terms with a trace part).
 //   lane_su2_tma_kernel  midpoint, 2 or 4 controls (the driven qubit): TMA
 //                        2-D tensor loads of the amplitude rows
 //   lane_su2_kernel      every mode / control count: cp.async row ring
@@ -28,22 +29,22 @@ struct Su2Kernel {
   int rows = 0;       // TMA: rows per lane per round (C)
 };
 
-template <int MODE, int NCC, class R, bool PFX>
+template <int MODE, int NCC, class R, bool PFX, bool U2>
 Su2Kernel su2_pick(int m) {
-  using S = Su2Shape<MODE, NCC, R>;
+  using S = Su2Shape<MODE, NCC, R, U2>;
   Su2Kernel k;
   k.smem = S::SMEM_PER_THREAD * S::TPB;
   k.max_block = S::TPB;
   switch (m) {
-    case 3: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 3, R, PFX>; break;
-    case 5: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 5, R, PFX>; break;
-    case 7: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 7, R, PFX>; break;
-    default: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 0, R, PFX>;
+    case 3: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 3, R, PFX, U2>; break;
+    case 5: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 5, R, PFX, U2>; break;
+    case 7: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 7, R, PFX, U2>; break;
+    default: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 0, R, PFX, U2>;
   }
   return k;
 }
 
-template <int NCC, int C, class R, bool PFX>
+template <int NCC, int C, class R, bool PFX, bool U2>
 Su2Kernel su2_pick_tma(int m) {
   using G = Su2Tma<NCC, C>;
   Su2Kernel k;
@@ -51,6 +52,12 @@ Su2Kernel su2_pick_tma(int m) {
   k.max_block = G::TPB;
   k.tma = true;
   k.rows = C;
+  if constexpr (U2) {  // the random systems' fp64 / fp32 plan orders compiled in
+    k.fn = m == 13 ? (const void*)lane_su2_tma_kernel<NCC, 13, C, R, PFX, true>
+           : m == 7 ? (const void*)lane_su2_tma_kernel<NCC, 7, C, R, PFX, true>
+                    : (const void*)lane_su2_tma_kernel<NCC, 0, C, R, PFX, true>;
+    return k;
+  }
   switch (m) {
     case 3: k.fn = (const void*)lane_su2_tma_kernel<NCC, 3, C, R, PFX>; break;
     case 5: k.fn = (const void*)lane_su2_tma_kernel<NCC, 5, C, R, PFX>; break;
@@ -60,13 +67,13 @@ Su2Kernel su2_pick_tma(int m) {
   return k;
 }
 
-template <int MODE, class R, bool PFX>
+template <int MODE, class R, bool PFX, bool U2>
 Su2Kernel su2_pick_n(int n_ctrl, int m) {
   switch (n_ctrl) {
-    case 1: return su2_pick<MODE, 1, R, PFX>(m);
-    case 2: return su2_pick<MODE, 2, R, PFX>(m);
-    case 3: return su2_pick<MODE, 3, R, PFX>(m);
-    case 4: return su2_pick<MODE, 4, R, PFX>(m);
+    case 1: return su2_pick<MODE, 1, R, PFX, U2>(m);
+    case 2: return su2_pick<MODE, 2, R, PFX, U2>(m);
+    case 3: return su2_pick<MODE, 3, R, PFX, U2>(m);
+    case 4: return su2_pick<MODE, 4, R, PFX, U2>(m);
   }
   return {};
 }
@@ -76,27 +83,39 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-template <class R, bool PFX>
+template <class R, bool PFX, bool U2>
 Su2Kernel su2_kernel_for_t(const Su2Job& job) {
   static const int use_tma = env_int("SP_SU2_TMA", 1);
   // 128-byte lane rows per round (measured: 64-byte rounds with 1024-thread
   // CTAs 1.4x slower at 1e7 slices)
   if (use_tma && job.mode == SP_MODE_MIDPOINT && (job.n_ctrl == 2 || job.n_ctrl == 4))
-    return job.n_ctrl == 2 ? su2_pick_tma<2, 8, R, PFX>(job.m)
-                           : su2_pick_tma<4, 4, R, PFX>(job.m);
+    return job.n_ctrl == 2 ? su2_pick_tma<2, 8, R, PFX, U2>(job.m)
+                           : su2_pick_tma<4, 4, R, PFX, U2>(job.m);
   switch (job.mode) {
-    case SP_MODE_MIDPOINT: return su2_pick_n<SP_MODE_MIDPOINT, R, PFX>(job.n_ctrl, job.m);
-    case SP_MODE_SIMPSON: return su2_pick_n<SP_MODE_SIMPSON, R, PFX>(job.n_ctrl, job.m);
-    case SP_MODE_MAGNUS: return su2_pick_n<SP_MODE_MAGNUS, R, PFX>(job.n_ctrl, job.m);
+    case SP_MODE_MIDPOINT: return su2_pick_n<SP_MODE_MIDPOINT, R, PFX, U2>(job.n_ctrl, job.m);
+    case SP_MODE_SIMPSON: return su2_pick_n<SP_MODE_SIMPSON, R, PFX, U2>(job.n_ctrl, job.m);
+    case SP_MODE_MAGNUS: return su2_pick_n<SP_MODE_MAGNUS, R, PFX, U2>(job.n_ctrl, job.m);
   }
   return {};
 }
 
 // complex64 contexts: the same kernels in float32 arithmetic; lane mode
-// (lane_out set: sequential reduction / equiprop_all) is complex128 only
+// (lane_out set: sequential reduction / equiprop_all) is complex128 only;
+// u(2) systems (job.u2) on the 2 x 2 complex algebra: the TMA lanes only
+// (engine.cu su2_applies routes the rest to lane_small_kernel<2,1>)
+template <bool PFX>
+Su2Kernel u2_kernel_for(const Su2Job& job) {  // complex128, midpoint, 2 / 4 controls
+  if (job.mode != SP_MODE_MIDPOINT || job.arith32) return {};
+  if (job.n_ctrl == 2) return su2_pick_tma<2, 8, double, PFX, true>(job.m);
+  if (job.n_ctrl == 4) return su2_pick_tma<4, 4, double, PFX, true>(job.m);
+  return {};
+}
+
 Su2Kernel su2_kernel_for(const Su2Job& job) {
-  if (job.lane_out) return su2_kernel_for_t<double, true>(job);
-  return job.arith32 ? su2_kernel_for_t<float, false>(job) : su2_kernel_for_t<double, false>(job);
+  if (job.u2) return job.lane_out ? u2_kernel_for<true>(job) : u2_kernel_for<false>(job);
+  if (job.lane_out) return su2_kernel_for_t<double, true, false>(job);
+  return job.arith32 ? su2_kernel_for_t<float, false, false>(job)
+                     : su2_kernel_for_t<double, false, false>(job);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
