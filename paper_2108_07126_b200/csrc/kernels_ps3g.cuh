@@ -169,6 +169,33 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   constexpr int QB = UPT < 4 ? UPT : (C::MT >= 4 ? 2 : 4);  // (D512: register budget)
   static_assert(UNITS % C::THREADS == 0 && UPT % QB == 0, "assembly tiling");
   constexpr size_t TD = (size_t)2 * D * D;  // doubles per 2-plane term
+  // (s = 3: TMEM block 3 is free — the powers are T_1, T_2 — and holds the
+  // scaled drift xs H0 of this thread's units for the whole call: the
+  // per-slice assembly reads one term fewer from L2.  8 columns per unit.)
+  static_assert(UPT * 8 == 4 * NE && QB % 2 == 0, "drift block in TMEM");
+  const bool drift_tm = s == 3;
+  auto unit_blk = [&](int unit) {
+    return (unit / (KBC * 32)) * KB + cb * KBC + (unit / 32) % KBC;
+  };
+  if (drift_tm) {
+#pragma unroll 1
+    for (int b = 0; b < UPT; b += 2) {
+      double re[4], im[4];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const double* h = terms + (size_t)unit_blk(threadIdx.x + (b + v) * C::THREADS) * 128 +
+                          2 * ln;
+        const double2 hr = __ldg(reinterpret_cast<const double2*>(h));
+        const double2 hi = __ldg(reinterpret_cast<const double2*>(h + 64));
+        re[2 * v] = job.xs * hr.x;
+        re[2 * v + 1] = job.xs * hr.y;
+        im[2 * v] = job.xs * hi.x;
+        im[2 * v + 1] = job.xs * hi.y;
+      }
+      tmem_st4(tm(3) + 8 * b, re, im);
+    }
+    tmem_wait_st();
+  }
   auto assemble = [&](int64_t sl, int t1_off) {
     for (int tt = threadIdx.x; tt < T; tt += C::THREADS)
       smem[w_off + tt] = (tt == 0) ? job.xs : job.xs * slice_weight(job, sl, tt);
@@ -178,11 +205,22 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       int blk[QB];
       double2 xr[QB], xi[QB];
 #pragma unroll
-      for (int u = 0; u < QB; ++u) {
-        const int unit = threadIdx.x + (b + u) * C::THREADS;
-        blk[u] = (unit / (KBC * 32)) * KB + cb * KBC + (unit / 32) % KBC;
-      }
-      {
+      for (int u = 0; u < QB; ++u) blk[u] = unit_blk(threadIdx.x + (b + u) * C::THREADS);
+      if (drift_tm) {  // xs H0 (the drift's weight is xs) from TMEM
+        uint32_t w[QB / 2][16];
+#pragma unroll
+        for (int v = 0; v < QB / 2; ++v) tmem_ld16(tm(3) + 8 * (b + 2 * v), w[v]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < QB / 2; ++v) {
+          double re[4], im[4];
+          tmem_unpack4(w[v], re, im);
+          xr[2 * v] = make_double2(re[0], re[1]);
+          xr[2 * v + 1] = make_double2(re[2], re[3]);
+          xi[2 * v] = make_double2(im[0], im[1]);
+          xi[2 * v + 1] = make_double2(im[2], im[3]);
+        }
+      } else {
         const double w = smem[w_off];
 #pragma unroll
         for (int u = 0; u < QB; ++u) {
