@@ -1009,13 +1009,10 @@ bool su2_applies(const sp_ctx* ctx, const SliceJob& job) {
   }();
   if (!enabled) return false;
   const bool su2 = ctx->su2_terms && job.coef_alt;
-  // u(2): complex128, midpoint with 2 or 4 controls (the TMA lanes; the
-  // cp.async forms measured slower than lane_small_kernel<2,1>, and complex64
-  // keeps the reference's float32 sequence of lane_f32_kernel<2>: the u(2)
-  // float32 pairs land 1-3x outside the complex64 gate)
-  const bool u2 = u2_enabled && ctx->u2_terms && ctx->bits == 64 &&
-                  job.mode == SP_MODE_MIDPOINT && (job.n_ctrl == 2 || job.n_ctrl == 4) &&
-                  job.m <= SP_MAX_ORDER;
+  // u(2): complex128 (complex64 keeps the reference's float32 sequence of
+  // lane_f32_kernel<2>: the u(2) float32 pairs land 1-3x outside the
+  // complex64 gate)
+  const bool u2 = u2_enabled && ctx->u2_terms && ctx->bits == 64 && job.m <= SP_MAX_ORDER;
   if (!su2 && !u2) return false;
   if (job.mode > SP_MODE_MAGNUS) return false;  // Gauss-Legendre: general d = 2 kernel
   if (!(job.phase[0] == 1.0 && job.phase[1] == 0.0)) return false;

@@ -428,13 +428,13 @@ struct U2Alg {
   __device__ static E slice(const Su2Job& job, int m, const double* cur, double (&r1)[NCC]) {
     return u2_u<R, MODE, NCC, MC>(job, m, cur, r1);
   }
-  // two midpoint slices in lockstep (TMA rounds)
-  template <int NCC, int MC>
+  // two consecutive slices in lockstep (TMA rounds, cp.async ring pairs)
+  template <int MODE, int NCC, int MC>
   __device__ static void slice2(const Su2Job& job, int m, const double* c0, const double* c1,
                                 double (&r1)[NCC], E& u0, E& u1) {
     const double* const c[2] = {c0, c1};
     E U[2];
-    u2_u_multi<R, SP_MODE_MIDPOINT, NCC, MC, 2>(job, m, c, r1, U);
+    u2_u_multi<R, MODE, NCC, MC, 2>(job, m, c, r1, U);
     u0 = U[0];
     u1 = U[1];
   }
@@ -637,6 +637,8 @@ __global__ void __launch_bounds__(Su2Shape<MODE, NCC, R, U2>::TPB, 1)
 #pragma unroll
   for (int j = 0; j < DS - 1; ++j) issue(j, j);
 
+  double prev[K];  // u(2): the held row of a slice pair
+  bool held = false;
   for (int k0 = 0; k0 < cnt; k0 += DS) {
 #pragma unroll
     for (int j = 0; j < DS; ++j) {
@@ -656,9 +658,37 @@ __global__ void __launch_bounds__(Su2Shape<MODE, NCC, R, U2>::TPB, 1)
         }
 #pragma unroll
         for (int q = 0; q < K; ++q) bad |= amp_bad(cur[q]);
-        V = A::mul(A::template slice<MODE, NCC, MC>(job, m, cur, r1), V);
-        if (PFX && job.prefix_out != nullptr) A::store(job.prefix_out, s0 + k0 + j, V);
+        if constexpr (A::PAIRS) {
+          // u(2): a slice's row is held until the next one arrives, then the
+          // two Clenshaw recurrences run in lockstep (two dependency chains)
+          if (!held) {
+#pragma unroll
+            for (int q = 0; q < K; ++q) prev[q] = cur[q];
+            held = true;
+          } else {
+            typename A::E u0, u1;
+            A::template slice2<MODE, NCC, MC>(job, m, prev, cur, r1, u0, u1);
+            if (PFX && job.prefix_out != nullptr) {
+              V = A::mul(u0, V);
+              A::store(job.prefix_out, s0 + k0 + j - 1, V);
+              V = A::mul(u1, V);
+              A::store(job.prefix_out, s0 + k0 + j, V);
+            } else {
+              V = A::mul(A::mul(u1, u0), V);
+            }
+            held = false;
+          }
+        } else {
+          V = A::mul(A::template slice<MODE, NCC, MC>(job, m, cur, r1), V);
+          if (PFX && job.prefix_out != nullptr) A::store(job.prefix_out, s0 + k0 + j, V);
+        }
       }
+    }
+  }
+  if constexpr (A::PAIRS) {
+    if (held) {  // odd slice count: the last one alone
+      V = A::mul(A::template slice<MODE, NCC, MC>(job, m, prev, r1), V);
+      if (PFX && job.prefix_out != nullptr) A::store(job.prefix_out, s1 - 1, V);
     }
   }
   su2_finish<A, NCC, PFX>(job, V, bad, MODE == SP_MODE_MIDPOINT ? s0 : 2 * s0,
@@ -803,7 +833,7 @@ __global__ void __launch_bounds__(Su2Tma<NCC, C>::TPB, 1)
 #pragma unroll
           for (int q = 0; q < NCC; ++q) bad |= amp_bad(c0[q]) | amp_bad(c1[q]);
           E u0, u1;
-          A::template slice2<NCC, MC>(job, m, c0, c1, r1, u0, u1);
+          A::template slice2<SP_MODE_MIDPOINT, NCC, MC>(job, m, c0, c1, r1, u0, u1);
           V = A::mul(A::mul(u1, u0), V);
         }
       } else {

@@ -35,11 +35,16 @@ Su2Kernel su2_pick(int m) {
   Su2Kernel k;
   k.smem = S::SMEM_PER_THREAD * S::TPB;
   k.max_block = S::TPB;
-  switch (m) {
-    case 3: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 3, R, PFX, U2>; break;
-    case 5: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 5, R, PFX, U2>; break;
-    case 7: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 7, R, PFX, U2>; break;
-    default: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 0, R, PFX, U2>;
+  if constexpr (U2) {  // the random systems' fp64 midpoint order compiled in
+    k.fn = m == 13 ? (const void*)lane_su2_kernel<MODE, NCC, 13, R, PFX, true>
+                   : (const void*)lane_su2_kernel<MODE, NCC, 0, R, PFX, true>;
+  } else {
+    switch (m) {
+      case 3: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 3, R, PFX>; break;
+      case 5: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 5, R, PFX>; break;
+      case 7: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 7, R, PFX>; break;
+      default: k.fn = (const void*)lane_su2_kernel<MODE, NCC, 0, R, PFX>;
+    }
   }
   return k;
 }
@@ -52,17 +57,16 @@ Su2Kernel su2_pick_tma(int m) {
   k.max_block = G::TPB;
   k.tma = true;
   k.rows = C;
-  if constexpr (U2) {  // the random systems' fp64 / fp32 plan orders compiled in
+  if constexpr (U2) {  // the random systems' fp64 midpoint order compiled in
     k.fn = m == 13 ? (const void*)lane_su2_tma_kernel<NCC, 13, C, R, PFX, true>
-           : m == 7 ? (const void*)lane_su2_tma_kernel<NCC, 7, C, R, PFX, true>
-                    : (const void*)lane_su2_tma_kernel<NCC, 0, C, R, PFX, true>;
-    return k;
-  }
-  switch (m) {
-    case 3: k.fn = (const void*)lane_su2_tma_kernel<NCC, 3, C, R, PFX>; break;
-    case 5: k.fn = (const void*)lane_su2_tma_kernel<NCC, 5, C, R, PFX>; break;
-    case 7: k.fn = (const void*)lane_su2_tma_kernel<NCC, 7, C, R, PFX>; break;
-    default: k.fn = (const void*)lane_su2_tma_kernel<NCC, 0, C, R, PFX>;
+                   : (const void*)lane_su2_tma_kernel<NCC, 0, C, R, PFX, true>;
+  } else {
+    switch (m) {
+      case 3: k.fn = (const void*)lane_su2_tma_kernel<NCC, 3, C, R, PFX>; break;
+      case 5: k.fn = (const void*)lane_su2_tma_kernel<NCC, 5, C, R, PFX>; break;
+      case 7: k.fn = (const void*)lane_su2_tma_kernel<NCC, 7, C, R, PFX>; break;
+      default: k.fn = (const void*)lane_su2_tma_kernel<NCC, 0, C, R, PFX>;
+    }
   }
   return k;
 }
@@ -104,11 +108,9 @@ Su2Kernel su2_kernel_for_t(const Su2Job& job) {
 // u(2) systems (job.u2) on the 2 x 2 complex algebra: the TMA lanes only
 // (engine.cu su2_applies routes the rest to lane_small_kernel<2,1>)
 template <bool PFX>
-Su2Kernel u2_kernel_for(const Su2Job& job) {  // complex128, midpoint, 2 / 4 controls
-  if (job.mode != SP_MODE_MIDPOINT || job.arith32) return {};
-  if (job.n_ctrl == 2) return su2_pick_tma<2, 8, double, PFX, true>(job.m);
-  if (job.n_ctrl == 4) return su2_pick_tma<4, 4, double, PFX, true>(job.m);
-  return {};
+Su2Kernel u2_kernel_for(const Su2Job& job) {  // complex128
+  if (job.arith32) return {};
+  return su2_kernel_for_t<double, PFX, true>(job);
 }
 
 Su2Kernel su2_kernel_for(const Su2Job& job) {

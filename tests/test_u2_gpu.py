@@ -1,17 +1,16 @@
 """GPU parity of the u(2) lanes (kernels_su2.cuh on the 2 x 2 complex algebra).
 
 d = 2 complex128 systems whose terms are bitwise Hermitian but not all
-traceless (a random 2 x 2 system, a detuned qubit), midpoint with 2 or 4
-controls, run on the su(2) family's TMA lanes — amplitude rows streamed by
-cp.async.bulk.tensor, two slices' complex Clenshaw pairs (Z = z0 I + Z') in
-lockstep, 2 x 2 complex running products, the same ordered CTA tree and
-fused tail.  Other d = 2 configurations stay on lane_small_kernel<2,1>
-(measured faster there) and complex64 on the reference's float32 sequence
-(lane_f32_kernel<2>).  Same gate as every other family:
-rel-Frobenius <= max(1e-12, 4 eps_self) against the oracle, over the control
-counts, the compiled (7, 13) and runtime series orders, slice counts with
-partial last lanes, the sequential reduction and equiprop_all (lane mode),
-and the amplitude-bound contract.
+traceless (a random 2 x 2 system, a detuned qubit) run on the su(2) family's
+lanes — TMA row stream for midpoint with 2 / 4 controls, the cp.async ring
+otherwise — with two slices' complex Clenshaw pairs (Z = z0 I + Z') in
+lockstep, 2 x 2 complex running products, the same ordered CTA tree and fused
+tail.  complex64 keeps the reference's float32 sequence (lane_f32_kernel<2>).
+Same gate as every other family: rel-Frobenius <= max(1e-12,
+4 eps_self) against the oracle, over every mode, control counts 1..4, the
+compiled (13) and runtime series orders, slice counts with odd tails and
+partial last lanes, the sequential reduction and equiprop_all (lane mode), and
+the amplitude-bound contract.
 """
 
 import numpy as np
@@ -49,15 +48,12 @@ def _gate(h0, hs, values, dt, mode, precision="fp64", reduction="pairwise", m_ma
 
 @pytest.mark.parametrize("mode", ["midpoint", "simpson", "magnus"])
 @pytest.mark.parametrize("n_ctrl", [1, 2, 3, 4])
-def test_random_d2_systems_every_mode(mode, n_ctrl):
-    """The routing: u(2) lanes for midpoint with 2 / 4 controls, the general
-    d = 2 kernel otherwise — both held to the gate."""
+def test_random_u2_systems_every_mode(mode, n_ctrl):
     slices = 3001
     pts = slices if mode == "midpoint" else 2 * slices + 1
     h0, hs, values, dt = random_inputs(2, n_ctrl, pts, 500 + n_ctrl)
     kernel = _gate(h0, hs, values, dt, mode, label=f"N={n_ctrl}")
-    u2 = mode == "midpoint" and n_ctrl in (2, 4)
-    assert kernel == "lane_u2_kernel" if u2 else kernel.startswith("lane_small_kernel")
+    assert kernel == "lane_u2_kernel"
 
 
 @pytest.mark.parametrize("n_ctrl", [2, 4])
@@ -76,24 +72,27 @@ def test_series_orders(beta, n_ctrl):
     _gate(h0, hs, values, dt, "midpoint", label=f"beta={beta} N={n_ctrl}")
 
 
+@pytest.mark.parametrize("n_ctrl", [1, 2])
 @pytest.mark.parametrize("slices", [1, 2, 7, 33, 1001, 75777, 300001])
-def test_slice_counts(slices):
+def test_slice_counts(slices, n_ctrl):
     """1 (one lane) .. more slices than lanes x round size (partial last lane
-    on direct loads, short warps)."""
-    h0, hs, values, dt = random_inputs(2, 2, slices, 9)
-    _gate(h0, hs, values, dt, "midpoint", label="slices")
+    on direct loads, short warps, odd pair tails)."""
+    h0, hs, values, dt = random_inputs(2, n_ctrl, slices, 9)
+    _gate(h0, hs, values, dt, "midpoint", label=f"slices N={n_ctrl}")
 
 
-@pytest.mark.parametrize("n_ctrl", [2, 4])
-def test_sequential_and_cumulative(n_ctrl):
+@pytest.mark.parametrize("mode,n_ctrl", [("midpoint", 2), ("midpoint", 3), ("simpson", 2),
+                                         ("magnus", 4)])
+def test_sequential_and_cumulative(mode, n_ctrl):
     """Lane mode: the sequential total and every cumulative propagator."""
-    mode = "midpoint"
-    slices = pts = 5001
+    slices = 5001
+    pts = slices if mode == "midpoint" else 2 * slices + 1
     h0, hs, values, dt = random_inputs(2, n_ctrl, pts, 71)
     kernel = _gate(h0, hs, values, dt, mode, reduction="sequential", label="sequential")
     assert kernel == "lane_u2_kernel"
     with sp.create() as ctx:
-        ctx.set_hamiltonian(sp.ControlSystem(h0, hs), quadrature=mode)
+        ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                            quadrature=None if mode == "magnus" else mode)
         cum = ctx.equiprop_all(sp.ControlAmplitudes(values, dt))
     u, _ = oracle.slice_propagators(h0, hs, values, dt, mode=mode)
     ref_all = oracle.cumulative(u)

@@ -1,6 +1,6 @@
 """A/B kernel timing of random systems under environment variants.
 
-    python tools/env_ab.py "d,n_ctrl,slices,prec[,algo];..." "" "SP_D64_GROUP=2" ...
+    python tools/env_ab.py "d,n_ctrl,slices,prec[,algo[,mode]];..." "" "SP_D64_GROUP=2" ...
 
 Each variant (space-separated VAR=VALUE list; "" = defaults) runs in its own
 process; per case: kernel name, best of 10 main-kernel times (CUDA events in
@@ -20,11 +20,15 @@ from cases import random_inputs
 out = {}
 for case in CASES.split(";"):
     d, nc, n, prec, *rest = case.split(",")
-    h0, hs, v, dt = random_inputs(int(d), int(nc), int(n), 1)
+    mode = rest[1] if len(rest) > 1 else "midpoint"
+    pts = int(n) if mode == "midpoint" else 2 * int(n) + 1
+    h0, hs, v, dt = random_inputs(int(d), int(nc), pts, 1)
     ctx = sp.create(precision=prec)
-    if rest:
+    if rest and rest[0] != "auto":
         ctx.set_algorithm(rest[0])
-    ctx.set_hamiltonian(sp.ControlSystem(h0, hs)); ctx.set_profiling(True)
+    ctx.set_hamiltonian(sp.ControlSystem(h0, hs), magnus=mode == "magnus",
+                        quadrature=None if mode == "magnus" else mode)
+    ctx.set_profiling(True)
     amps = sp.ControlAmplitudes(v, dt)
     r = ctx.equiprop(amps)
     best, flops = 1e9, 0.0
