@@ -34,6 +34,12 @@
 // Amplitude bounds (|c| <= 1, NaN) are accumulated into a predicate; a lane
 // that saw an offender rescans its own rows for the first one (row-major)
 // and records it in the epoch slot (SliceJob::viol) — no branch per slice.
+//
+// u(2) systems (complex128 d = 2 terms with a trace part: Z = z0 I + Z')
+// run on the same lanes with the algebra as a template parameter (QuatAlg /
+// U2Alg): complex Clenshaw pairs (lane_small_kernel<2,1>'s d = 2 sequence)
+// for two slices in lockstep, 2 x 2 complex running products (32 FP64
+// operations), the same ordered CTA tree and fused tail.
 #pragma once
 
 #include <cuda.h>
