@@ -487,6 +487,21 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     for (int e = 0; e < NE; ++e)
       o[(size_t)row_of(e) * D + col0 + col_of(e)] = make_double2(pr[e], pi[e]);
   }
+  // the exchange buffers are dead: once every CTA of the group is past its
+  // last product GEMM, each drops the lines of its own column chunks from L2
+  // (discard: no write-back to HBM, and the evict_last lines of this call do
+  // not outlive it)
+  if (s0 < s1) {
+    gsync();
+    constexpr int RUN = KBC * 3 * 64;  // doubles of one strip's column chunk
+    for (int i = threadIdx.x; i < 3 * C::S * (RUN / 16); i += C::THREADS) {
+      const int buf = i / (C::S * (RUN / 16)), rem = i % (C::S * (RUN / 16));
+      const int strip = rem / (RUN / 16), line = rem % (RUN / 16);
+      const double* a = gx + (size_t)buf * C::XDBL +
+                        ((size_t)(strip * KB + cb * KBC) * 3) * 64 + 16 * line;
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+    }
+  }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();

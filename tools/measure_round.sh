@@ -4,10 +4,12 @@
 # captures of the C4, c1m (su2) and D64 lane kernels.  Outputs: gpurun_out/m_*.
 set -x
 P=${1:-m}
-timeout 1200 python -m pytest tests -m gpu -q -rf > gpurun_out/${P}_tests.log 2>&1
-timeout 900 python bench.py > gpurun_out/${P}_bench.log 2>&1
+# full-size DRAM traffic first: a fresh process on a fresh box (the L2 state left by
+# earlier processes changes the write-back / re-read traffic of the exchange buffers)
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:lane_ps3g -c 1 --csv --log-file gpurun_out/${P}_traffic_c4.csv python tools/ncu_target.py --workload c4 --slices 1000000 --repeat 1 > /dev/null 2>&1
 timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:lane_su2 -c 1 --csv --log-file gpurun_out/${P}_traffic_c1m.csv python tools/ncu_target.py --workload c1m --slices 1000000 --repeat 1 > /dev/null 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -rf > gpurun_out/${P}_tests.log 2>&1
+timeout 900 python bench.py > gpurun_out/${P}_bench.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${P}_launches_c4.csv python bench.py --steps 1 --warmup 3 --secondary '' --no-cpu > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:lane_ps3g -c 1 -o gpurun_out/${P}_c4_full python tools/ncu_target.py --workload c4 --slices 2000 --repeat 1 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:lane_su2 -c 1 -o gpurun_out/${P}_c1m_full python tools/ncu_target.py --workload c1m --slices 1000000 --repeat 1 > /dev/null 2>&1
