@@ -412,16 +412,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     // also ends every warp's last power GEMM, which read bo(pb))
     garrive();
     int pc = 0;
-    {
-      double qr[NE], qi[NE];
-      load_Q(r - 1, qr, qi);
-      write_B(bo(pc), qr, qi, (r - 1 == 1) ? 0.5 : 1.0);
-    }
-    gwait();  // everybody's 2y published (and done reading 2X); b_{r-1} staged
-    first_frags(gy);
-    PH(3);
-    // ---- Clenshaw in y
-    for (int j = r - 2; j >= 0; --j) {
+    // Clenshaw step j's accumulator start Q_j - b_{j+2} (own positions: TMEM
+    // and the owner's entries of bo(pc^1), which nobody writes before step
+    // j's GEMM is over)
+    auto clen_init = [&](int j) {
       load_Q(j, accR, accI);
       if (j + 2 <= r - 1) {
         const int o = bo(pc ^ 1);
@@ -432,13 +426,31 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           accI[e] -= smem[o + bfrag3_index<C>(rr, n, 1)];
         }
       }
+    };
+    {
+      double qr[NE], qi[NE];
+      load_Q(r - 1, qr, qi);
+      write_B(bo(pc), qr, qi, (r - 1 == 1) ? 0.5 : 1.0);
+    }
+    // EARLY (D128, measured +0.9 %; D256 -2 %): each Clenshaw step's start
+    // is formed before the barrier that ends the previous step, so a warp's
+    // wait for the slowest warp covers its TMEM / shared-memory round trips
+    constexpr bool EARLY = C::D == 128;
+    if (EARLY && r >= 2) clen_init(r - 2);  // (TMEM only) while the group arrives
+    gwait();  // everybody's 2y published (and done reading 2X); b_{r-1} staged
+    first_frags(gy);
+    PH(3);
+    // ---- Clenshaw in y
+    for (int j = r - 2; j >= 0; --j) {
+      if (!EARLY) clen_init(j);
       step(gy, j >= 1 ? gy : nullptr, bo(pc), accR, accI);
       if (j >= 1) {
-        // b_j overwrites b_{j+2} at own positions only (read above by the
-        // owner); every warp finished reading bo(pc^1) as the previous
+        // b_j overwrites b_{j+2} at own positions only (read by the owner in
+        // clen_init); every warp finished reading bo(pc^1) as the previous
         // step's B operand before the barrier that ended that step
         write_B(bo(pc ^ 1), accR, accI, (j == 1) ? 0.5 : 1.0);
         pc ^= 1;
+        if (EARLY) clen_init(j - 1);  // b_{j+1}'s own entries: B operand still being read
         __syncthreads();
       }
     }
